@@ -1,0 +1,185 @@
+/*
+ * radix_b200.h — C ABI of the B200-native RadixMLP hot path.
+ *
+ * Every entry point takes raw device pointers, plain integer sizes and a
+ * cudaStream_t passed as `void*` (NULL = legacy default stream), is
+ * stream-ordered, re-entrant, keeps no global state beyond cached device
+ * attributes, and returns an rdx_status.  Errors that can only be detected
+ * on the device (index out of range, hash-verification exhaustion, invalid
+ * offsets) are reported through a caller-owned device status word so the
+ * launch never needs a host synchronisation.
+ *
+ * Reference interfaces replaced (paths relative to the reference checkout):
+ *   rdx_plan_build        <- radix_compact.trie.build_plan / _build_indices
+ *                            (pkg/src/radix_compact/trie.py:73-148) and the
+ *                            binding radix_bindings.compute_plan
+ *                            (pkg/bindings/src/radix_bindings/__init__.py:57-69)
+ *   rdx_gather_rows       <- radix_compact.ops.gather_rows / scatter_rows
+ *                            (pkg/src/radix_compact/ops.py:50-66) and the
+ *                            bindings gather_rows / scatter_rows (…:72-89)
+ *   rdx_embed_rmsnorm     <- model.py:329,341 (token gather + embedding rows)
+ *                            fused with the layer-0 rmsnorm (model.py:147-152,349)
+ *   rdx_rmsnorm_rows      <- rmsnorm (model.py:147-152) at model.py:392,404
+ *   rdx_rope_table        <- _rope_tables (model.py:165-172) on compact positions
+ *   rdx_gemm              <- _mm (model.py:131-144) for q/k/v/o, gate/up/down,
+ *                            lm_head, with the fused epilogues of
+ *                            model.py:356-366 (q/k norm + RoPE), 387-389 (o-proj
+ *                            + residual), 394-397 (SwiGLU), 397-399 (down +
+ *                            residual)
+ *   rdx_rerank_scores     <- last-token scoring contract (no reference
+ *                            counterpart)
+ */
+#ifndef RADIX_B200_H
+#define RADIX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  One code per reference exception class that can arise on
+ * this path (pkg/src/radix_compact/errors.py:8-87); the Python shim maps each
+ * code back to the class of the same name. */
+typedef enum rdx_status {
+  RDX_OK = 0,
+  RDX_ERR_MISMATCHED_LENGTHS = 1,    /* errors.py:15  MismatchedLengths  */
+  RDX_ERR_NON_MONOTONE_OFFSETS = 2,  /* errors.py:19  NonMonotoneOffsets */
+  RDX_ERR_BOUNDARY_MISMATCH = 3,     /* errors.py:23  BoundaryMismatch   */
+  RDX_ERR_OVERFLOW_ID = 4,           /* errors.py:27  OverflowId         */
+  RDX_ERR_CAPACITY_EXCEEDED = 5,     /* errors.py:34  CapacityExceeded   */
+  RDX_ERR_EMPTY_PLAN = 6,            /* errors.py:38  EmptyPlan          */
+  RDX_ERR_INDEX_OUT_OF_RANGE = 7,    /* errors.py:45  IndexOutOfRange    */
+  RDX_ERR_SHAPE_MISMATCH = 8,        /* errors.py:49  ShapeMismatch      */
+  RDX_ERR_PLAN_BATCH_MISMATCH = 9,   /* errors.py:60  PlanBatchMismatch  */
+  RDX_ERR_ODD_HEAD_DIM = 10,         /* errors.py:56  OddHeadDim         */
+  RDX_ERR_HASH_RETRIES = 11,         /* GPU planner: every hash seed collided */
+  RDX_ERR_INVALID_ARGUMENT = 12,
+  RDX_ERR_UNSUPPORTED = 13,
+  RDX_ERR_CUDA = 100
+} rdx_status;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int rdx_version(void);
+/* Stable name of a status code ("RDX_OK", "IndexOutOfRange", …). */
+const char* rdx_status_name(int status);
+/* Last CUDA error string recorded by a failing call on this thread. */
+const char* rdx_last_cuda_error(void);
+
+/* ---------------------------------------------------------------------
+ * Index build (the prefix-trie planner), bit-exact to trie.build_plan.
+ *
+ * Inputs (device): tok[N], pos[N] (u32), cu[B+1] (i64, validated on device
+ * with the reference's precedence: BoundaryMismatch(start) ->
+ * NonMonotoneOffsets(decrease) -> NonMonotoneOffsets(empty, unless
+ * RDX_PLAN_ALLOW_EMPTY) -> BoundaryMismatch(end), ragged.py:68-102).
+ * Outputs (device, caller-allocated worst case):
+ *   gather_out[N]   first N' entries valid (compact -> original)
+ *   scatter_out[N]  original -> compact
+ *   cpos_out[N]     first N' entries valid (positions of representatives)
+ *   cu_q_out[B+1]   i32 offsets of the per-sequence compact suffixes
+ *                   (compact rows of sequence s are [cu_q[s], cu_q[s+1]))
+ *   lcp_out[B]      i32 shared-prefix length of each sequence (may be NULL)
+ *   info_out[4]     u32: [0]=N', [1]=status (rdx_status), [2]=hash attempts
+ *                   used, [3]=reserved
+ * scratch: at least rdx_plan_scratch_bytes(N, B) bytes of device memory.
+ * --------------------------------------------------------------------- */
+#define RDX_PLAN_ALLOW_EMPTY 0x1u
+
+size_t rdx_plan_scratch_bytes(int64_t n_tokens, int64_t n_seqs);
+int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const int64_t* cu,
+                   int64_t n_seqs, int64_t n_tokens, uint32_t flags,
+                   uint32_t* gather_out, uint32_t* scatter_out, uint32_t* cpos_out,
+                   int32_t* cu_q_out, int32_t* lcp_out, uint32_t* info_out,
+                   void* scratch, size_t scratch_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Row gather / scatter: dst[j, :] = src[idx[j], :] as a bit-exact byte copy
+ * (scatter_rows is the same call with the scatter map, ops.py:64-66).
+ * row_bytes is the payload per row; ld_* are row strides in bytes.  An index
+ * >= src_rows sets *err_flag = RDX_ERR_INDEX_OUT_OF_RANGE and zero-fills the
+ * destination row (err_flag may be NULL to skip reporting).
+ * --------------------------------------------------------------------- */
+int rdx_gather_rows(const void* src, int64_t src_rows, int64_t ld_src_bytes,
+                    const uint32_t* idx, int64_t n_idx, void* dst,
+                    int64_t ld_dst_bytes, int64_t row_bytes, uint32_t* err_flag,
+                    void* stream);
+
+/* ---------------------------------------------------------------------
+ * Compact embedding gather fused with RMSNorm:
+ *   t      = tok[gather[j]] (or tok[j] when gather == NULL)
+ *   h[j]   = embed[t, :]                       (fp32 residual stream)
+ *   hn[j]  = bf16(h[j] / rms(h[j]) * w)        (input of the QKV GEMM)
+ * embed is bf16 [vocab, d].  Out-of-range tokens set *err_flag.
+ * --------------------------------------------------------------------- */
+int rdx_embed_rmsnorm(const uint32_t* tok, const uint32_t* gather, int64_t n_rows,
+                      const void* embed_bf16, int64_t vocab, int64_t d,
+                      const float* norm_w, float eps, float* h_out, void* hn_bf16_out,
+                      uint32_t* err_flag, void* stream);
+
+/* RMSNorm of selected fp32 rows: out[j] = bf16(x[rows[j]] / rms * w)
+ * (rows == NULL selects row j). */
+int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t n_rows,
+                     int64_t d, const float* w, float eps, void* out_bf16, int64_t ld_out,
+                     void* stream);
+
+/* RoPE table for compact rows: table[j][i] = (cos, sin)(pos[j] * theta^(-2i/hd))
+ * for i < hd/2, computed in fp64 and rounded to fp32 (model.py:165-172). */
+int rdx_rope_table(const uint32_t* pos, int64_t n_rows, int32_t head_dim, double theta,
+                   float* table_out, void* stream);
+
+/* ---------------------------------------------------------------------
+ * tcgen05/TMEM GEMM on sm_100a: acc[m, n] = sum_k A[m, k] * B[n, k]
+ * (A [M, K] bf16 row-major = activations, B [N, K] bf16 row-major = weight
+ * in the reference's [out, in] layout, model.py:107-116), fp32 accumulate in
+ * TMEM, persistent warp-specialised kernel, fused epilogue selected by `epi`.
+ * Each output row depends only on its own input row (no split-K, fixed tile
+ * shape), so dedup-on and dedup-off rows are bit-identical.
+ * --------------------------------------------------------------------- */
+typedef enum rdx_epilogue {
+  RDX_EPI_STORE_BF16 = 0, /* out_bf16[m, n] = bf16(acc)                              */
+  RDX_EPI_STORE_F32 = 1,  /* out_f32[m, n]  = acc                                    */
+  RDX_EPI_RESID_F32 = 2,  /* resid_f32[m, n] += acc                                  */
+  RDX_EPI_SWIGLU = 3,     /* B rows interleaved per tile: [gate(BN/2) | up(BN/2)];
+                             out_bf16[m, n/2] = bf16(silu(g) * u)                    */
+  RDX_EPI_QKV = 4         /* per-head RMSNorm of q/k heads (q_norm/k_norm weights)
+                             + rotate-half RoPE from rope_table, v passthrough,
+                             bf16 store (model.py:356-366)                           */
+} rdx_epilogue;
+
+typedef struct rdx_gemm_args {
+  const void* a;       /* bf16 [M, lda] */
+  const void* b;       /* bf16 [N, ldb] */
+  int64_t m, n, k;
+  int64_t lda, ldb;    /* elements */
+  int32_t epi;         /* rdx_epilogue */
+  int32_t block_n;     /* 0 = auto, else 128 or 256 */
+  void* out;           /* bf16 or f32 output / residual */
+  int64_t ldo;         /* elements */
+  /* RDX_EPI_QKV */
+  const float* q_norm_w;   /* [head_dim] */
+  const float* k_norm_w;   /* [head_dim] */
+  const float* rope_table; /* [M, head_dim/2, 2] (cos, sin) */
+  int32_t head_dim, q_heads, kv_heads;
+  float eps;
+} rdx_gemm_args;
+
+int rdx_gemm(const rdx_gemm_args* args, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Reranker scores from last-token logits (fp32 [B, ld]):
+ *   score[b] = sigmoid(logits[b, yes_id] - logits[b, no_id])
+ * (= softmax([no, yes])[yes], the Qwen3-reranker read-out).
+ * --------------------------------------------------------------------- */
+int rdx_rerank_scores(const float* logits, int64_t n_rows, int64_t ld, int64_t yes_id,
+                      int64_t no_id, float* scores_out, void* stream);
+
+/* Number of SMs of the current device (cached). */
+int rdx_num_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RADIX_B200_H */

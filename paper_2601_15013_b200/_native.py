@@ -1,0 +1,148 @@
+"""ctypes binding of the sm_100a C-ABI library (include/radix_b200.h).
+
+The library is built in-tree (``python -m paper_2601_15013_b200.build`` or
+``__graft_entry__.build()``) into ``paper_2601_15013_b200/_rdx.so``.  There is
+no fallback: :func:`lib` raises :class:`NativeLibraryError` when the shared
+object is missing or no CUDA device is visible, and every call's status code
+is turned into the reference exception of the same name.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import NativeLibraryError, raise_for_status
+
+SO_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_rdx.so")
+
+# Every symbol include/radix_b200.h declares (tests check the export list).
+EXPORTS = (
+    "rdx_version",
+    "rdx_status_name",
+    "rdx_last_cuda_error",
+    "rdx_plan_scratch_bytes",
+    "rdx_plan_build",
+    "rdx_gather_rows",
+    "rdx_embed_rmsnorm",
+    "rdx_rmsnorm_rows",
+    "rdx_rope_table",
+    "rdx_gemm",
+    "rdx_rerank_scores",
+    "rdx_num_sms",
+)
+
+RDX_PLAN_ALLOW_EMPTY = 0x1
+
+EPI_STORE_BF16 = 0
+EPI_STORE_F32 = 1
+EPI_RESID_F32 = 2
+EPI_SWIGLU = 3
+EPI_QKV = 4
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_u32 = ctypes.c_uint32
+_f32 = ctypes.c_float
+_f64 = ctypes.c_double
+
+
+class GemmArgs(ctypes.Structure):
+    """Mirror of ``rdx_gemm_args``."""
+
+    _fields_ = [
+        ("a", _vp),
+        ("b", _vp),
+        ("m", _i64),
+        ("n", _i64),
+        ("k", _i64),
+        ("lda", _i64),
+        ("ldb", _i64),
+        ("epi", _i32),
+        ("block_n", _i32),
+        ("out", _vp),
+        ("ldo", _i64),
+        ("q_norm_w", _vp),
+        ("k_norm_w", _vp),
+        ("rope_table", _vp),
+        ("head_dim", _i32),
+        ("q_heads", _i32),
+        ("kv_heads", _i32),
+        ("eps", _f32),
+    ]
+
+
+_SIGNATURES = {
+    "rdx_version": (ctypes.c_int, []),
+    "rdx_status_name": (ctypes.c_char_p, [ctypes.c_int]),
+    "rdx_last_cuda_error": (ctypes.c_char_p, []),
+    "rdx_plan_scratch_bytes": (ctypes.c_size_t, [_i64, _i64]),
+    "rdx_plan_build": (
+        ctypes.c_int,
+        [_vp, _vp, _vp, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp],
+    ),
+    "rdx_gather_rows": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _vp]),
+    "rdx_embed_rmsnorm": (
+        ctypes.c_int,
+        [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _vp, _vp, _vp],
+    ),
+    "rdx_rmsnorm_rows": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _i64, _vp]),
+    "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
+    "rdx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmArgs), _vp]),
+    "rdx_rerank_scores": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "rdx_num_sms": (ctypes.c_int, []),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = SO_PATH) -> ctypes.CDLL:
+    """dlopen the library and bind signatures (no device needed)."""
+    if not os.path.exists(path):
+        raise NativeLibraryError(
+            f"sm_100a library not built: {path} missing (run __graft_entry__.build())"
+        )
+    handle = ctypes.CDLL(path)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    return handle
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library; requires a visible CUDA device (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                import torch
+
+                if not torch.cuda.is_available():
+                    raise NativeLibraryError("no CUDA device: the RadixMLP hot path runs on sm_100a only")
+                _lib = load_library()
+    return _lib
+
+
+def check(code: int, what: str) -> None:
+    """Raise the mapped exception for a non-zero status."""
+    if code:
+        detail = ""
+        if code == 100:
+            detail = (lib().rdx_last_cuda_error() or b"").decode()
+        raise_for_status(code, what, detail)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

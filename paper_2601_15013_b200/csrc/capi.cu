@@ -1,0 +1,57 @@
+// capi.cu — status plumbing and device queries shared by every entry point.
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace rdx {
+
+static thread_local char g_last_error[256] = "";
+
+int set_cuda_error(cudaError_t e) {
+  std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", cudaGetErrorName(e),
+                cudaGetErrorString(e));
+  return RDX_ERR_CUDA;
+}
+
+int num_sms() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      return 148;
+    cached = n;
+  }
+  return cached;
+}
+
+}  // namespace rdx
+
+extern "C" int rdx_version(void) { return 100; }  // 0.1.0
+
+extern "C" const char* rdx_status_name(int status) {
+  switch (status) {
+    case RDX_OK: return "RDX_OK";
+    case RDX_ERR_MISMATCHED_LENGTHS: return "MismatchedLengths";
+    case RDX_ERR_NON_MONOTONE_OFFSETS: return "NonMonotoneOffsets";
+    case RDX_ERR_BOUNDARY_MISMATCH: return "BoundaryMismatch";
+    case RDX_ERR_OVERFLOW_ID: return "OverflowId";
+    case RDX_ERR_CAPACITY_EXCEEDED: return "CapacityExceeded";
+    case RDX_ERR_EMPTY_PLAN: return "EmptyPlan";
+    case RDX_ERR_INDEX_OUT_OF_RANGE: return "IndexOutOfRange";
+    case RDX_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+    case RDX_ERR_PLAN_BATCH_MISMATCH: return "PlanBatchMismatch";
+    case RDX_ERR_ODD_HEAD_DIM: return "OddHeadDim";
+    case RDX_ERR_HASH_RETRIES: return "HashRetriesExhausted";
+    case RDX_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+    case RDX_ERR_UNSUPPORTED: return "Unsupported";
+    case RDX_ERR_CUDA: return "CudaError";
+    default: return "UnknownStatus";
+  }
+}
+
+extern "C" const char* rdx_last_cuda_error(void) { return rdx::g_last_error; }
+
+extern "C" int rdx_num_sms(void) { return rdx::num_sms(); }

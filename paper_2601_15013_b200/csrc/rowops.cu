@@ -1,0 +1,254 @@
+// rowops.cu — HBM-bound row kernels of the RadixMLP hot path:
+//   rdx_gather_rows     gather/scatter of rows (ops.py:50-66), 16-byte vectors
+//   rdx_embed_rmsnorm   compact embedding gather + layer-0 RMSNorm (model.py:329-349)
+//   rdx_rmsnorm_rows    RMSNorm of (selected) fp32 rows (model.py:147-152)
+//   rdx_rope_table      fp64 RoPE tables on compact positions (model.py:165-172)
+//   rdx_rerank_scores   last-token reranker read-out (DESIGN.md scoring contract)
+#include "common.cuh"
+
+namespace rdx {
+namespace {
+
+__device__ __forceinline__ void report(uint32_t* err, uint32_t code) {
+  if (err) atomicCAS(err, 0u, code);
+}
+
+
+// One warp per output row; UNROLL independent vector loads in flight per lane.
+template <typename V, int UNROLL>
+__global__ void __launch_bounds__(256)
+gather_rows_kernel(const char* __restrict__ src, int64_t src_rows, int64_t ld_src,
+                   const uint32_t* __restrict__ idx, int64_t n_idx, char* __restrict__ dst,
+                   int64_t ld_dst, int64_t row_vecs, uint32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp0; j < n_idx; j += nwarps) {
+    const uint32_t r = __ldg(idx + j);
+    V* d = reinterpret_cast<V*>(dst + j * ld_dst);
+    if (static_cast<int64_t>(r) >= src_rows) {
+      V z;
+      memset(&z, 0, sizeof(V));
+      for (int64_t c = lane; c < row_vecs; c += 32) d[c] = z;
+      if (lane == 0) report(err, RDX_ERR_INDEX_OUT_OF_RANGE);
+      continue;
+    }
+    const V* s = reinterpret_cast<const V*>(src + static_cast<int64_t>(r) * ld_src);
+    for (int64_t c = lane; c < row_vecs; c += 32 * UNROLL) {
+      V tmp[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (c + u * 32 < row_vecs) tmp[u] = s[c + u * 32];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (c + u * 32 < row_vecs) d[c + u * 32] = tmp[u];
+    }
+  }
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const int4 v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+// One warp per compact row; d % 8 == 0.
+__global__ void __launch_bounds__(256)
+embed_rmsnorm_kernel(const uint32_t* __restrict__ tok, const uint32_t* __restrict__ gather,
+                     int64_t n_rows, const __nv_bfloat16* __restrict__ embed, int64_t vocab,
+                     int64_t d, const float* __restrict__ w, float eps, float* __restrict__ h,
+                     __nv_bfloat16* __restrict__ hn, uint32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp0; j < n_rows; j += nwarps) {
+    const uint32_t src = gather ? __ldg(gather + j) : static_cast<uint32_t>(j);
+    const uint32_t t = __ldg(tok + src);
+    float* hrow = h + j * d;
+    __nv_bfloat16* orow = hn + j * d;
+    if (static_cast<int64_t>(t) >= vocab) {
+      for (int64_t c = lane; c < d; c += 32) {
+        hrow[c] = 0.f;
+        orow[c] = __float2bfloat16(0.f);
+      }
+      if (lane == 0) report(err, RDX_ERR_INDEX_OUT_OF_RANGE);
+      continue;
+    }
+    const int4* erow = reinterpret_cast<const int4*>(embed + static_cast<int64_t>(t) * d);
+    float ss = 0.f;
+    for (int64_t c = lane; c < d / 8; c += 32) {
+      float f[8];
+      bf16x8_to_f32(__ldg(erow + c), f);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ss += f[i] * f[i];
+      float4* hp = reinterpret_cast<float4*>(hrow + c * 8);
+      hp[0] = make_float4(f[0], f[1], f[2], f[3]);
+      hp[1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / static_cast<float>(d) + eps);
+    for (int64_t c = lane; c < d / 8; c += 32) {
+      float f[8];
+      bf16x8_to_f32(__ldg(erow + c), f);
+      const float4* wp = reinterpret_cast<const float4*>(w + c * 8);
+      const float4 w0 = __ldg(wp), w1 = __ldg(wp + 1);
+      st_global_v4(orow + c * 8, pack_bf16x2(f[0] * inv * w0.x, f[1] * inv * w0.y),
+                   pack_bf16x2(f[2] * inv * w0.z, f[3] * inv * w0.w),
+                   pack_bf16x2(f[4] * inv * w1.x, f[5] * inv * w1.y),
+                   pack_bf16x2(f[6] * inv * w1.z, f[7] * inv * w1.w));
+    }
+  }
+}
+
+// One warp per selected row; d % 8 == 0.
+__global__ void __launch_bounds__(256)
+rmsnorm_rows_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_t* __restrict__ rows,
+                    int64_t n_rows, int64_t d, const float* __restrict__ w, float eps,
+                    __nv_bfloat16* __restrict__ out, int64_t ld_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp0; j < n_rows; j += nwarps) {
+    const int64_t r = rows ? static_cast<int64_t>(__ldg(rows + j)) : j;
+    const float4* xr = reinterpret_cast<const float4*>(x + r * ld_x);
+    float ss = 0.f;
+    for (int64_t c = lane; c < d / 4; c += 32) {
+      const float4 v = xr[c];
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / static_cast<float>(d) + eps);
+    __nv_bfloat16* orow = out + j * ld_out;
+    for (int64_t c = lane; c < d / 8; c += 32) {
+      const float4 a = xr[2 * c], b = xr[2 * c + 1];
+      const float4* wp = reinterpret_cast<const float4*>(w + c * 8);
+      const float4 w0 = __ldg(wp), w1 = __ldg(wp + 1);
+      st_global_v4(orow + c * 8, pack_bf16x2(a.x * inv * w0.x, a.y * inv * w0.y),
+                   pack_bf16x2(a.z * inv * w0.z, a.w * inv * w0.w),
+                   pack_bf16x2(b.x * inv * w1.x, b.y * inv * w1.y),
+                   pack_bf16x2(b.z * inv * w1.z, b.w * inv * w1.w));
+    }
+  }
+}
+
+__global__ void rope_table_kernel(const uint32_t* __restrict__ pos, int64_t n_rows, int half,
+                                  double theta, int head_dim, float2* __restrict__ table) {
+  const int64_t total = n_rows * half;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = t / half;
+    const int i = static_cast<int>(t - j * half);
+    const double inv_freq = pow(theta, -static_cast<double>(2 * i) / static_cast<double>(head_dim));
+    const double ang = static_cast<double>(pos[j]) * inv_freq;
+    double sn, cs;
+    sincos(ang, &sn, &cs);
+    table[t] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+  }
+}
+
+__global__ void rerank_kernel(const float* __restrict__ logits, int64_t n, int64_t ld, int64_t yes,
+                              int64_t no, float* __restrict__ out) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b < n) {
+    const float z = logits[b * ld + yes] - logits[b * ld + no];
+    out[b] = 1.f / (1.f + __expf(-z));
+  }
+}
+
+int grid_for_rows(int64_t rows, int warps_per_block) {
+  int64_t g = (rows + warps_per_block - 1) / warps_per_block;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace
+}  // namespace rdx
+
+extern "C" int rdx_gather_rows(const void* src, int64_t src_rows, int64_t ld_src_bytes,
+                               const uint32_t* idx, int64_t n_idx, void* dst, int64_t ld_dst_bytes,
+                               int64_t row_bytes, uint32_t* err_flag, void* stream) {
+  using namespace rdx;
+  if (n_idx < 0 || src_rows < 0 || row_bytes < 0) return RDX_ERR_INVALID_ARGUMENT;
+  if (n_idx == 0 || row_bytes == 0) return RDX_OK;
+  if (!src || !idx || !dst) return RDX_ERR_INVALID_ARGUMENT;
+  const int grid = grid_for_rows(n_idx, 8);
+  const uintptr_t align = reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) |
+                          static_cast<uintptr_t>(ld_src_bytes) | static_cast<uintptr_t>(ld_dst_bytes) |
+                          static_cast<uintptr_t>(row_bytes);
+  cudaStream_t st = as_stream(stream);
+  if ((align & 15) == 0) {
+    gather_rows_kernel<int4, 4><<<grid, 256, 0, st>>>(
+        static_cast<const char*>(src), src_rows, ld_src_bytes, idx, n_idx, static_cast<char*>(dst),
+        ld_dst_bytes, row_bytes / 16, err_flag);
+  } else if ((align & 3) == 0) {
+    gather_rows_kernel<uint32_t, 8><<<grid, 256, 0, st>>>(
+        static_cast<const char*>(src), src_rows, ld_src_bytes, idx, n_idx, static_cast<char*>(dst),
+        ld_dst_bytes, row_bytes / 4, err_flag);
+  } else {
+    gather_rows_kernel<uint8_t, 8><<<grid, 256, 0, st>>>(
+        static_cast<const char*>(src), src_rows, ld_src_bytes, idx, n_idx, static_cast<char*>(dst),
+        ld_dst_bytes, row_bytes, err_flag);
+  }
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}
+
+extern "C" int rdx_embed_rmsnorm(const uint32_t* tok, const uint32_t* gather, int64_t n_rows,
+                                 const void* embed_bf16, int64_t vocab, int64_t d, const float* norm_w,
+                                 float eps, float* h_out, void* hn_bf16_out, uint32_t* err_flag,
+                                 void* stream) {
+  using namespace rdx;
+  if (n_rows < 0 || d <= 0 || (d % 8) != 0) return RDX_ERR_SHAPE_MISMATCH;
+  if (n_rows == 0) return RDX_OK;
+  embed_rmsnorm_kernel<<<grid_for_rows(n_rows, 8), 256, 0, as_stream(stream)>>>(
+      tok, gather, n_rows, static_cast<const __nv_bfloat16*>(embed_bf16), vocab, d, norm_w, eps, h_out,
+      static_cast<__nv_bfloat16*>(hn_bf16_out), err_flag);
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}
+
+extern "C" int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t n_rows,
+                                int64_t d, const float* w, float eps, void* out_bf16, int64_t ld_out,
+                                void* stream) {
+  using namespace rdx;
+  if (n_rows < 0 || d <= 0 || (d % 8) != 0 || (ld_x % 4) != 0 || (ld_out % 8) != 0)
+    return RDX_ERR_SHAPE_MISMATCH;
+  if (n_rows == 0) return RDX_OK;
+  rmsnorm_rows_kernel<<<grid_for_rows(n_rows, 8), 256, 0, as_stream(stream)>>>(
+      x, ld_x, rows, n_rows, d, w, eps, static_cast<__nv_bfloat16*>(out_bf16), ld_out);
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}
+
+extern "C" int rdx_rope_table(const uint32_t* pos, int64_t n_rows, int32_t head_dim, double theta,
+                              float* table_out, void* stream) {
+  using namespace rdx;
+  if (head_dim <= 0) return RDX_ERR_SHAPE_MISMATCH;
+  if (head_dim % 2) return RDX_ERR_ODD_HEAD_DIM;
+  if (n_rows <= 0) return RDX_OK;
+  const int half = head_dim / 2;
+  int64_t total = n_rows * half;
+  int64_t g = (total + 255) / 256;
+  if (g > num_sms() * 8) g = num_sms() * 8;
+  rope_table_kernel<<<static_cast<int>(g), 256, 0, as_stream(stream)>>>(
+      pos, n_rows, half, theta, head_dim, reinterpret_cast<float2*>(table_out));
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}
+
+extern "C" int rdx_rerank_scores(const float* logits, int64_t n_rows, int64_t ld, int64_t yes_id,
+                                 int64_t no_id, float* scores_out, void* stream) {
+  using namespace rdx;
+  if (n_rows <= 0) return RDX_OK;
+  if (yes_id < 0 || no_id < 0 || yes_id >= ld || no_id >= ld) return RDX_ERR_INDEX_OUT_OF_RANGE;
+  rerank_kernel<<<static_cast<int>((n_rows + 127) / 128), 128, 0, as_stream(stream)>>>(
+      logits, n_rows, ld, yes_id, no_id, scores_out);
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}

@@ -1,0 +1,547 @@
+"""RadixMLP-wrapped Qwen3 prefill on B200 (reference: pkg/src/radix_compact/model.py).
+
+Algorithm 1 of the paper as the reference's
+``_forward_cached`` runs it (model.py:322-416): every position-wise stage
+(embedding, RMSNorms, Q/K/V/O projections, q/k norm + RoPE, SwiGLU MLP,
+residuals, LM head) runs on the N' compact rows; only attention sees the
+original ragged layout.  Here each stage is an sm_100a kernel behind the C ABI
+(include/radix_b200.h):
+
+  embed + ln1          rdx_embed_rmsnorm       (gathers tok[gather[j]])
+  QKV + q/k-norm+RoPE  rdx_gemm EPI_QKV        (tcgen05, fused epilogue)
+  attention boundary   rdx_gather_rows (scatter K/V, or Q/K/V) + FlashAttention-2
+                       varlen (library kernel, the declared boundary)
+  O-proj + residual    rdx_gemm EPI_RESID_F32
+  ln2                  rdx_rmsnorm_rows
+  gate|up + SiLU*mul   rdx_gemm EPI_SWIGLU
+  down + residual      rdx_gemm EPI_RESID_F32
+  final norm + head    rdx_rmsnorm_rows (+ last-token row select) + rdx_gemm
+
+Attention boundary modes:
+  ``attention="full"``   exactly the reference: scatter Q/K/V to N rows,
+                         attention over the original layout, gather N -> N'
+                         (model.py:368-383).
+  ``attention="suffix"`` (default) SURVEY §8f-1: compact rows of sequence s
+                         are its suffix [lcp_s, L_s), so Q stays compact
+                         (cu_seqlens_q = cu_q), only K/V are scattered, and the
+                         causal mask is bottom-right aligned.  Mathematically
+                         identical; removes the Q scatter and the gather.
+
+Numerics: weights/activations bf16, fp32 accumulation (TMEM), fp32 residual
+stream and norm statistics.  Parity vs the fp64 reference is a tolerance
+(tests/test_model_gpu.py), dedup-on vs dedup-off differs only through the
+attention kernel's row blocking.
+
+Scoring contract (no reference counterpart; SURVEY finding 5): full-vocab
+logits for all N rows are infeasible at Qwen3 scale, so ``logits="last"``
+returns the last-token logits [B, vocab] of each sequence (the reranker
+read-out); ``logits="all"`` returns the reference's [N, vocab].
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, fields
+
+import numpy as np
+
+from . import _native
+from .errors import NativeLibraryError, OddHeadDim, PlanBatchMismatch, ShapeMismatch
+from .ops import gather_rows_device
+from .plan import CompactionPlan, DevicePlan, build_plan_device, host_plan_cu_q, upload_batch
+from .ragged import RaggedBatch, validate_batch
+
+SWIGLU_UNIT = 64  # gate/up interleave unit of the SwiGLU epilogue (csrc/gemm.cu)
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """Hyper-parameters (model.py:31-67), same fields and validation."""
+
+    num_layers: int = 2
+    hidden_size: int = 256
+    intermediate_size: int = 512
+    num_heads: int = 4
+    num_kv_heads: int = 2
+    head_dim: int = 64
+    vocab_size: int = 128
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-6
+
+    def __post_init__(self):
+        if self.hidden_size != self.num_heads * self.head_dim:
+            raise ShapeMismatch("hidden_size must equal num_heads * head_dim")
+        self._check_common()
+
+    def _check_common(self):
+        if self.num_kv_heads < 1 or self.num_heads % self.num_kv_heads:
+            raise ShapeMismatch("num_heads must be divisible by num_kv_heads")
+        for name in ("num_layers", "hidden_size", "intermediate_size", "vocab_size"):
+            if getattr(self, name) < 1:
+                raise ShapeMismatch(f"{name} must be >= 1")
+
+    @property
+    def q_dim(self) -> int:
+        return self.num_heads * self.head_dim
+
+    @property
+    def kv_dim(self) -> int:
+        return self.num_kv_heads * self.head_dim
+
+    def to_json(self) -> dict:
+        return {f.name: getattr(self, f.name) for f in fields(self)}
+
+
+@dataclass(frozen=True)
+class Qwen3Config(ModelConfig):
+    """ModelConfig that admits q_dim != hidden (real Qwen3 head layouts).
+
+    The reference's check (model.py:44-45) rejects Qwen3-0.6B/4B/8B although
+    the rest of its model already handles q_dim != hidden (SURVEY finding 3).
+    """
+
+    def __post_init__(self):
+        self._check_common()
+
+
+# Public HF config.json values (SURVEY §8 notation), random-init only.
+QWEN3_PRESETS = {
+    "qwen3-0.6b": Qwen3Config(28, 1024, 3072, 16, 8, 128, 151936, 1e6, 1e-6),
+    "qwen3-4b": Qwen3Config(36, 2560, 9728, 32, 8, 128, 151936, 1e6, 1e-6),
+    "qwen3-8b": Qwen3Config(36, 4096, 12288, 32, 8, 128, 151936, 1e6, 1e-6),
+}
+# C1 of BASELINE.json: 2 layers, d=64, 4 heads
+TINY_C1 = Qwen3Config(2, 64, 192, 4, 2, 16, 1024, 10000.0, 1e-6)
+
+
+class FlopLedger:
+    """Row counters per stage (model.py:70-91), same fields and methods."""
+
+    def __init__(self):
+        self.positionwise_row_ops = 0
+        self.attention_row_ops = 0
+        self.gather_scatter_rows = 0
+        self.phases: list[tuple[str, int]] = []
+
+    def positionwise(self, name: str, rows: int) -> None:
+        self.positionwise_row_ops += rows
+        self.phases.append((name, rows))
+
+    def attention(self, rows: int) -> None:
+        self.attention_row_ops += rows
+
+    def index_copy(self, rows: int) -> None:
+        self.gather_scatter_rows += rows
+
+
+def init_params(config: ModelConfig, seed: int = 0, dtype=np.float64) -> dict:
+    """Seeded uniform[-0.05, 0.05] init, norms = 1 (model.py:94-119).
+
+    Same parameter names, shapes ([out, in]) and RNG draw order as the
+    reference, so the oracle and the GPU model see identical weights.
+    """
+    rng = np.random.default_rng(seed)
+    d, di = config.hidden_size, config.intermediate_size
+
+    def u(*shape):
+        return rng.uniform(-0.05, 0.05, size=shape).astype(dtype)
+
+    p = {"embed": u(config.vocab_size, d)}
+    for i in range(config.num_layers):
+        pre = f"layers.{i}."
+        p[pre + "ln1"] = np.ones(d, dtype=dtype)
+        p[pre + "wq"] = u(config.q_dim, d)
+        p[pre + "wk"] = u(config.kv_dim, d)
+        p[pre + "wv"] = u(config.kv_dim, d)
+        p[pre + "wo"] = u(d, config.q_dim)
+        p[pre + "q_norm"] = np.ones(config.head_dim, dtype=dtype)
+        p[pre + "k_norm"] = np.ones(config.head_dim, dtype=dtype)
+        p[pre + "ln2"] = np.ones(d, dtype=dtype)
+        p[pre + "w_gate"] = u(di, d)
+        p[pre + "w_up"] = u(di, d)
+        p[pre + "w_down"] = u(d, di)
+    p["final_norm"] = np.ones(d, dtype=dtype)
+    p["lm_head"] = u(config.vocab_size, d)
+    return p
+
+
+def padded_intermediate(config: ModelConfig) -> int:
+    return -(-config.intermediate_size // SWIGLU_UNIT) * SWIGLU_UNIT
+
+
+def _check_kernel_shapes(config: ModelConfig) -> None:
+    hd = config.head_dim
+    if hd % 2:
+        raise OddHeadDim(f"head_dim {hd} is odd")
+    if hd % 16 or hd > 128:
+        raise ShapeMismatch(f"head_dim {hd}: the fused QKV epilogue needs a multiple of 16, <= 128")
+    if config.hidden_size % 8:
+        raise ShapeMismatch("hidden_size must be a multiple of 8 (16-byte TMA rows)")
+
+
+class DeviceWeights:
+    """Kernel-ready weights on one GPU.
+
+    w_qkv  bf16 [q+2kv, d]  (wq | wk | wv stacked, model.py:352-354)
+    w_gu   bf16 [2*di_pad, d] gate/up rows interleaved in units of 64 so each
+           GEMM tile holds matching gate and up columns (EPI_SWIGLU)
+    w_down bf16 [d, di_pad] zero-padded columns
+    norms  fp32
+    """
+
+    def __init__(self, config: ModelConfig, tensors: dict):
+        self.config = config
+        self.t = tensors
+
+    @staticmethod
+    def _interleave_gate_up(gate, up, di_pad):
+        import torch
+
+        d = gate.shape[1]
+        pad = di_pad - gate.shape[0]
+        if pad:
+            z = torch.zeros(pad, d, dtype=gate.dtype, device=gate.device)
+            gate, up = torch.cat([gate, z]), torch.cat([up, z])
+        g = gate.view(di_pad // SWIGLU_UNIT, 1, SWIGLU_UNIT, d)
+        u = up.view(di_pad // SWIGLU_UNIT, 1, SWIGLU_UNIT, d)
+        return torch.cat([g, u], dim=1).reshape(2 * di_pad, d).contiguous()
+
+    @classmethod
+    def from_tensors(cls, config: ModelConfig, get, device="cuda"):
+        """Build from a callable name -> torch tensor (any float dtype, any device)."""
+        import torch
+
+        _check_kernel_shapes(config)
+        bf, f32 = torch.bfloat16, torch.float32
+        di_pad = padded_intermediate(config)
+
+        def dev(name, dtype):
+            return get(name).to(device=device, dtype=dtype).contiguous()
+
+        t = {"embed": dev("embed", bf), "final_norm": dev("final_norm", f32), "lm_head": dev("lm_head", bf)}
+        for i in range(config.num_layers):
+            pre = f"layers.{i}."
+            t[pre + "w_qkv"] = torch.cat(
+                [dev(pre + "wq", bf), dev(pre + "wk", bf), dev(pre + "wv", bf)]).contiguous()
+            t[pre + "wo"] = dev(pre + "wo", bf)
+            t[pre + "w_gu"] = cls._interleave_gate_up(dev(pre + "w_gate", bf), dev(pre + "w_up", bf), di_pad)
+            wd = dev(pre + "w_down", bf)
+            if di_pad != config.intermediate_size:
+                wd = torch.cat([wd, torch.zeros(wd.shape[0], di_pad - wd.shape[1], dtype=bf, device=device)],
+                               dim=1).contiguous()
+            t[pre + "w_down"] = wd
+            for nm in ("ln1", "ln2", "q_norm", "k_norm"):
+                t[pre + nm] = dev(pre + nm, f32)
+        return cls(config, t)
+
+    @classmethod
+    def from_params(cls, config: ModelConfig, params: dict, device="cuda"):
+        import torch
+
+        return cls.from_tensors(config, lambda n: torch.from_numpy(np.ascontiguousarray(params[n])), device)
+
+    @classmethod
+    def random(cls, config: ModelConfig, seed: int = 0, device="cuda"):
+        """On-device seeded uniform[-0.05, 0.05] init (norms = 1), for benchmarks."""
+        import torch
+
+        gen = torch.Generator(device=device)
+        gen.manual_seed(seed)
+        d, di = config.hidden_size, config.intermediate_size
+        shapes = {"embed": (config.vocab_size, d), "lm_head": (config.vocab_size, d), "final_norm": (d,)}
+        for i in range(config.num_layers):
+            pre = f"layers.{i}."
+            shapes.update({pre + "ln1": (d,), pre + "ln2": (d,), pre + "q_norm": (config.head_dim,),
+                           pre + "k_norm": (config.head_dim,), pre + "wq": (config.q_dim, d),
+                           pre + "wk": (config.kv_dim, d), pre + "wv": (config.kv_dim, d),
+                           pre + "wo": (d, config.q_dim), pre + "w_gate": (di, d), pre + "w_up": (di, d),
+                           pre + "w_down": (d, di)})
+
+        def get(name):
+            shape = shapes[name]
+            if len(shape) == 1:
+                return torch.ones(shape, dtype=torch.float32, device=device)
+            w = torch.empty(shape, dtype=torch.float32, device=device)
+            w.uniform_(-0.05, 0.05, generator=gen)
+            return w
+
+        return cls.from_tensors(config, get, device)
+
+
+@dataclass
+class DeviceBatch:
+    """A ragged batch resident on the GPU (u32 ids stored as int32)."""
+
+    tok: object
+    pos: object
+    cu: object        # int64 [B+1]
+    cu32: object      # int32 [B+1] (attention kernel)
+    cu_host: np.ndarray
+    n: int
+    b: int
+    max_len: int
+
+    @classmethod
+    def from_batch(cls, batch: RaggedBatch, device="cuda", non_blocking=False):
+        import torch
+
+        tok, pos, cu = upload_batch(batch, device)
+        cu_host = np.asarray(batch.cu_seqlens, dtype=np.int64)
+        lens = np.diff(cu_host)
+        return cls(tok, pos, cu, cu.to(torch.int32), cu_host, int(batch.num_tokens),
+                   int(batch.num_sequences), int(lens.max()) if lens.size else 0)
+
+
+@dataclass
+class _Layout:
+    m: int                 # rows computed by position-wise stages
+    n_compact: int
+    gather: object         # int32 [m] or None (identity)
+    scatter: object        # int32 [n] or None
+    positions: object      # int32 [m]
+    cu_q32: object         # int32 [B+1] compact-suffix offsets (suffix mode)
+    max_q: int
+    suffix_ok: bool
+    dedup: bool
+
+
+def _flash_varlen(q, k, v, cu_q, cu_k, max_q, max_k, scale):
+    try:
+        from flash_attn.flash_attn_interface import flash_attn_varlen_func
+    except Exception as exc:  # pragma: no cover - image always has it
+        raise NativeLibraryError(f"attention boundary kernel unavailable: {exc}") from exc
+    return flash_attn_varlen_func(q, k, v, cu_q, cu_k, max_q, max_k, dropout_p=0.0,
+                                  softmax_scale=scale, causal=True)
+
+
+class RadixQwen3:
+    """Qwen3 prefill whose position-wise work runs on the compact rows."""
+
+    def __init__(self, config: ModelConfig, weights: DeviceWeights):
+        _check_kernel_shapes(config)
+        self.config = config
+        self.w = weights
+        self.di_pad = padded_intermediate(config)
+        self.gemm_hook = None  # optional callable(name, fn) used by bench.py for per-GEMM events
+
+    # ------------------------------------------------------------ kernels
+    def _gemm(self, name, a, w, epi, out, *, m, stream, qkv=False, rope=None, layer=None):
+        cfg = self.config
+        args = _native.GemmArgs()
+        args.a = a.data_ptr()
+        args.b = w.data_ptr()
+        args.m = m
+        args.n = w.shape[0]
+        args.k = w.shape[1]
+        args.lda = a.stride(0)
+        args.ldb = w.stride(0)
+        args.epi = epi
+        args.block_n = 0
+        args.out = out.data_ptr()
+        args.ldo = out.stride(0)
+        if qkv:
+            args.q_norm_w = self.w.t[layer + "q_norm"].data_ptr()
+            args.k_norm_w = self.w.t[layer + "k_norm"].data_ptr()
+            args.rope_table = rope.data_ptr()
+            args.head_dim = cfg.head_dim
+            args.q_heads = cfg.num_heads
+            args.kv_heads = cfg.num_kv_heads
+            args.eps = cfg.norm_eps
+        lib = _native.lib()
+
+        def launch():
+            _native.check(lib.rdx_gemm(args, stream), f"rdx_gemm[{name}]")
+
+        if self.gemm_hook is not None:
+            self.gemm_hook(name, launch, m, args.n, args.k)
+        else:
+            launch()
+
+    def _rmsnorm(self, x, w, out, rows=None, n_rows=None, stream=None):
+        lib = _native.lib()
+        n_rows = x.shape[0] if n_rows is None else n_rows
+        code = lib.rdx_rmsnorm_rows(x.data_ptr(), x.stride(0), None if rows is None else rows.data_ptr(),
+                                    n_rows, x.shape[1], w.data_ptr(), self.config.norm_eps,
+                                    out.data_ptr(), out.stride(0), stream)
+        _native.check(code, "rdx_rmsnorm_rows")
+
+    # ------------------------------------------------------------ layout
+    def _layout(self, db: DeviceBatch, plan, attention: str) -> _Layout:
+        import torch
+
+        if plan is None:
+            return _Layout(db.n, db.n, None, None, db.pos, db.cu32, db.max_len, True, False)
+        if isinstance(plan, str) and plan == "auto":
+            plan = build_plan_device(db.tok, db.pos, db.cu)
+        if isinstance(plan, DevicePlan):
+            if plan.n_original != db.n or plan.scatter.shape[0] != db.n:
+                raise PlanBatchMismatch(f"plan built for {plan.n_original} tokens, batch has {db.n}")
+            return _Layout(plan.n_padded, plan.n_compact, plan.gather, plan.scatter, plan.compact_positions,
+                           plan.cu_q, plan.max_q_len, True, True)
+        if isinstance(plan, CompactionPlan):
+            if plan.n_original != db.n:
+                raise PlanBatchMismatch(f"plan built for {plan.n_original} tokens, batch has {db.n}")
+            if plan.scatter_indices.shape[0] != db.n:
+                raise PlanBatchMismatch("scatter index length disagrees with batch")
+            dev = db.tok.device
+            g = torch.from_numpy(plan.gather_indices.view(np.int32)).to(dev)
+            s = torch.from_numpy(plan.scatter_indices.view(np.int32)).to(dev)
+            p = torch.from_numpy(plan.compact_positions.view(np.int32)).to(dev)
+            cu_q = host_plan_cu_q(plan, db.cu_host) if attention == "suffix" else None
+            if cu_q is None:
+                return _Layout(plan.n_padded, plan.n_compact, g, s, p, None, 0, False, True)
+            cu_q32 = torch.from_numpy(cu_q.astype(np.int32)).to(dev)
+            max_q = int(np.diff(cu_q).max()) if cu_q.size > 1 else 0
+            return _Layout(plan.n_padded, plan.n_compact, g, s, p, cu_q32, max_q, True, True)
+        raise TypeError(f"unsupported plan type {type(plan).__name__}")
+
+    # ------------------------------------------------------------ forward
+    def prefill(self, db: DeviceBatch, plan=None, *, attention: str = "suffix", logits: str = "all",
+                ledger: FlopLedger | None = None, stream=None):
+        """Run the prefill; returns fp32 logits [N, vocab] ("all") or [B, vocab] ("last")."""
+        import torch
+
+        if attention not in ("suffix", "full"):
+            raise ValueError("attention must be 'suffix' or 'full'")
+        if logits not in ("all", "last"):
+            raise ValueError("logits must be 'all' or 'last'")
+        cfg, T = self.config, self.w.t
+        if ledger is None:
+            ledger = FlopLedger()
+        lay = self._layout(db, plan, attention)
+        use_suffix = lay.dedup and attention == "suffix" and lay.suffix_ok
+        lib = _native.lib()
+        st = _native.stream_handle(stream)
+        dev = db.tok.device
+        m, n = lay.m, db.n
+        d, hd, H, KV = cfg.hidden_size, cfg.head_dim, cfg.num_heads, cfg.num_kv_heads
+        qd, kvd = cfg.q_dim, cfg.kv_dim
+        bf = torch.bfloat16
+        if lay.dedup:
+            ledger.index_copy(m)
+
+        h = torch.empty(m, d, dtype=torch.float32, device=dev)
+        hn = torch.empty(m, d, dtype=bf, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        code = lib.rdx_embed_rmsnorm(db.tok.data_ptr(), None if lay.gather is None else lay.gather.data_ptr(),
+                                     m, T["embed"].data_ptr(), cfg.vocab_size, d,
+                                     T["layers.0.ln1"].data_ptr(), cfg.norm_eps, h.data_ptr(),
+                                     hn.data_ptr(), err.data_ptr(), st)
+        _native.check(code, "rdx_embed_rmsnorm")
+        ledger.positionwise("embed", m)
+        rope = torch.empty(m, hd // 2, 2, dtype=torch.float32, device=dev)
+        _native.check(lib.rdx_rope_table(lay.positions.data_ptr(), m, hd, float(cfg.rope_theta),
+                                         rope.data_ptr(), st), "rdx_rope_table")
+        qkv = torch.empty(m, qd + 2 * kvd, dtype=bf, device=dev)
+        act = torch.empty(m, self.di_pad, dtype=bf, device=dev)
+        scale = 1.0 / math.sqrt(hd)
+        last_rows = None
+        if logits == "last":
+            ends = db.cu[1:] - 1
+            last_rows = (lay.scatter[ends] if lay.dedup else ends).to(torch.int32).contiguous()
+
+        for i in range(cfg.num_layers):
+            pre = f"layers.{i}."
+            ledger.positionwise(f"l{i}.ln1", m)
+            self._gemm("qkv", hn, T[pre + "w_qkv"], _native.EPI_QKV, qkv, m=m, stream=st, qkv=True,
+                       rope=rope, layer=pre)
+            ledger.positionwise(f"l{i}.qkv_proj", m)
+            ledger.positionwise(f"l{i}.qk_norm_rope", m)
+            if not lay.dedup:
+                a = _flash_varlen(qkv[:, :qd].view(m, H, hd), qkv[:, qd:qd + kvd].view(m, KV, hd),
+                                  qkv[:, qd + kvd:].view(m, KV, hd), db.cu32, db.cu32, db.max_len,
+                                  db.max_len, scale)
+                ledger.attention(n)
+            elif use_suffix:
+                kv_full = gather_rows_device(qkv[:, qd:], lay.scatter, stream=stream)
+                ledger.index_copy(2 * n)
+                a = _flash_varlen(qkv[:, :qd].view(m, H, hd), kv_full[:, :kvd].view(n, KV, hd),
+                                  kv_full[:, kvd:].view(n, KV, hd), lay.cu_q32, db.cu32, max(lay.max_q, 1),
+                                  db.max_len, scale)
+                if m > lay.n_compact:
+                    a[lay.n_compact:] = 0
+                ledger.attention(lay.n_compact)
+            else:
+                qkv_full = gather_rows_device(qkv, lay.scatter, stream=stream)
+                ledger.index_copy(3 * n)
+                a_full = _flash_varlen(qkv_full[:, :qd].view(n, H, hd), qkv_full[:, qd:qd + kvd].view(n, KV, hd),
+                                       qkv_full[:, qd + kvd:].view(n, KV, hd), db.cu32, db.cu32, db.max_len,
+                                       db.max_len, scale)
+                ledger.attention(n)
+                a = gather_rows_device(a_full.view(n, qd), lay.gather, stream=stream)
+                ledger.index_copy(m)
+            a = a.reshape(m, qd)
+            self._gemm("o_proj", a, T[pre + "wo"], _native.EPI_RESID_F32, h, m=m, stream=st)
+            ledger.positionwise(f"l{i}.o_proj", m)
+            ledger.positionwise(f"l{i}.attn_residual", m)
+            self._rmsnorm(h, T[pre + "ln2"], hn, stream=st)
+            self._gemm("gate_up", hn, T[pre + "w_gu"], _native.EPI_SWIGLU, act, m=m, stream=st)
+            self._gemm("down", act, T[pre + "w_down"], _native.EPI_RESID_F32, h, m=m, stream=st)
+            ledger.positionwise(f"l{i}.mlp", m)
+            ledger.positionwise(f"l{i}.mlp_residual", m)
+            if i + 1 < cfg.num_layers:
+                self._rmsnorm(h, T[f"layers.{i + 1}.ln1"], hn, stream=st)
+
+        vocab = cfg.vocab_size
+        if logits == "last":
+            hl = torch.empty(db.b, d, dtype=bf, device=dev)
+            self._rmsnorm(h, T["final_norm"], hl, rows=last_rows, n_rows=db.b, stream=st)
+            ledger.positionwise("final_norm", db.b)
+            out = torch.empty(db.b, vocab, dtype=torch.float32, device=dev)
+            self._gemm("lm_head", hl, T["lm_head"], _native.EPI_STORE_F32, out, m=db.b, stream=st)
+            ledger.positionwise("lm_head", db.b)
+            result = out
+        else:
+            self._rmsnorm(h, T["final_norm"], hn, stream=st)
+            ledger.positionwise("final_norm", m)
+            out = torch.empty(m, vocab, dtype=torch.float32, device=dev)
+            self._gemm("lm_head", hn, T["lm_head"], _native.EPI_STORE_F32, out, m=m, stream=st)
+            ledger.positionwise("lm_head", m)
+            if lay.dedup:
+                result = gather_rows_device(out, lay.scatter, stream=stream)
+                ledger.index_copy(n)
+            else:
+                result = out
+        if int(err.item()):
+            from .errors import IndexOutOfRange
+
+            raise IndexOutOfRange("token id outside [0, vocab_size)")
+        return result
+
+
+_MODEL_CACHE: dict = {}
+
+
+def _model_for(config: ModelConfig, params) -> RadixQwen3:
+    if isinstance(params, RadixQwen3):
+        return params
+    if isinstance(params, DeviceWeights):
+        return RadixQwen3(config, params)
+    key = (id(params), config)
+    hit = _MODEL_CACHE.get(key)
+    if hit is not None and hit[0] is params:
+        return hit[1]
+    model = RadixQwen3(config, DeviceWeights.from_params(config, params))
+    _MODEL_CACHE.clear()
+    _MODEL_CACHE[key] = (params, model)
+    return model
+
+
+def forward(config: ModelConfig, params, batch: RaggedBatch, plan=None, ledger: FlopLedger | None = None,
+            *, attention: str = "suffix", logits: str = "all"):
+    """Reference-compatible entry (model.py:310-319) returning device fp32 logits.
+
+    ``params`` is the reference's numpy dict (converted once and cached), a
+    :class:`DeviceWeights` or a :class:`RadixQwen3`.  ``plan`` is None (dedup
+    off), a host :class:`CompactionPlan`, a :class:`DevicePlan` or "auto"
+    (GPU planner).
+    """
+    validate_batch(batch, allow_empty=True)
+    model = _model_for(config, params)
+    db = DeviceBatch.from_batch(batch)
+    return model.prefill(db, plan, attention=attention, logits=logits, ledger=ledger)
+
+
+def forward_scores(config: ModelConfig, params, batch: RaggedBatch, plan="auto"):
+    """Last-token logits [B, vocab] (the scoring contract), device fp32."""
+    return forward(config, params, batch, plan=plan, logits="last")

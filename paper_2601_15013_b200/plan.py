@@ -1,0 +1,275 @@
+"""Compaction plans: the GPU prefix-trie planner behind the reference API.
+
+Python surface mirrors pkg/src/radix_compact/trie.py:36-233:
+``CompactionPlan``, ``build_plan``, ``build_plan_fast_paths``,
+``build_plan_auto``, ``should_enable`` and ``pad_plan`` keep their names,
+argument meaning, outputs and exceptions.  The index computation itself runs
+on the GPU (csrc/plan_build.cu, ``rdx_plan_build``), bit-exact to the
+reference's trie; there is no CPU planner in this package.
+
+``build_plan_device`` is the hot-path entry: device-resident inputs in,
+device-resident :class:`DevicePlan` out, with a single small D2H read of
+(N', status, cu_q) so the host can size the compact buffers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from . import _native
+from .errors import CapacityExceeded, EmptyPlan, raise_for_status
+from .ragged import RaggedBatch, validate_batch
+
+
+@dataclass(frozen=True)
+class CompactionPlan:
+    """Host copy of a plan; same fields and properties as trie.py:36-70."""
+
+    gather_indices: np.ndarray
+    scatter_indices: np.ndarray
+    compact_positions: np.ndarray
+    n_original: int
+    n_compact: int
+
+    def __post_init__(self):
+        for name in ("gather_indices", "scatter_indices", "compact_positions"):
+            arr = np.ascontiguousarray(getattr(self, name), dtype=np.uint32)
+            arr.flags.writeable = False
+            object.__setattr__(self, name, arr)
+
+    @property
+    def n_padded(self) -> int:
+        return int(self.gather_indices.shape[0])
+
+    @property
+    def gamma(self) -> float:
+        return self.n_compact / self.n_original if self.n_original else 1.0
+
+    @property
+    def gamma_exact(self) -> Fraction:
+        return Fraction(self.n_compact, self.n_original) if self.n_original else Fraction(1)
+
+
+@dataclass
+class DevicePlan:
+    """Device-resident plan produced by :func:`build_plan_device`.
+
+    ``gather`` / ``compact_positions`` have exactly ``n_compact`` rows,
+    ``scatter`` has ``n_original``; all int32 views of the u32 maps.
+    ``cu_q`` (device, int32 [B+1]) delimits each sequence's compact suffix
+    (finding 2 of SURVEY.md: compact rows of sequence s are the contiguous
+    range [cu_q[s], cu_q[s+1]) ); ``cu_q_host`` is its host copy.
+    """
+
+    gather: "object"
+    scatter: "object"
+    compact_positions: "object"
+    cu_q: "object"
+    lcp: "object"
+    cu_q_host: np.ndarray
+    n_original: int
+    n_compact: int
+    attempts: int = 1
+    extras: dict = field(default_factory=dict)
+
+    @property
+    def n_padded(self) -> int:
+        return int(self.gather.shape[0])
+
+    @property
+    def gamma(self) -> float:
+        return self.n_compact / self.n_original if self.n_original else 1.0
+
+    @property
+    def max_q_len(self) -> int:
+        return int(np.diff(self.cu_q_host).max()) if self.cu_q_host.size > 1 else 0
+
+    def to_host(self) -> CompactionPlan:
+        return CompactionPlan(
+            gather_indices=self.gather.cpu().numpy().view(np.uint32),
+            scatter_indices=self.scatter.cpu().numpy().view(np.uint32),
+            compact_positions=self.compact_positions.cpu().numpy().view(np.uint32),
+            n_original=self.n_original,
+            n_compact=self.n_compact,
+        )
+
+
+class _Workspace:
+    """Grow-only per-device scratch arena for the planner."""
+
+    def __init__(self):
+        self._buf = {}
+        self._lock = threading.Lock()
+
+    def get(self, device, nbytes: int):
+        import torch
+
+        key = str(device)
+        with self._lock:
+            buf = self._buf.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+                self._buf[key] = buf
+            return buf
+
+
+_WORKSPACE = _Workspace()
+
+
+def build_plan_device(tok, pos, cu, *, allow_empty: bool = False, stream=None,
+                      n_original: int | None = None) -> DevicePlan:
+    """GPU planner on device tensors (tok/pos int32-viewed u32 [N], cu int64 [B+1]).
+
+    One cooperative kernel computes gather/scatter/compact_positions/cu_q;
+    one D2H copy of (N', status, attempts, cu_q) follows.
+    """
+    import torch
+
+    lib = _native.lib()
+    dev = tok.device
+    n = int(tok.shape[0]) if n_original is None else int(n_original)
+    b = int(cu.shape[0]) - 1
+    if n >= (1 << 32) - 1:
+        raise CapacityExceeded(f"{n} tokens exceed 32-bit index range")
+    gather = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    scatter = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    cpos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    info_cu = torch.empty(4 + b + 1, dtype=torch.int32, device=dev)
+    lcp = torch.empty(max(b, 1), dtype=torch.int32, device=dev)
+    scratch_bytes = int(lib.rdx_plan_scratch_bytes(n, b))
+    scratch = _WORKSPACE.get(dev, scratch_bytes)
+    flags = _native.RDX_PLAN_ALLOW_EMPTY if allow_empty else 0
+    st = _native.stream_handle(stream)
+    code = lib.rdx_plan_build(
+        tok.data_ptr(), pos.data_ptr(), cu.data_ptr(), b, n, flags,
+        gather.data_ptr(), scatter.data_ptr(), cpos.data_ptr(),
+        info_cu.data_ptr() + 16, lcp.data_ptr(), info_cu.data_ptr(),
+        scratch.data_ptr(), ctypes.c_size_t(scratch.numel()), st,
+    )
+    _native.check(code, "rdx_plan_build")
+    host = info_cu.cpu().numpy()  # the one synchronising read
+    n_compact, status, attempts = int(host[0]), int(host[1]), int(host[2])
+    raise_for_status(status, "rdx_plan_build")
+    return DevicePlan(
+        gather=gather[:n_compact],
+        scatter=scatter[:n],
+        compact_positions=cpos[:n_compact],
+        cu_q=info_cu[4:],
+        lcp=lcp[:b],
+        cu_q_host=host[4:].astype(np.int64),
+        n_original=n,
+        n_compact=n_compact,
+        attempts=attempts,
+    )
+
+
+def upload_batch(batch: RaggedBatch, device="cuda"):
+    """Host batch -> (tok, pos, cu) device tensors (u32 stored as int32)."""
+    import torch
+
+    _native.lib()  # fail loudly (NativeLibraryError) before touching CUDA
+    tok = torch.from_numpy(np.array(batch.token_ids, dtype=np.uint32).view(np.int32))
+    pos = torch.from_numpy(np.array(batch.position_ids, dtype=np.uint32).view(np.int32))
+    cu = torch.from_numpy(np.array(batch.cu_seqlens, dtype=np.int64))
+    return tok.to(device), pos.to(device), cu.to(device)
+
+
+def build_plan(batch: RaggedBatch, allow_empty: bool = False) -> CompactionPlan:
+    """Reference ``build_plan`` (trie.py:125-148), computed on the GPU."""
+    validate_batch(batch, allow_empty=allow_empty)
+    n = batch.num_tokens
+    if n >= 2**32:
+        raise CapacityExceeded(f"{n} tokens exceed 32-bit index range")
+    if n == 0:
+        z = np.zeros(0, np.uint32)
+        return CompactionPlan(z, z, z, 0, 0)
+    tok, pos, cu = upload_batch(batch)
+    return build_plan_device(tok, pos, cu, allow_empty=allow_empty).to_host()
+
+
+def build_plan_fast_paths(batch: RaggedBatch) -> CompactionPlan | None:
+    """Reference fast paths (trie.py:151-188): B == 1 or all-identical batches.
+
+    Returns None when neither applies.  The GPU planner produces the same
+    identity / tiled plan for those batches, so the plan is built there.
+    """
+    validate_batch(batch)
+    b, n = batch.num_sequences, batch.num_tokens
+    if b == 1:
+        return build_plan(batch)
+    if b > 1:
+        lengths = batch.seq_lengths()
+        length = int(lengths[0])
+        if np.all(lengths == length):
+            t = batch.token_ids.reshape(b, length)
+            p = batch.position_ids.reshape(b, length)
+            if np.all(t == t[0]) and np.all(p == p[0]):
+                return build_plan(batch)
+    del n
+    return None
+
+
+def build_plan_auto(batch: RaggedBatch) -> CompactionPlan:
+    """Reference ``build_plan_auto`` (trie.py:191-194): one GPU build covers all cases."""
+    return build_plan(batch)
+
+
+def should_enable(plan, threshold) -> bool:
+    """gamma <= threshold, inclusive, exact rational (trie.py:197-203)."""
+    n, m = int(plan.n_original), int(plan.n_compact)
+    gamma = Fraction(m, n) if n else Fraction(1)
+    return gamma <= Fraction(threshold).limit_denominator(10**9)
+
+
+def pad_plan(plan: CompactionPlan, bucket_size: int) -> CompactionPlan:
+    """Pad N' to a multiple of bucket_size by repeating row 0 (trie.py:206-233)."""
+    if bucket_size < 1:
+        raise ValueError("bucket_size must be >= 1")
+    if plan.n_compact == 0:
+        raise EmptyPlan("cannot pad a plan with zero compact tokens")
+    target = -(-plan.n_compact // bucket_size) * bucket_size
+    if target == plan.n_padded:
+        return plan
+    extra = target - plan.n_compact
+    g = plan.gather_indices[: plan.n_compact]
+    p = plan.compact_positions[: plan.n_compact]
+    return CompactionPlan(
+        gather_indices=np.concatenate([g, np.repeat(g[:1], extra)]),
+        scatter_indices=plan.scatter_indices,
+        compact_positions=np.concatenate([p, np.repeat(p[:1], extra)]),
+        n_original=plan.n_original,
+        n_compact=plan.n_compact,
+    )
+
+
+def host_plan_cu_q(plan: CompactionPlan, cu_seqlens) -> np.ndarray | None:
+    """cu_q of a host plan if it has the per-sequence-suffix structure, else None.
+
+    Plans from build_plan always have it (compact rows of sequence s are
+    [cu[s] + lcp_s, cu[s+1]) in order); hand-made plans may not.
+    """
+    cu = np.asarray(cu_seqlens, dtype=np.int64)
+    n, m = plan.n_original, plan.n_compact
+    g = plan.gather_indices[:m].astype(np.int64)
+    s = plan.scatter_indices.astype(np.int64)
+    if n == 0:
+        return np.zeros(cu.shape[0], dtype=np.int64)
+    if s.size != n or (m and (g.max() >= n or s.max() >= m)):
+        return None
+    is_rep = g[s] == np.arange(n)
+    csum = np.concatenate([[0], np.cumsum(is_rep.astype(np.int64))])
+    counts = csum[cu[1:]] - csum[cu[:-1]]
+    cu_q = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    if cu_q[-1] != m:
+        return None
+    lcp = np.diff(cu) - counts
+    expect = np.concatenate([np.arange(cu[i] + lcp[i], cu[i + 1]) for i in range(cu.shape[0] - 1)]) \
+        if cu.shape[0] > 1 else np.zeros(0, np.int64)
+    if expect.shape[0] != m or not np.array_equal(expect, g):
+        return None
+    return cu_q

@@ -1,0 +1,155 @@
+"""tcgen05 GEMM + fused epilogues vs a plain PyTorch fp32 reference of the same op.
+
+Inputs are bf16; the reference computes in fp32 from the same bf16 values, so
+the only difference is accumulation order (fp32) and the final bf16 rounding.
+Tolerances are stated per epilogue.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(a, w, epi, out, block_n=0, **qkv):
+    from paper_2601_15013_b200 import _native
+
+    args = _native.GemmArgs()
+    args.a, args.b = a.data_ptr(), w.data_ptr()
+    args.m, args.n, args.k = a.shape[0], w.shape[0], w.shape[1]
+    args.lda, args.ldb = a.stride(0), w.stride(0)
+    args.epi, args.block_n = epi, block_n
+    args.out, args.ldo = out.data_ptr(), out.stride(0)
+    if qkv:
+        args.q_norm_w = qkv["qn"].data_ptr()
+        args.k_norm_w = qkv["kn"].data_ptr()
+        args.rope_table = qkv["rope"].data_ptr()
+        args.head_dim, args.q_heads, args.kv_heads = qkv["hd"], qkv["H"], qkv["KV"]
+        args.eps = qkv["eps"]
+    _native.check(_native.lib().rdx_gemm(args, _native.stream_handle()), "rdx_gemm")
+
+
+def _rand(m, k, seed, scale=1.0):
+    import torch
+
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(m, k, generator=g, device="cuda") * scale).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (1, 128, 64), (300, 384, 256), (7040, 4096, 1024),
+                                   (129, 200, 72), (1000, 1024, 2048)])
+@pytest.mark.parametrize("block_n", [128, 256])
+def test_store_bf16_and_f32(m, n, k, block_n):
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    a, w = _rand(m, k, 1), _rand(n, k, 2)
+    ref = a.float() @ w.float().T
+    out = torch.full((m, n), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _gemm(a, w, _native.EPI_STORE_BF16, out, block_n)
+    torch.cuda.synchronize()
+    tol = 2e-2 * ref.abs().max().item() + 1e-3
+    assert (out.float() - ref).abs().max().item() <= tol
+    out32 = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    _gemm(a, w, _native.EPI_STORE_F32, out32, block_n)
+    assert (out32 - ref).abs().max().item() <= 1e-3 * math.sqrt(k) * ref.abs().max().item() / 8 + 1e-4
+
+
+def test_rows_batch_invariant():
+    """Row r of the output is bit-identical whatever M is (no split-K, fixed tiles)."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    a, w = _rand(1000, 512, 3), _rand(768, 512, 4)
+    full = torch.empty(1000, 768, dtype=torch.float32, device="cuda")
+    _gemm(a, w, _native.EPI_STORE_F32, full)
+    sub = torch.empty(37, 768, dtype=torch.float32, device="cuda")
+    _gemm(a[500:537], w, _native.EPI_STORE_F32, sub)
+    assert torch.equal(full[500:537], sub)
+
+
+def test_resid_f32():
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    a, w = _rand(333, 512, 5), _rand(1024, 512, 6)
+    h0 = torch.randn(333, 1024, device="cuda")
+    h = h0.clone()
+    _gemm(a, w, _native.EPI_RESID_F32, h)
+    ref = h0 + a.float() @ w.float().T
+    assert (h - ref).abs().max().item() <= 1e-3
+
+
+@pytest.mark.parametrize("block_n", [128, 256])
+def test_swiglu(block_n):
+    import torch
+
+    from paper_2601_15013_b200 import _native
+    from paper_2601_15013_b200.model import DeviceWeights
+
+    m, d, di = 515, 256, 384
+    a = _rand(m, d, 7)
+    wg, wu = _rand(di, d, 8, 0.1), _rand(di, d, 9, 0.1)
+    wgu = DeviceWeights._interleave_gate_up(wg, wu, di)
+    out = torch.empty(m, di, dtype=torch.bfloat16, device="cuda")
+    _gemm(a, wgu, _native.EPI_SWIGLU, out, block_n)
+    g = a.float() @ wg.float().T
+    u = a.float() @ wu.float().T
+    ref = g / (1 + torch.exp(-g)) * u
+    assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item() + 1e-3
+
+
+@pytest.mark.parametrize("hd,H,KV", [(128, 16, 8), (16, 4, 2), (64, 4, 2)])
+def test_qkv_norm_rope(hd, H, KV):
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    m, d = 300, 256
+    a = _rand(m, d, 10)
+    n = (H + 2 * KV) * hd
+    w = _rand(n, d, 11, 0.2)
+    qn = torch.rand(hd, device="cuda") + 0.5
+    kn = torch.rand(hd, device="cuda") + 0.5
+    pos = torch.randint(0, 4000, (m,), device="cuda", dtype=torch.int32)
+    rope = torch.empty(m, hd // 2, 2, device="cuda")
+    _native.check(_native.lib().rdx_rope_table(pos.data_ptr(), m, hd, 1e6, rope.data_ptr(),
+                                               _native.stream_handle()), "rope")
+    out = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    _gemm(a, w, _native.EPI_QKV, out, 0, qn=qn, kn=kn, rope=rope, hd=hd, H=H, KV=KV, eps=1e-6)
+    # fp32 torch reference of model.py:356-366 with fp64 rope tables
+    x = a.float() @ w.float().T
+    inv = 1e6 ** (-torch.arange(0, hd, 2, dtype=torch.float64, device="cuda") / hd)
+    ang = pos.double()[:, None] * inv[None, :]
+    cos = torch.cat([ang.cos(), ang.cos()], 1).float()[:, None, :]
+    sin = torch.cat([ang.sin(), ang.sin()], 1).float()[:, None, :]
+
+    def norm_rope(t, wgt):
+        t = t / torch.sqrt((t * t).mean(-1, keepdim=True) + 1e-6) * wgt
+        rot = torch.cat([-t[..., hd // 2:], t[..., : hd // 2]], -1)
+        return t * cos + rot * sin
+
+    q = norm_rope(x[:, : H * hd].view(m, H, hd), qn).reshape(m, -1)
+    k = norm_rope(x[:, H * hd:(H + KV) * hd].view(m, KV, hd), kn).reshape(m, -1)
+    v = x[:, (H + KV) * hd:]
+    ref = torch.cat([q, k, v], 1)
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item(), err
+
+
+def test_gemm_error_codes():
+    import torch
+
+    from paper_2601_15013_b200 import ShapeMismatch, _native
+
+    a = torch.zeros(4, 12, dtype=torch.bfloat16, device="cuda")
+    w = torch.zeros(8, 12, dtype=torch.bfloat16, device="cuda")
+    out = torch.zeros(4, 8, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ShapeMismatch):
+        _gemm(a, w, _native.EPI_STORE_BF16, out)
+    np.testing.assert_equal(1, 1)

@@ -1,0 +1,143 @@
+"""RadixQwen3 prefill on the GPU vs the reference's golden logits (fp64).
+
+Tolerance (BASELINE.json north star): max |gpu - ref| / max |ref| <= 2e-2 on
+final logits, bf16 weights/activations vs the fp64 reference.  Dedup on vs
+off, and both attention-boundary modes, are compared against each other too.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+def maxrel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def test_patterns_vs_reference(golden_forward):
+    from paper_2601_15013_b200 import ModelConfig, forward, init_params
+    from paper_2601_15013_b200.workloads import Pattern, make_pattern_batch
+
+    cfg = ModelConfig()
+    params = init_params(cfg, seed=7)
+    for pat in Pattern:
+        b = make_pattern_batch(pat, seed=3)
+        ref = golden_forward[f"pattern_{pat.value}_logits"]
+        for plan in (None, "auto"):
+            for attention in ("suffix", "full"):
+                out = forward(cfg, params, b, plan=plan, attention=attention).cpu().numpy()
+                assert out.shape == ref.shape
+                assert maxrel(out, ref) <= TOL, (pat.value, plan, attention, maxrel(out, ref))
+
+
+def test_c1_vs_reference(golden_forward):
+    from paper_2601_15013_b200 import TINY_C1, forward, init_params
+    from paper_2601_15013_b200.workloads import SyntheticSpec, make_synthetic_batch
+
+    params = init_params(TINY_C1, seed=0)
+    b = make_synthetic_batch(SyntheticSpec(B=8, prefix_len=32, suffix_len=16, vocab=1024, seed=0))
+    ref = golden_forward["c1_logits"]
+    base = forward(TINY_C1, params, b).cpu().numpy()
+    radix = forward(TINY_C1, params, b, plan="auto").cpu().numpy()
+    full = forward(TINY_C1, params, b, plan="auto", attention="full").cpu().numpy()
+    assert maxrel(base, ref) <= TOL
+    assert maxrel(radix, ref) <= TOL
+    assert maxrel(full, ref) <= TOL
+    # full-layout attention boundary = the reference's algorithm; rows are bit-identical to dedup off
+    assert np.array_equal(full, base)
+
+
+def test_qwen3_06b_slice_vs_reference(golden_forward):
+    from paper_2601_15013_b200 import Qwen3Config, forward, init_params
+    from paper_2601_15013_b200.workloads import SyntheticSpec, make_synthetic_batch
+
+    cfg = Qwen3Config(1, 1024, 3072, 16, 8, 128, 512, 1e6, 1e-6)
+    params = init_params(cfg, seed=0)
+    b = make_synthetic_batch(SyntheticSpec(B=4, prefix_len=48, suffix_len=16, vocab=512, seed=5))
+    ref = golden_forward["q06_slice_logits"]
+    for plan in (None, "auto"):
+        out = forward(cfg, params, b, plan=plan).cpu().numpy()
+        assert maxrel(out, ref) <= TOL, (plan, maxrel(out, ref))
+
+
+def test_last_token_logits_match_full(golden_forward):
+    from paper_2601_15013_b200 import TINY_C1, forward, init_params
+    from paper_2601_15013_b200.workloads import SyntheticSpec, make_synthetic_batch
+
+    params = init_params(TINY_C1, seed=0)
+    b = make_synthetic_batch(SyntheticSpec(B=8, prefix_len=32, suffix_len=16, vocab=1024, seed=0))
+    last = forward(TINY_C1, params, b, plan="auto", logits="last").cpu().numpy()
+    ref = golden_forward["c1_logits"][b.cu_seqlens[1:] - 1]
+    assert maxrel(last, ref) <= TOL
+
+
+def test_ledger_law():
+    """tests/test_model.py:265-283: m + L*(3n + m) + n row copies with the full boundary."""
+    from paper_2601_15013_b200 import FlopLedger, ModelConfig, build_plan, forward, init_params
+    from paper_2601_15013_b200.workloads import Pattern, make_pattern_batch
+
+    cfg = ModelConfig(num_layers=1, hidden_size=64, intermediate_size=128, num_heads=2, num_kv_heads=1,
+                      head_dim=32, vocab_size=11)
+    params = init_params(cfg, seed=0)
+    b = make_pattern_batch(Pattern.COMPLEX_SHARING, seed=3, vocab=11)
+    plan = build_plan(b)
+    n, m = plan.n_original, plan.n_compact
+    base, radix = FlopLedger(), FlopLedger()
+    forward(cfg, params, b, ledger=base)
+    forward(cfg, params, b, plan=plan, ledger=radix, attention="full")
+    assert all(rows == n for _, rows in base.phases)
+    assert all(rows == m for _, rows in radix.phases)
+    assert base.attention_row_ops == radix.attention_row_ops == n * cfg.num_layers
+    assert base.gather_scatter_rows == 0
+    assert radix.gather_scatter_rows == m + cfg.num_layers * (3 * n + m) + n
+
+
+def test_padded_plan_identical():
+    from paper_2601_15013_b200 import ModelConfig, build_plan, forward, init_params, pad_plan
+    from paper_2601_15013_b200.workloads import Pattern, make_pattern_batch
+
+    cfg = ModelConfig(num_layers=1, hidden_size=64, intermediate_size=128, num_heads=2, num_kv_heads=1,
+                      head_dim=32, vocab_size=11)
+    params = init_params(cfg, seed=1)
+    b = make_pattern_batch(Pattern.SHARED_PREFIX, seed=3, vocab=11)
+    plan = build_plan(b)
+    a = forward(cfg, params, b, plan=plan).cpu().numpy()
+    p = forward(cfg, params, b, plan=pad_plan(plan, 16)).cpu().numpy()
+    assert np.array_equal(a, p)
+
+
+def test_plan_batch_mismatch():
+    from paper_2601_15013_b200 import ModelConfig, PlanBatchMismatch, build_plan, forward, init_params
+    from paper_2601_15013_b200.ragged import RaggedBatch, default_positions
+
+    cfg = ModelConfig(num_layers=1, hidden_size=64, intermediate_size=128, num_heads=2, num_kv_heads=1,
+                      head_dim=32, vocab_size=11)
+    params = init_params(cfg, seed=0)
+    cu = np.array([0, 3, 6])
+    b = RaggedBatch(np.array([1, 2, 3, 1, 2, 4]), default_positions(cu), cu)
+    cu2 = np.array([0, 2, 4])
+    other = RaggedBatch(np.array([1, 2, 1, 2]), default_positions(cu2), cu2)
+    with pytest.raises(PlanBatchMismatch):
+        forward(cfg, params, b, plan=build_plan(other))
+
+
+def test_causality():
+    from paper_2601_15013_b200 import ModelConfig, forward, init_params
+    from paper_2601_15013_b200.ragged import RaggedBatch, default_positions
+
+    cfg = ModelConfig(num_layers=1, hidden_size=64, intermediate_size=128, num_heads=2, num_kv_heads=1,
+                      head_dim=32, vocab_size=11)
+    params = init_params(cfg, seed=2)
+    cu = np.array([0, 3, 7])
+    a_b = RaggedBatch(np.array([1, 2, 3, 1, 2, 4, 5]), default_positions(cu), cu)
+    p_b = RaggedBatch(np.array([1, 2, 3, 1, 9, 4, 5]), default_positions(cu), cu)
+    for plan, att in ((None, "suffix"), ("auto", "full")):
+        a = forward(cfg, params, a_b, plan=plan, attention=att).cpu().numpy()
+        p = forward(cfg, params, p_b, plan=plan, attention=att).cpu().numpy()
+        diff = np.abs(a - p).max(axis=1)
+        assert np.all(diff[:4] == 0.0)
+        assert np.all(diff[4:] > 0.0)

@@ -1,0 +1,145 @@
+"""GPU planner parity: rdx_plan_build vs the reference's golden plans and the C oracle.
+
+Bit-exact for every index (gather, scatter, compact_positions, N').  Sizes
+up to 1M tokens are checked against the oracle trie; the long-prefix C4
+shape is checked through its closed form N' = P + B*S and the plan
+invariants (tests/test_trie.py:95-112 of the reference).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import unpack
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_plan(tok, pos, cu, allow_empty=False):
+    from paper_2601_15013_b200 import RaggedBatch, build_plan
+
+    return build_plan(RaggedBatch(tok, pos, cu), allow_empty=allow_empty)
+
+
+def _assert_plan(plan, gather, scatter, m, pos=None):
+    assert plan.n_compact == m
+    np.testing.assert_array_equal(plan.gather_indices, gather)
+    np.testing.assert_array_equal(plan.scatter_indices, scatter)
+    if pos is not None:
+        np.testing.assert_array_equal(plan.compact_positions, np.asarray(pos)[np.asarray(gather, np.int64)])
+
+
+@pytest.mark.parametrize("prefix", ["known", "rand", "arbpos", "pattern"])
+def test_golden_plans_bit_exact(golden_plans, prefix):
+    count = 0
+    for tok, pos, cu, gather, scatter, m in unpack(golden_plans, prefix):
+        _assert_plan(_gpu_plan(tok, pos, cu), gather, scatter, m, pos)
+        count += 1
+    assert count > 0
+
+
+def test_toy_known_answer():
+    plan = _gpu_plan(np.array([1, 2, 3, 1, 2, 4]), np.array([0, 1, 2, 0, 1, 2]), np.array([0, 3, 6]))
+    assert plan.gather_indices.tolist() == [0, 1, 2, 5]
+    assert plan.scatter_indices.tolist() == [0, 1, 2, 0, 1, 3]
+    assert plan.compact_positions.tolist() == [0, 1, 2, 2]
+    assert plan.gamma == pytest.approx(4 / 6)
+
+
+def test_table_rows(golden_plans):
+    from paper_2601_15013_b200.workloads import SyntheticSpec, make_synthetic_batch
+
+    for p, s, n, m in golden_plans["table"]:
+        b = make_synthetic_batch(SyntheticSpec(B=32, prefix_len=int(p), suffix_len=int(s)))
+        plan = _gpu_plan(b.token_ids, b.position_ids, b.cu_seqlens)
+        assert plan.n_original == n and plan.n_compact == m
+
+
+@pytest.mark.parametrize("n_target,prefix_ratio", [(1024, 0.0), (16384, 0.25), (131072, 0.5), (1 << 20, 0.75),
+                                                   (1 << 20, 1.0)])
+def test_vs_oracle_large(oracle, n_target, prefix_ratio):
+    """C5 microbench shapes: L=512, B=N/512, shared prefix ratio, bit-exact vs the oracle."""
+    from paper_2601_15013_b200.workloads import SyntheticSpec, make_synthetic_batch
+
+    L = 512
+    p = int(L * prefix_ratio)
+    b = make_synthetic_batch(SyntheticSpec(B=n_target // L, prefix_len=p, suffix_len=L - p, vocab=151936, seed=3))
+    g, s, cp, m = oracle.build_plan_oracle(b.token_ids, b.position_ids, b.cu_seqlens)
+    plan = _gpu_plan(b.token_ids, b.position_ids, b.cu_seqlens)
+    _assert_plan(plan, g, s, m)
+    np.testing.assert_array_equal(plan.compact_positions, cp)
+
+
+def test_multilevel_trie_vs_oracle(oracle):
+    """Branching at many depths with a tiny alphabet (deep shared structure)."""
+    rng = np.random.default_rng(11)
+    for _ in range(20):
+        bsz = int(rng.integers(50, 400))
+        lens = rng.integers(1, 300, size=bsz)
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        tok = rng.integers(0, 2, size=int(cu[-1])).astype(np.uint32)
+        starts = np.repeat(cu[:-1], lens)
+        pos = (np.arange(int(cu[-1])) - starts).astype(np.uint32)
+        g, s, cp, m = oracle.build_plan_oracle(tok, pos, cu)
+        _assert_plan(_gpu_plan(tok, pos, cu), g, s, m)
+
+
+def test_long_prefix_c4_closed_form():
+    from paper_2601_15013_b200.workloads import long_prefix_batch
+
+    b = long_prefix_batch()
+    plan = _gpu_plan(b.token_ids, b.position_ids, b.cu_seqlens)
+    assert plan.n_original == 294_912 and plan.n_compact == 2048 + 128 * 256
+    g = plan.gather_indices.astype(np.int64)
+    s = plan.scatter_indices.astype(np.int64)
+    assert np.all(np.diff(g) > 0)
+    assert np.array_equal(s[g], np.arange(plan.n_compact))
+    rep = g[s]
+    assert np.array_equal(b.token_ids[rep], b.token_ids)
+    assert np.array_equal(b.position_ids[rep], b.position_ids)
+
+
+def test_empty_sequences_allowed(oracle):
+    tok = np.array([1, 2, 1, 2, 3], dtype=np.uint32)
+    cu = np.array([0, 2, 2, 5, 5], dtype=np.int64)
+    pos = np.array([0, 1, 0, 1, 2], dtype=np.uint32)
+    g, s, cp, m = oracle.build_plan_oracle(tok, pos, cu)
+    _assert_plan(_gpu_plan(tok, pos, cu, allow_empty=True), g, s, m)
+
+
+def test_validation_errors():
+    from paper_2601_15013_b200 import BoundaryMismatch, MismatchedLengths, NonMonotoneOffsets
+
+    with pytest.raises(NonMonotoneOffsets):
+        _gpu_plan(np.array([1, 2, 3]), np.array([0, 1, 0]), np.array([0, 3, 2]))
+    with pytest.raises(NonMonotoneOffsets):
+        _gpu_plan(np.array([1, 2]), np.array([0, 1]), np.array([0, 2, 2]))
+    with pytest.raises(BoundaryMismatch):
+        _gpu_plan(np.array([1, 2]), np.array([0, 1]), np.array([1, 2]))
+    with pytest.raises(MismatchedLengths):
+        _gpu_plan(np.array([1, 2]), np.array([0]), np.array([0, 2]))
+
+
+def test_device_side_validation_codes():
+    """The C ABI reports bad offsets itself (no host pre-check)."""
+    import torch
+
+    from paper_2601_15013_b200 import NonMonotoneOffsets, build_plan_device
+
+    tok = torch.tensor([1, 2, 3], dtype=torch.int32, device="cuda")
+    cu = torch.tensor([0, 3, 2], dtype=torch.int64, device="cuda")
+    with pytest.raises(NonMonotoneOffsets):
+        build_plan_device(tok, tok, cu)
+
+
+def test_cu_q_matches_suffix_structure():
+    from paper_2601_15013_b200 import RaggedBatch, build_plan_device
+    from paper_2601_15013_b200.plan import host_plan_cu_q, upload_batch
+    from paper_2601_15013_b200.workloads import RerankSpec, msmarco_rerank_batch
+
+    b = msmarco_rerank_batch(RerankSpec(queries=2, passages_per_query=16))
+    tok, pos, cu = upload_batch(b)
+    dp = build_plan_device(tok, pos, cu)
+    assert np.array_equal(dp.cu_q_host, host_plan_cu_q(dp.to_host(), b.cu_seqlens))
+    lcp = dp.lcp.cpu().numpy()
+    assert np.array_equal(np.diff(dp.cu_q_host), np.diff(b.cu_seqlens) - lcp)
+    assert isinstance(b, RaggedBatch)
