@@ -127,8 +127,19 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
+class _Counter:
+    """C-ABI calls that reached the device (each launches one kernel); bench.py reads it."""
+
+    launches = 0
+
+
+LAUNCHES = _Counter()
+
+
 def check(code: int, what: str) -> None:
-    """Raise the mapped exception for a non-zero status."""
+    """Raise the mapped exception for a non-zero status; count successful launches."""
+    if code == 0:
+        LAUNCHES.launches += 1
     if code:
         detail = ""
         if code == 100:

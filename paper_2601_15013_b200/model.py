@@ -384,9 +384,9 @@ class RadixQwen3:
             if plan.scatter_indices.shape[0] != db.n:
                 raise PlanBatchMismatch("scatter index length disagrees with batch")
             dev = db.tok.device
-            g = torch.from_numpy(plan.gather_indices.view(np.int32)).to(dev)
-            s = torch.from_numpy(plan.scatter_indices.view(np.int32)).to(dev)
-            p = torch.from_numpy(plan.compact_positions.view(np.int32)).to(dev)
+            g = torch.from_numpy(np.array(plan.gather_indices).view(np.int32)).to(dev)
+            s = torch.from_numpy(np.array(plan.scatter_indices).view(np.int32)).to(dev)
+            p = torch.from_numpy(np.array(plan.compact_positions).view(np.int32)).to(dev)
             cu_q = host_plan_cu_q(plan, db.cu_host) if attention == "suffix" else None
             if cu_q is None:
                 return _Layout(plan.n_padded, plan.n_compact, g, s, p, None, 0, False, True)
@@ -483,25 +483,26 @@ class RadixQwen3:
                 self._rmsnorm(h, T[f"layers.{i + 1}.ln1"], hn, stream=st)
 
         vocab = cfg.vocab_size
+        vpad = -(-vocab // 8) * 8  # 16-byte aligned logits rows
         if logits == "last":
             hl = torch.empty(db.b, d, dtype=bf, device=dev)
             self._rmsnorm(h, T["final_norm"], hl, rows=last_rows, n_rows=db.b, stream=st)
             ledger.positionwise("final_norm", db.b)
-            out = torch.empty(db.b, vocab, dtype=torch.float32, device=dev)
+            out = torch.empty(db.b, vpad, dtype=torch.float32, device=dev)[:, :vocab]
             self._gemm("lm_head", hl, T["lm_head"], _native.EPI_STORE_F32, out, m=db.b, stream=st)
             ledger.positionwise("lm_head", db.b)
-            result = out
+            result = out if vpad == vocab else out.contiguous()
         else:
             self._rmsnorm(h, T["final_norm"], hn, stream=st)
             ledger.positionwise("final_norm", m)
-            out = torch.empty(m, vocab, dtype=torch.float32, device=dev)
+            out = torch.empty(m, vpad, dtype=torch.float32, device=dev)[:, :vocab]
             self._gemm("lm_head", hn, T["lm_head"], _native.EPI_STORE_F32, out, m=m, stream=st)
             ledger.positionwise("lm_head", m)
             if lay.dedup:
                 result = gather_rows_device(out, lay.scatter, stream=stream)
                 ledger.index_copy(n)
             else:
-                result = out
+                result = out if vpad == vocab else out.contiguous()
         if int(err.item()):
             from .errors import IndexOutOfRange
 
