@@ -199,19 +199,22 @@ def time_wall_steps(fn, steps, warmup, world):
 
 
 # ------------------------------------------------------------------ roofline of the GEMMs
-def gemm_roofline(model, step, steps, peak_tflops):
+def op_breakdown(model, step, steps, peak_tflops):
+    """Per-op CUDA events over ``steps`` eager steps; the GEMM roofline comes from
+    the gemm.* launches (algorithmic 2*M*N*K FLOPs / event time)."""
     import torch
 
     records = []
 
-    def hook(name, launch, m, n, k):
+    def hook(name, launch, flops):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
-        launch()
+        out = launch()
         e.record()
-        records.append((name, 2.0 * m * n * k, s, e))
+        records.append((name, flops, s, e))
+        return out
 
-    model.gemm_hook = hook
+    model.op_hook = hook
     try:
         step()
         records.clear()
@@ -219,24 +222,25 @@ def gemm_roofline(model, step, steps, peak_tflops):
             step()
         torch.cuda.synchronize()
     finally:
-        model.gemm_hook = None
-    flops = sum(r[1] for r in records)
-    ms = sum(r[2].elapsed_time(r[3]) for r in records)
+        model.op_hook = None
     by = {}
     for name, f, s, e in records:
         d = by.setdefault(name, [0.0, 0.0, 0])
         d[0] += f
         d[1] += s.elapsed_time(e)
         d[2] += 1
-    launches = len(records)
+    gemm = [(f, s.elapsed_time(e)) for name, f, s, e in records if name.startswith("gemm.")]
+    flops = sum(g[0] for g in gemm)
+    ms = sum(g[1] for g in gemm)
     achieved = flops / (ms * 1e-3) / 1e12
-    per_kind = {k: {"tflops": round(v[0] / (v[1] * 1e-3) / 1e12, 1), "launches": v[2],
-                    "avg_us": round(v[1] * 1e3 / v[2], 2)} for k, v in by.items()}
-    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tflops, "unit": "TFLOP/s",
+    breakdown = {k: {"us_per_step": round(v[1] * 1e3 / steps, 1), "launches_per_step": v[2] // steps,
+                     **({"tflops": round(v[0] / (v[1] * 1e-3) / 1e12, 1)} if v[0] else {})}
+                 for k, v in sorted(by.items(), key=lambda kv: -kv[1][1])}
+    roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak_tflops, "unit": "TFLOP/s",
             "frac": round(achieved / peak_tflops, 4), "traffic": None,
-            "kernel": "rdx gemm_kernel (tcgen05, all launches of a step)",
-            "flops_per_launch": round(flops / launches), "avg_launch_us": round(ms * 1e3 / launches, 2),
-            "per_gemm": per_kind}, ms / steps
+            "kernel": "rdx gemm_kernel (tcgen05, every GEMM launch of a step)",
+            "flops_per_launch": round(flops / max(len(gemm), 1)), "avg_launch_us": round(ms * 1e3 / max(len(gemm), 1), 2)}
+    return roof, ms / steps, breakdown
 
 
 # ------------------------------------------------------------------ gather GB/s
@@ -361,7 +365,7 @@ def run_ours(args):
     config, model_name, global_batch, label = build_config(args.config, world)
     shards = partition_by_subtree(global_batch, world)
     mine = shards[rank]
-    model = RadixQwen3(config, DeviceWeights.random(config, seed=0))
+    model = RadixQwen3(config, DeviceWeights.random(config, seed=0), use_graphs=not args.no_graphs)
     db = DeviceBatch.from_batch(mine.batch)
     rr = RadixReranker(model, dedup=True)
     rr_base = RadixReranker(model, dedup=False)
@@ -383,11 +387,20 @@ def run_ours(args):
     tokens_all = max_over_ranks(0, 1) + global_batch.num_tokens
 
     # launches per step (our C-ABI kernels; FlashAttention is counted separately)
+    step_radix()  # captures the CUDA graph (if enabled) outside the count
+    torch.cuda.synchronize()
+    model.use_graphs, graphs_on = False, model.use_graphs
     c0 = _native.LAUNCHES.launches
     step_radix()
     torch.cuda.synchronize()
     launches_per_step = _native.LAUNCHES.launches - c0
+    model.use_graphs = graphs_on
 
+    if args.profile:  # short run for ncu: warm-ups + a few radix steps, no JSON
+        for _ in range(args.warmup + args.steps):
+            step_radix()
+        torch.cuda.synchronize()
+        return
     sampler = ClockSampler(local) if rank == 0 else None
     ms_radix, per_radix, clocks = time_steps(step_radix, args.steps, args.warmup, world, flush, sampler)
     ms_base, per_base, _ = time_steps(step_base, args.steps, args.warmup, world, flush)
@@ -406,10 +419,11 @@ def run_ours(args):
     ms_e2e = time_wall_steps(e2e_step, args.steps, args.warmup, world)
     e2e_value = tokens_all * args.steps / (ms_e2e * 1e-3)
 
-    roof, gemm_ms_per_step = gemm_roofline(model, step_radix, max(3, min(args.steps, 10)),
-                                           peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
+    roof, gemm_ms_per_step, breakdown = op_breakdown(model, step_radix, max(3, min(args.steps, 10)),
+                                                     peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
     roof["peak_source"] = f"{peaks_src} bf16_tflops_sustained (kernels inside a long step)"
     roof["gemm_share_of_step"] = round(gemm_ms_per_step / (ms_radix / args.steps), 3)
+    _, _, breakdown_base = op_breakdown(model, step_base, 3, 1.0)
 
     gather = gather_microbench(peaks["hbm_gbs"]) if rank == 0 else None
     cpu = None
@@ -425,12 +439,15 @@ def run_ours(args):
                        "tokens_per_step": int(tokens_all), "n_compact_rank0": int(n_comp),
                        "gamma_rank0": round(n_comp / n_tok, 4), "parallelism": f"dp{world} (trie-subtree shards)",
                        "logits": "last-token, full vocab", "attention": "suffix-query (FlashAttention-2 varlen)",
+                       "cuda_graphs": not args.no_graphs,
                        "l2": "L2 flushed (256 MiB write) between timed steps"},
             "nodedup": {"value": round(value_base, 1), "ms_per_step": round(ms_base / args.steps, 4)},
             "speedup_vs_nodedup": round(value / value_base, 3),
             "e2e": {"value": round(e2e_value, 1), "unit": "tokens/s", "h2d_bytes_per_step": int(rr.h2d_bytes),
                     "d2h_bytes_per_step": int(rr.d2h_bytes), "ms_per_step": round(ms_e2e / args.steps, 4)},
             "roofline": roof,
+            "breakdown_us_radix": breakdown,
+            "breakdown_us_nodedup": {k: v["us_per_step"] for k, v in breakdown_base.items()},
             "cpu_baseline": cpu,
             "gather": gather,
             "gpu_launches": int(launches_per_step * args.steps),
@@ -454,6 +471,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--profile", action="store_true", help="radix steps only, for ncu")
+    ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA-graph replay")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

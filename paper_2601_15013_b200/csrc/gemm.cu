@@ -3,16 +3,21 @@
 //
 //   acc[m, n] = sum_k A[m, k] * B[n, k]        A: activations [M, K] bf16
 //                                              B: weight [N, K] bf16 ([out, in])
+// CG = 1: one CTA per 128 x BN tile, tcgen05.mma.cta_group::1 (M = 128).
+// CG = 2: a CTA pair (cluster of 2) per 256 x BN tile, tcgen05.mma.cta_group::2
+//         (M = 256): each CTA stages its 128 rows of A and BN/2 rows of B, the
+//         leader issues the MMA for both, so per-SM operand traffic drops by a
+//         third versus CG = 1 at the same accumulator size.
 // CTA = 6 warps:
-//   warp 0      TMA producer (one elected lane): A/B k-blocks -> smem ring
-//   warp 1      TMEM allocator + MMA issuer (one lane): tcgen05.mma 128xBNx16
-//   warps 2..5  epilogue: tcgen05.ld accumulator rows -> fused op -> global
+//   warp 0      TMA producer (one lane): A/B k-blocks -> smem ring
+//   warp 1      TMEM allocator + MMA issuer (one lane, leader CTA)
+//   warps 2..5  epilogue: tcgen05.ld -> fused op -> swizzled smem box ->
+//               TMA store (bf16 / fp32) or TMA reduce-add (fp32 residual)
 // Pipelines: smem full/empty mbarriers (TMA <-> MMA), two TMEM accumulator
 // buffers with full/empty mbarriers (MMA <-> epilogue), static persistent
-// tile schedule (tile = blockIdx.x + i * gridDim.x, M fastest).
-// Each output row depends only on its own A row: no split-K, M-independent
-// tiling, so the compact and the full forward give bit-identical rows
-// (the reference's _mm batch-invariance rule, model.py:124-144).
+// tile schedule (M fastest).  Each output row depends only on its own A row:
+// no split-K and an M-independent tile shape, so compact and full forwards
+// give bit-identical rows (the reference's _mm rule, model.py:124-144).
 #include <mutex>
 
 #include "common.cuh"
@@ -20,14 +25,14 @@
 namespace rdx {
 namespace gemm {
 
-constexpr int BM = 128;
-constexpr int BK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B atom row
-constexpr int kThreads = 192;
-constexpr int kSwigluUnit = 64;  // gate/up interleave unit (columns)
+constexpr int BM = 128;  // rows per CTA
+constexpr int BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B atom row
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kSwigluUnit = 64;   // gate/up interleave unit (columns)
+constexpr int kEpiBoxBytes = 4096;  // 32 rows x 128 B staging box (SWIZZLE_128B)
 
 struct EpiParams {
-  void* out;
-  int64_t ldo;
   const float* qn;
   const float* kn;
   const float2* rope;
@@ -35,162 +40,193 @@ struct EpiParams {
   float eps;
 };
 
-template <int BN, int STAGES>
+template <int BN, int CG>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_ROWS = BN / CG;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-  static constexpr uint32_t IDESC = umma_idesc_bf16(BM, BN);
+  static constexpr int EPI_BYTES = kEpiWarps * 2 * kEpiBoxBytes;
+  static constexpr int AUX_BYTES = 1024;
+  static constexpr int BUDGET = 227 * 1024 - 1024 - 256 - EPI_BYTES - AUX_BYTES;
+  static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + AUX_BYTES + 256;
+  static constexpr uint32_t IDESC = umma_idesc_bf16(BM * CG, BN);
   static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static_assert(STAGES >= 3, "pipeline too shallow");
 };
 
-__device__ __forceinline__ void store8_bf16(void* out, int64_t ldo, int64_t gm, int64_t col,
-                                            int64_t ncols, const float (&v)[8]) {
-  __nv_bfloat16* p = static_cast<__nv_bfloat16*>(out) + gm * ldo + col;
-  if (col + 8 <= ncols) {
-    st_global_v4(p, pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
-                 pack_bf16x2(v[6], v[7]));
-  } else {
+// ------------------------------------------------------------------ epilogue plumbing
+struct EpiWarp {
+  uint8_t* buf[2];
+  int cur;
+  int lane;
+  int32_t row0;  // first global row of this warp's 32-row slab
+};
+
+// Write this lane's 128-byte row into the swizzled box and TMA-store it at (c0, row0).
+__device__ __forceinline__ void epi_emit(EpiWarp& e, const uint32_t (&w)[32], const CUtensorMap* map, int32_t c0,
+                                         bool reduce_add) {
+  if (e.lane == 0) bulk_wait_read<1>();  // the box written two emits ago has been read
+  __syncwarp();
+  const uint32_t base = smem_u32(e.buf[e.cur]) + e.lane * 128;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (col + j < ncols) p[j] = __float2bfloat16(v[j]);
+  for (int j = 0; j < 8; ++j)
+    st_shared_v4(base + ((j ^ (e.lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (e.lane == 0) {
+    if (reduce_add) tma_reduce_add_2d(map, e.buf[e.cur], c0, e.row0);
+    else tma_store_2d(map, e.buf[e.cur], c0, e.row0);
+    bulk_commit();
+  }
+  e.cur ^= 1;
+}
+
+__device__ __forceinline__ void pack64(const float* v, uint32_t (&w)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+}
+
+__device__ __forceinline__ void bits32(const float* v, uint32_t (&w)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
+}
+
+// q/k head: RMSNorm over HD (weight w from smem), then rotate-half RoPE.
+template <int HD>
+__device__ __forceinline__ void norm_rope(float* x, const float* w, const float2* __restrict__ rope, float eps) {
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < HD; ++j) ss += x[j] * x[j];
+  const float inv = rsqrtf(ss / static_cast<float>(HD) + eps);
+  constexpr int H = HD / 2;
+#pragma unroll
+  for (int j = 0; j < H; j += 2) {
+    const float4 cs = __ldg(reinterpret_cast<const float4*>(rope + j));  // (cos_j, sin_j, cos_j+1, sin_j+1)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const float c = t ? cs.z : cs.x, s = t ? cs.w : cs.y;
+      const float a = x[j + t] * inv * w[j + t];
+      const float b = x[j + t + H] * inv * w[j + t + H];
+      x[j + t] = a * c - b * s;
+      x[j + t + H] = b * c + a * s;
+    }
   }
 }
 
-__device__ __forceinline__ void store8_f32(void* out, int64_t ldo, int64_t gm, int64_t col,
-                                           int64_t ncols, const float (&v)[8], bool accumulate) {
-  float* p = static_cast<float*>(out) + gm * ldo + col;
-  if (col + 8 <= ncols) {
-    float4* q = reinterpret_cast<float4*>(p);
-    float4 a = make_float4(v[0], v[1], v[2], v[3]), b = make_float4(v[4], v[5], v[6], v[7]);
-    if (accumulate) {
-      const float4 a0 = q[0], b0 = q[1];
-      a.x += a0.x; a.y += a0.y; a.z += a0.z; a.w += a0.w;
-      b.x += b0.x; b.y += b0.y; b.z += b0.z; b.w += b0.w;
-    }
-    q[0] = a;
-    q[1] = b;
-  } else {
+template <int HD>
+__device__ __forceinline__ void qkv_tile(EpiWarp& e, uint32_t taddr, int64_t n0, int64_t N, const EpiParams& ep,
+                                         const float* s_qn, const float* s_kn, const float2* rope_row,
+                                         const CUtensorMap* map, int BN) {
+  if constexpr (HD >= 64) {
+    for (int h0 = 0; h0 < BN; h0 += HD) {
+      const int64_t col0 = n0 + h0;
+      if (col0 >= N) break;
+      float x[HD];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (col + j < ncols) p[j] = accumulate ? p[j] + v[j] : v[j];
+      for (int c = 0; c < HD; c += 32) tmem_ld32p(taddr + h0 + c, x + c);
+      tmem_wait_ld();
+      const int kind = col0 < ep.q_dim ? 0 : (col0 < ep.q_dim + ep.kv_dim ? 1 : 2);
+      if (kind < 2) norm_rope<HD>(x, kind == 0 ? s_qn : s_kn, rope_row, ep.eps);
+#pragma unroll
+      for (int b = 0; b < HD; b += 64) {
+        uint32_t w[32];
+        pack64(x + b, w);
+        epi_emit(e, w, map, static_cast<int32_t>(col0 + b), false);
+      }
+    }
+  } else {
+    for (int b0 = 0; b0 < BN; b0 += 64) {
+      if (n0 + b0 >= N) break;
+      float x[64];
+#pragma unroll
+      for (int c = 0; c < 64; c += 32) tmem_ld32p(taddr + b0 + c, x + c);
+      tmem_wait_ld();
+#pragma unroll
+      for (int h = 0; h < 64; h += HD) {
+        const int64_t col0 = n0 + b0 + h;
+        const int kind = col0 < ep.q_dim ? 0 : (col0 < ep.q_dim + ep.kv_dim ? 1 : 2);
+        if (kind < 2 && col0 < N) norm_rope<HD>(x + h, kind == 0 ? s_qn : s_kn, rope_row, ep.eps);
+      }
+      uint32_t w[32];
+      pack64(x, w);
+      epi_emit(e, w, map, static_cast<int32_t>(n0 + b0), false);
+    }
   }
 }
 
 template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_tile(uint32_t taddr, int64_t gm, bool row_ok, int64_t n_blk,
-                                              int64_t N, const EpiParams& ep) {
-  const int64_t gn0 = n_blk * BN;
-  if constexpr (EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
+__device__ __forceinline__ void epilogue_tile(EpiWarp& e, uint32_t taddr, int64_t gm_lane, int64_t M, int64_t n_blk,
+                                              int64_t N, const EpiParams& ep, const float* s_qn,
+                                              const float* s_kn, const CUtensorMap* map) {
+  const int64_t n0 = n_blk * BN;
+  if constexpr (EPI == RDX_EPI_STORE_BF16) {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 64) {
+      if (n0 + c >= N) break;
+      float v[64];
+      tmem_ld32p(taddr + c, v);
+      tmem_ld32p(taddr + c + 32, v + 32);
+      tmem_wait_ld();
+      uint32_t w[32];
+      pack64(v, w);
+      epi_emit(e, w, map, static_cast<int32_t>(n0 + c), false);
+    }
+  } else if constexpr (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
-      if (gn0 + c >= N) break;
+      if (n0 + c >= N) break;
       float v[32];
-      tmem_ld32(taddr + c, v);
+      tmem_ld32p(taddr + c, v);
       tmem_wait_ld();
-      if (row_ok) {
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          float w[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) w[j] = v[g * 8 + j];
-          const int64_t col = gn0 + c + g * 8;
-          if (col < N) {
-            if constexpr (EPI == RDX_EPI_STORE_BF16) store8_bf16(ep.out, ep.ldo, gm, col, N, w);
-            else store8_f32(ep.out, ep.ldo, gm, col, N, w, EPI == RDX_EPI_RESID_F32);
-          }
-        }
-      }
+      uint32_t w[32];
+      bits32(v, w);
+      epi_emit(e, w, map, static_cast<int32_t>(n0 + c), EPI == RDX_EPI_RESID_F32);
     }
   } else if constexpr (EPI == RDX_EPI_SWIGLU) {
-    // tile columns: [g(64) u(64)] x (BN/128); out col = n_blk*BN/2 + pair*64 + j
     const int64_t nout = N / 2;
 #pragma unroll 1
     for (int p = 0; p < BN / (2 * kSwigluUnit); ++p) {
       const int64_t ocol0 = n_blk * (BN / 2) + p * kSwigluUnit;
       if (ocol0 >= nout) break;
-#pragma unroll 1
-      for (int c = 0; c < kSwigluUnit; c += 32) {
-        float g[32], u[32];
-        tmem_ld32(taddr + p * 2 * kSwigluUnit + c, g);
-        tmem_ld32(taddr + p * 2 * kSwigluUnit + kSwigluUnit + c, u);
-        tmem_wait_ld();
-        if (row_ok) {
+      float g[64], u[64];
+      tmem_ld32p(taddr + p * 128, g);
+      tmem_ld32p(taddr + p * 128 + 32, g + 32);
+      tmem_ld32p(taddr + p * 128 + 64, u);
+      tmem_ld32p(taddr + p * 128 + 96, u + 32);
+      tmem_wait_ld();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float w[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float x = g[q * 8 + j];
-              w[j] = x / (1.f + __expf(-x)) * u[q * 8 + j];
-            }
-            store8_bf16(ep.out, ep.ldo, gm, ocol0 + c + q * 8, nout, w);
-          }
-        }
-      }
+      for (int j = 0; j < 64; ++j) g[j] = g[j] / (1.f + __expf(-g[j])) * u[j];
+      uint32_t w[32];
+      pack64(g, w);
+      epi_emit(e, w, map, static_cast<int32_t>(ocol0), false);
     }
   } else if constexpr (EPI == RDX_EPI_QKV) {
-    const int hd = ep.hd, half = hd >> 1;
-#pragma unroll 1
-    for (int h0 = 0; h0 < BN; h0 += hd) {
-      const int64_t col0 = gn0 + h0;
-      if (col0 >= N) break;
-      const int kind = col0 < ep.q_dim ? 0 : (col0 < ep.q_dim + ep.kv_dim ? 1 : 2);
-      if (kind == 2) {
-#pragma unroll 1
-        for (int c = 0; c < hd; c += 8) {
-          float v[8];
-          tmem_ld8(taddr + h0 + c, v);
-          tmem_wait_ld();
-          if (row_ok) store8_bf16(ep.out, ep.ldo, gm, col0 + c, N, v);
-        }
-        continue;
-      }
-      const float* __restrict__ nw = kind == 0 ? ep.qn : ep.kn;
-      float ss = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < hd; c += 8) {
-        float v[8];
-        tmem_ld8(taddr + h0 + c, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 8; ++j) ss += v[j] * v[j];
-      }
-      const float inv = rsqrtf(ss / static_cast<float>(hd) + ep.eps);
-      const float2* __restrict__ rope = ep.rope + (row_ok ? gm : 0) * half;
-#pragma unroll 1
-      for (int c = 0; c < half; c += 8) {
-        float x1[8], x2[8], o1[8], o2[8];
-        tmem_ld8(taddr + h0 + c, x1);
-        tmem_ld8(taddr + h0 + half + c, x2);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float a = x1[j] * inv * __ldg(nw + c + j);
-          const float b = x2[j] * inv * __ldg(nw + half + c + j);
-          const float2 cs = __ldg(rope + c + j);
-          o1[j] = a * cs.x - b * cs.y;
-          o2[j] = b * cs.x + a * cs.y;
-        }
-        if (row_ok) {
-          store8_bf16(ep.out, ep.ldo, gm, col0 + c, N, o1);
-          store8_bf16(ep.out, ep.ldo, gm, col0 + half + c, N, o2);
-        }
-      }
+    const int64_t r = gm_lane < M ? gm_lane : (M > 0 ? M - 1 : 0);
+    const float2* rope_row = ep.rope + r * (ep.hd >> 1);
+    switch (ep.hd) {
+      case 128: qkv_tile<128>(e, taddr, n0, N, ep, s_qn, s_kn, rope_row, map, BN); break;
+      case 64: qkv_tile<64>(e, taddr, n0, N, ep, s_qn, s_kn, rope_row, map, BN); break;
+      case 32: qkv_tile<32>(e, taddr, n0, N, ep, s_qn, s_kn, rope_row, map, BN); break;
+      default: qkv_tile<16>(e, taddr, n0, N, ep, s_qn, s_kn, rope_row, map, BN); break;
     }
   }
 }
 
-template <int BN, int STAGES, int EPI>
+// ------------------------------------------------------------------ the kernel
+template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-            int64_t M, int64_t N, int64_t K, EpiParams ep) {
-  using C = Cfg<BN, STAGES>;
+            const __grid_constant__ CUtensorMap tmC, int64_t M, int64_t N, int64_t K, EpiParams ep) {
+  using C = Cfg<BN, CG>;
+  constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint8_t* epi_smem = smem + STAGES * C::STAGE_BYTES;
+  float* s_norm = reinterpret_cast<float*>(epi_smem + C::EPI_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + C::EPI_BYTES + C::AUX_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -198,7 +234,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t m_tiles = (M + BM - 1) / BM;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const int64_t unit = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
+  const int64_t n_units = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
+  const int64_t m_tiles = (M + BM * CG - 1) / (BM * CG);
   const int64_t n_tiles = (N + BN - 1) / BN;
   const int64_t num_tiles = m_tiles * n_tiles;
   const int kblocks = static_cast<int>((K + BK - 1) / BK);
@@ -206,22 +245,35 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], kEpiWarps * CG);
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    tmem_alloc(tmem_holder, C::TMEM_COLS);
-    tmem_relinquish();
+    if constexpr (CG == 2) {
+      tmem_alloc_cg2(tmem_holder, C::TMEM_COLS);
+      tmem_relinquish_cg2();
+    } else {
+      tmem_alloc(tmem_holder, C::TMEM_COLS);
+      tmem_relinquish();
+    }
+  }
+  if constexpr (EPI == RDX_EPI_QKV) {
+    for (int i = threadIdx.x; i < ep.hd; i += blockDim.x) {
+      s_norm[i] = ep.qn[i];
+      s_norm[128 + i] = ep.kn[i];
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -229,16 +281,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int32_t m0 = static_cast<int32_t>((tile % m_tiles) * BM);
-        const int32_t n0 = static_cast<int32_t>((tile / m_tiles) * BN);
+      for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
+        const int32_t m0 = static_cast<int32_t>((tile % m_tiles) * (BM * CG) + rank * BM);
+        const int32_t nb0 = static_cast<int32_t>((tile / m_tiles) * BN + rank * C::B_ROWS);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(&tmA, sa, &full[stage], kb * BK, m0);
-          tma_load_2d(&tmB, sb, &full[stage], kb * BK, n0);
+          if constexpr (CG == 2) {
+            const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tma_load_2d_cg2(&tmA, sa, bar, kb * BK, m0);
+            tma_load_2d_cg2(&tmB, sb, bar, kb * BK, nb0);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(&tmA, sa, &full[stage], kb * BK, m0);
+            tma_load_2d(&tmB, sb, &full[stage], kb * BK, nb0);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -247,12 +306,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -260,58 +319,72 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
-          const uint32_t sb = sa + C::A_BYTES;
           const uint64_t da = umma_sdesc_sw128(sa);
-          const uint64_t db = umma_sdesc_sw128(sb);
+          const uint64_t db = umma_sdesc_sw128(sa + C::A_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // +32 B per K=16 step inside the 128 B swizzle atom (encoded >> 4)
-            umma_bf16(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
+            if constexpr (CG == 2) umma_bf16_cg2(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
+            else umma_bf16(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (CG == 2) umma_commit_cg2_mc(&empty[stage], 0x3);
+          else umma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (CG == 2) umma_commit_cg2_mc(&tfull[acc], 0x3);
+        else umma_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else {
+    const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-    const int row = q * 32 + lane;
+    EpiWarp e;
+    e.buf[0] = epi_smem + ew * 2 * kEpiBoxBytes;
+    e.buf[1] = e.buf[0] + kEpiBoxBytes;
+    e.cur = 0;
+    e.lane = lane;
+    const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
       const int64_t m_blk = tile % m_tiles;
       const int64_t n_blk = tile / m_tiles;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      const int64_t gm = m_blk * BM + row;
-      epilogue_tile<BN, EPI>(taddr, gm, gm < M, n_blk, N, ep);
+      e.row0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM + q * 32);
+      epilogue_tile<BN, EPI>(e, taddr, e.row0 + lane, M, n_blk, N, ep, s_norm, s_norm + 128, &tmC);
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (lane == 0) bulk_wait_all();
   }
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C::TMEM_COLS);
+    if constexpr (CG == 2) tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
+    else tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
 }
 
 // ---------------------------------------------------------------- host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
@@ -326,37 +399,43 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-int make_map(CUtensorMap* map, const void* ptr, int64_t inner, int64_t outer, int64_t ld_elems,
-             int box_outer) {
+// 2-D row-major map: inner = columns (elements), outer = rows, box = box_inner x box_outer, 128B swizzle.
+int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* ptr, int64_t inner, int64_t outer,
+             int64_t ld_elems, int box_inner, int box_outer) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return RDX_ERR_UNSUPPORTED;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld_elems) * esize};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? RDX_OK : RDX_ERR_INVALID_ARGUMENT;
 }
 
-template <int BN, int STAGES, int EPI>
+template <int BN, int EPI, int CG>
 int launch(const rdx_gemm_args& a, cudaStream_t stream) {
-  using C = Cfg<BN, STAGES>;
-  auto kern = gemm_kernel<BN, STAGES, EPI>;
+  using C = Cfg<BN, CG>;
+  auto kern = gemm_kernel<BN, EPI, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    if (CG == 2) RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     attr_set = true;
   }
-  CUtensorMap ma, mb;
-  int st = make_map(&ma, a.a, a.k, a.m, a.lda, BM);
+  CUtensorMap ma, mb, mc;
+  int st = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.a, a.k, a.m, a.lda, BK, BM);
   if (st) return st;
-  st = make_map(&mb, a.b, a.k, a.n, a.ldb, BN);
+  st = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, C::B_ROWS);
+  if (st) return st;
+  if (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
+    st = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.out, a.n, a.m, a.ldo, 32, 32);
+  } else {
+    const int64_t ncols = EPI == RDX_EPI_SWIGLU ? a.n / 2 : a.n;
+    st = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.out, ncols, a.m, a.ldo, 64, 32);
+  }
   if (st) return st;
   EpiParams ep;
-  ep.out = a.out;
-  ep.ldo = a.ldo;
   ep.qn = a.q_norm_w;
   ep.kn = a.k_norm_w;
   ep.rope = reinterpret_cast<const float2*>(a.rope_table);
@@ -364,17 +443,50 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   ep.q_dim = a.q_heads * a.head_dim;
   ep.kv_dim = a.kv_heads * a.head_dim;
   ep.eps = a.eps;
-  const int64_t tiles = ((a.m + BM - 1) / BM) * ((a.n + BN - 1) / BN);
-  const int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, kThreads, C::SMEM, stream>>>(ma, mb, a.m, a.n, a.k, ep);
-  RDX_LAUNCH_CHECK();
+  const int64_t tiles = ((a.m + BM * CG - 1) / (BM * CG)) * ((a.n + BN - 1) / BN);
+  const int64_t units_max = num_sms() / CG;
+  const int64_t units = tiles < units_max ? tiles : units_max;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(units * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, a.m, a.n, a.k, ep));
   return RDX_OK;
 }
 
 template <int EPI>
-int dispatch_bn(const rdx_gemm_args& a, int bn, cudaStream_t s) {
-  if (bn == 256) return launch<256, 4, EPI>(a, s);
-  return launch<128, 6, EPI>(a, s);
+int dispatch(const rdx_gemm_args& a, int bn, int cg, cudaStream_t s) {
+  if (cg == 2) return bn == 256 ? launch<256, EPI, 2>(a, s) : launch<128, EPI, 2>(a, s);
+  return bn == 256 ? launch<256, EPI, 1>(a, s) : launch<128, EPI, 1>(a, s);
+}
+
+// Pick (CG, BN): fewest tile rounds x tile width, preferring the CTA pair.
+void choose_shape(const rdx_gemm_args& a, int* bn_out, int* cg_out) {
+  const int cg = a.m > BM ? 2 : 1;
+  int best_bn = 256;
+  double best_cost = 1e30;
+  for (int bn : {256, 128}) {
+    if (a.block_n && bn != a.block_n) continue;
+    if (a.epi == RDX_EPI_QKV && (bn % a.head_dim)) continue;
+    const int64_t tiles = ((a.m + BM * cg - 1) / (BM * cg)) * ((a.n + bn - 1) / bn);
+    const int64_t units = num_sms() / cg;
+    const int64_t rounds = (tiles + units - 1) / units;
+    const double cost = static_cast<double>(rounds) * (bn + 64);  // per-tile fixed cost ~ 64 columns
+    if (cost < best_cost) {
+      best_cost = cost;
+      best_bn = bn;
+    }
+  }
+  *bn_out = best_bn;
+  *cg_out = cg;
 }
 
 }  // namespace gemm
@@ -390,36 +502,34 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
   if ((a.k % 8) || (a.lda % 8) || (a.ldb % 8) || a.lda < a.k || a.ldb < a.k) return RDX_ERR_SHAPE_MISMATCH;
   if (a.m >= (int64_t(1) << 31) || a.n >= (int64_t(1) << 31)) return RDX_ERR_CAPACITY_EXCEEDED;
   if (!a.a || !a.b || !a.out) return RDX_ERR_INVALID_ARGUMENT;
-  if ((reinterpret_cast<uintptr_t>(a.a) | reinterpret_cast<uintptr_t>(a.b) |
-       reinterpret_cast<uintptr_t>(a.out)) & 15)
+  if ((reinterpret_cast<uintptr_t>(a.a) | reinterpret_cast<uintptr_t>(a.b) | reinterpret_cast<uintptr_t>(a.out)) &
+      15)
     return RDX_ERR_INVALID_ARGUMENT;
-  int bn = a.block_n;
-  if (bn == 0) {
-    const int64_t m_tiles = (a.m + BM - 1) / BM;
-    bn = (m_tiles * ((a.n + 255) / 256) >= 2 * num_sms()) ? 256 : 128;
-  }
-  if (bn != 128 && bn != 256) return RDX_ERR_INVALID_ARGUMENT;
+  if (a.block_n != 0 && a.block_n != 128 && a.block_n != 256) return RDX_ERR_INVALID_ARGUMENT;
+  int bn = 256, cg = 1;
+  if (a.epi == RDX_EPI_QKV && (a.head_dim <= 0 || a.head_dim % 16 || a.head_dim > 128))
+    return RDX_ERR_SHAPE_MISMATCH;
+  choose_shape(a, &bn, &cg);
   cudaStream_t s = as_stream(stream);
   switch (a.epi) {
     case RDX_EPI_STORE_BF16:
       if (a.ldo % 8 || a.ldo < a.n) return RDX_ERR_SHAPE_MISMATCH;
-      return dispatch_bn<RDX_EPI_STORE_BF16>(a, bn, s);
+      return dispatch<RDX_EPI_STORE_BF16>(a, bn, cg, s);
     case RDX_EPI_STORE_F32:
       if (a.ldo % 4 || a.ldo < a.n) return RDX_ERR_SHAPE_MISMATCH;
-      return dispatch_bn<RDX_EPI_STORE_F32>(a, bn, s);
+      return dispatch<RDX_EPI_STORE_F32>(a, bn, cg, s);
     case RDX_EPI_RESID_F32:
       if (a.ldo % 4 || a.ldo < a.n) return RDX_ERR_SHAPE_MISMATCH;
-      return dispatch_bn<RDX_EPI_RESID_F32>(a, bn, s);
+      return dispatch<RDX_EPI_RESID_F32>(a, bn, cg, s);
     case RDX_EPI_SWIGLU:
       if (a.n % (2 * kSwigluUnit) || a.ldo % 8 || a.ldo < a.n / 2) return RDX_ERR_SHAPE_MISMATCH;
-      return dispatch_bn<RDX_EPI_SWIGLU>(a, bn, s);
+      return dispatch<RDX_EPI_SWIGLU>(a, bn, cg, s);
     case RDX_EPI_QKV: {
-      const int hd = a.head_dim;
-      if (hd <= 0 || hd % 16 || hd > 128 || bn % hd) return RDX_ERR_SHAPE_MISMATCH;
-      if (a.n != static_cast<int64_t>(a.q_heads + 2 * a.kv_heads) * hd) return RDX_ERR_SHAPE_MISMATCH;
+      if (bn % a.head_dim) return RDX_ERR_SHAPE_MISMATCH;
+      if (a.n != static_cast<int64_t>(a.q_heads + 2 * a.kv_heads) * a.head_dim) return RDX_ERR_SHAPE_MISMATCH;
       if (!a.q_norm_w || !a.k_norm_w || !a.rope_table) return RDX_ERR_INVALID_ARGUMENT;
       if (a.ldo % 8 || a.ldo < a.n) return RDX_ERR_SHAPE_MISMATCH;
-      return dispatch_bn<RDX_EPI_QKV>(a, bn, s);
+      return dispatch<RDX_EPI_QKV>(a, bn, cg, s);
     }
     default:
       return RDX_ERR_INVALID_ARGUMENT;

@@ -135,6 +135,39 @@ rmsnorm_rows_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_t* _
   }
 }
 
+// Single pass: the row lives in registers (V float4 per lane, d = 128 * V), one
+// HBM read and one write per element.
+template <int V>
+__global__ void __launch_bounds__(256)
+rmsnorm_rows_reg_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_t* __restrict__ rows,
+                        int64_t n_rows, const float* __restrict__ w, float eps, __nv_bfloat16* __restrict__ out,
+                        int64_t ld_out) {
+  constexpr int D = 128 * V;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t j = warp0; j < n_rows; j += nwarps) {
+    const int64_t r = rows ? static_cast<int64_t>(__ldg(rows + j)) : j;
+    const float4* xr = reinterpret_cast<const float4*>(x + r * ld_x);
+    float4 v[V];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      v[i] = __ldcs(xr + lane + 32 * i);
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / static_cast<float>(D) + eps);
+    uint2* orow = reinterpret_cast<uint2*>(out + j * ld_out);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * i);
+      orow[lane + 32 * i] = make_uint2(pack_bf16x2(v[i].x * inv * g.x, v[i].y * inv * g.y),
+                                       pack_bf16x2(v[i].z * inv * g.z, v[i].w * inv * g.w));
+    }
+  }
+}
+
 __global__ void rope_table_kernel(const uint32_t* __restrict__ pos, int64_t n_rows, int half,
                                   double theta, int head_dim, float2* __restrict__ table) {
   const int64_t total = n_rows * half;
@@ -220,8 +253,20 @@ extern "C" int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* ro
   if (n_rows < 0 || d <= 0 || (d % 8) != 0 || (ld_x % 4) != 0 || (ld_out % 8) != 0)
     return RDX_ERR_SHAPE_MISMATCH;
   if (n_rows == 0) return RDX_OK;
-  rmsnorm_rows_kernel<<<grid_for_rows(n_rows, 8), 256, 0, as_stream(stream)>>>(
-      x, ld_x, rows, n_rows, d, w, eps, static_cast<__nv_bfloat16*>(out_bf16), ld_out);
+  const int grid = grid_for_rows(n_rows, 8);
+  cudaStream_t st = as_stream(stream);
+  __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out_bf16);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) == 0;
+  switch (aligned ? d : 0) {
+    case 1024: rmsnorm_rows_reg_kernel<8><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 2048: rmsnorm_rows_reg_kernel<16><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 2560: rmsnorm_rows_reg_kernel<20><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 4096: rmsnorm_rows_reg_kernel<32><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 512: rmsnorm_rows_reg_kernel<4><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 256: rmsnorm_rows_reg_kernel<2><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    default:
+      rmsnorm_rows_kernel<<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, d, w, eps, o, ld_out);
+  }
   RDX_LAUNCH_CHECK();
   return RDX_OK;
 }

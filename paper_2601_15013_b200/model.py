@@ -280,6 +280,7 @@ class DeviceBatch:
     n: int
     b: int
     max_len: int
+    max_token: int = -1  # host-known max token id (-1: unknown, checked on device)
 
     @classmethod
     def from_batch(cls, batch: RaggedBatch, device="cuda", non_blocking=False):
@@ -288,8 +289,9 @@ class DeviceBatch:
         tok, pos, cu = upload_batch(batch, device)
         cu_host = np.asarray(batch.cu_seqlens, dtype=np.int64)
         lens = np.diff(cu_host)
+        mt = int(batch.token_ids.max()) if batch.num_tokens else -1
         return cls(tok, pos, cu, cu.to(torch.int32), cu_host, int(batch.num_tokens),
-                   int(batch.num_sequences), int(lens.max()) if lens.size else 0)
+                   int(batch.num_sequences), int(lens.max()) if lens.size else 0, mt)
 
 
 @dataclass
@@ -303,6 +305,7 @@ class _Layout:
     max_q: int
     suffix_ok: bool
     dedup: bool
+    cu_q_host: object = None
 
 
 def _flash_varlen(q, k, v, cu_q, cu_k, max_q, max_k, scale):
@@ -314,17 +317,40 @@ def _flash_varlen(q, k, v, cu_q, cu_k, max_q, max_k, scale):
                                   softmax_scale=scale, causal=True)
 
 
-class RadixQwen3:
-    """Qwen3 prefill whose position-wise work runs on the compact rows."""
+class _Graph:
+    """One captured prefill body plus its static input buffers."""
 
-    def __init__(self, config: ModelConfig, weights: DeviceWeights):
+    def __init__(self, graph, inputs: dict, output):
+        self.graph = graph
+        self.inputs = inputs
+        self.output = output
+
+
+class RadixQwen3:
+    """Qwen3 prefill whose position-wise work runs on the compact rows.
+
+    ``prefill`` resolves the plan (GPU planner: one small D2H read for N'),
+    then runs the layer stack.  With ``use_graphs=True`` the layer stack is
+    captured once per shape key (rows, tokens, sequences, max lengths, modes)
+    into a CUDA graph and replayed, removing per-launch host overhead; pad
+    plans to a bucket (``pad_plan``) to bound the number of distinct keys.
+    """
+
+    def __init__(self, config: ModelConfig, weights: DeviceWeights, use_graphs: bool = False):
         _check_kernel_shapes(config)
         self.config = config
         self.w = weights
         self.di_pad = padded_intermediate(config)
-        self.gemm_hook = None  # optional callable(name, fn) used by bench.py for per-GEMM events
+        self.use_graphs = use_graphs
+        self.op_hook = None  # optional callable(name, launch_fn, flops) (bench.py per-op CUDA events)
+        self._graphs: dict = {}
 
-    # ------------------------------------------------------------ kernels
+    # ------------------------------------------------------------ launches
+    def _op(self, name, fn, flops=0.0):
+        if self.op_hook is not None:
+            return self.op_hook(name, fn, flops)
+        return fn()
+
     def _gemm(self, name, a, w, epi, out, *, m, stream, qkv=False, rope=None, layer=None):
         cfg = self.config
         args = _native.GemmArgs()
@@ -352,18 +378,25 @@ class RadixQwen3:
         def launch():
             _native.check(lib.rdx_gemm(args, stream), f"rdx_gemm[{name}]")
 
-        if self.gemm_hook is not None:
-            self.gemm_hook(name, launch, m, args.n, args.k)
-        else:
-            launch()
+        self._op("gemm." + name, launch, 2.0 * m * args.n * args.k)
 
     def _rmsnorm(self, x, w, out, rows=None, n_rows=None, stream=None):
         lib = _native.lib()
         n_rows = x.shape[0] if n_rows is None else n_rows
-        code = lib.rdx_rmsnorm_rows(x.data_ptr(), x.stride(0), None if rows is None else rows.data_ptr(),
-                                    n_rows, x.shape[1], w.data_ptr(), self.config.norm_eps,
-                                    out.data_ptr(), out.stride(0), stream)
-        _native.check(code, "rdx_rmsnorm_rows")
+
+        def launch():
+            code = lib.rdx_rmsnorm_rows(x.data_ptr(), x.stride(0), None if rows is None else rows.data_ptr(),
+                                        n_rows, x.shape[1], w.data_ptr(), self.config.norm_eps,
+                                        out.data_ptr(), out.stride(0), stream)
+            _native.check(code, "rdx_rmsnorm_rows")
+
+        self._op("rmsnorm", launch)
+
+    def _gather(self, name, x, idx, stream_obj):
+        return self._op(name, lambda: gather_rows_device(x, idx, stream=stream_obj))
+
+    def _attn(self, q, k, v, cu_q, cu_k, max_q, max_k, scale, flops):
+        return self._op("attention", lambda: _flash_varlen(q, k, v, cu_q, cu_k, max_q, max_k, scale), flops)
 
     # ------------------------------------------------------------ layout
     def _layout(self, db: DeviceBatch, plan, attention: str) -> _Layout:
@@ -372,12 +405,12 @@ class RadixQwen3:
         if plan is None:
             return _Layout(db.n, db.n, None, None, db.pos, db.cu32, db.max_len, True, False)
         if isinstance(plan, str) and plan == "auto":
-            plan = build_plan_device(db.tok, db.pos, db.cu)
+            plan = self._op("plan_build", lambda: build_plan_device(db.tok, db.pos, db.cu))
         if isinstance(plan, DevicePlan):
             if plan.n_original != db.n or plan.scatter.shape[0] != db.n:
                 raise PlanBatchMismatch(f"plan built for {plan.n_original} tokens, batch has {db.n}")
             return _Layout(plan.n_padded, plan.n_compact, plan.gather, plan.scatter, plan.compact_positions,
-                           plan.cu_q, plan.max_q_len, True, True)
+                           plan.cu_q, plan.max_q_len, True, True, plan.cu_q_host)
         if isinstance(plan, CompactionPlan):
             if plan.n_original != db.n:
                 raise PlanBatchMismatch(f"plan built for {plan.n_original} tokens, batch has {db.n}")
@@ -392,122 +425,190 @@ class RadixQwen3:
                 return _Layout(plan.n_padded, plan.n_compact, g, s, p, None, 0, False, True)
             cu_q32 = torch.from_numpy(cu_q.astype(np.int32)).to(dev)
             max_q = int(np.diff(cu_q).max()) if cu_q.size > 1 else 0
-            return _Layout(plan.n_padded, plan.n_compact, g, s, p, cu_q32, max_q, True, True)
+            return _Layout(plan.n_padded, plan.n_compact, g, s, p, cu_q32, max_q, True, True, cu_q)
         raise TypeError(f"unsupported plan type {type(plan).__name__}")
 
     # ------------------------------------------------------------ forward
     def prefill(self, db: DeviceBatch, plan=None, *, attention: str = "suffix", logits: str = "all",
                 ledger: FlopLedger | None = None, stream=None):
         """Run the prefill; returns fp32 logits [N, vocab] ("all") or [B, vocab] ("last")."""
-        import torch
-
         if attention not in ("suffix", "full"):
             raise ValueError("attention must be 'suffix' or 'full'")
         if logits not in ("all", "last"):
             raise ValueError("logits must be 'all' or 'last'")
-        cfg, T = self.config, self.w.t
+        if db.max_token >= self.config.vocab_size:
+            from .errors import IndexOutOfRange
+
+            raise IndexOutOfRange("token id outside [0, vocab_size)")
         if ledger is None:
             ledger = FlopLedger()
         lay = self._layout(db, plan, attention)
-        use_suffix = lay.dedup and attention == "suffix" and lay.suffix_ok
+        mode = "plain" if not lay.dedup else ("suffix" if attention == "suffix" and lay.suffix_ok else "full")
+        self._fill_ledger(ledger, lay, db, mode, logits)
+        self._att_pairs = self._attention_pairs(db, lay, mode)
+        if not self.use_graphs or self.op_hook is not None:
+            out, err = self._body(db.tok, lay.gather, lay.scatter, lay.positions, db.cu32, db.cu, lay.cu_q32,
+                                  lay.m, db.n, db.b, lay.n_compact, lay.max_q, db.max_len, mode, logits, stream)
+            if db.max_token < 0 and int(err.item()):
+                from .errors import IndexOutOfRange
+
+                raise IndexOutOfRange("token id outside [0, vocab_size)")
+            return out
+        return self._replay(db, lay, mode, logits, stream)
+
+    def _replay(self, db, lay, mode, logits, stream):
+        import torch
+
+        key = (lay.m, db.n, db.b, lay.n_compact, lay.max_q, db.max_len, mode, logits)
+        g = self._graphs.get(key)
+        dyn = {"tok": db.tok, "gather": lay.gather, "scatter": lay.scatter, "pos": lay.positions,
+               "cu32": db.cu32, "cu": db.cu, "cu_q32": lay.cu_q32}
+        if g is None:
+            inputs = {k: (None if v is None else v.clone()) for k, v in dyn.items()}
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):  # warm-up outside capture (allocator, lazy init)
+                self._body(inputs["tok"], inputs["gather"], inputs["scatter"], inputs["pos"], inputs["cu32"],
+                           inputs["cu"], inputs["cu_q32"], lay.m, db.n, db.b, lay.n_compact, lay.max_q,
+                           db.max_len, mode, logits, None)
+            torch.cuda.current_stream().wait_stream(side)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                out, _ = self._body(inputs["tok"], inputs["gather"], inputs["scatter"], inputs["pos"],
+                                    inputs["cu32"], inputs["cu"], inputs["cu_q32"], lay.m, db.n, db.b,
+                                    lay.n_compact, lay.max_q, db.max_len, mode, logits, None)
+            g = _Graph(graph, inputs, out)
+            self._graphs[key] = g
+        for k, v in dyn.items():
+            if v is not None:
+                g.inputs[k].copy_(v, non_blocking=True)
+        g.graph.replay()
+        return g.output
+
+    def _fill_ledger(self, ledger, lay, db, mode, logits):
+        """Row counters exactly as the reference's forward records them (model.py:331-411)."""
+        m, n = lay.m, db.n
+        if lay.dedup:
+            ledger.index_copy(m)
+        ledger.positionwise("embed", m)
+        for i in range(self.config.num_layers):
+            ledger.positionwise(f"l{i}.ln1", m)
+            ledger.positionwise(f"l{i}.qkv_proj", m)
+            ledger.positionwise(f"l{i}.qk_norm_rope", m)
+            if mode == "plain":
+                ledger.attention(n)
+            elif mode == "suffix":
+                ledger.index_copy(2 * n)          # K/V only
+                ledger.attention(lay.n_compact)   # query rows stay compact
+            else:
+                ledger.index_copy(3 * n)
+                ledger.attention(n)
+                ledger.index_copy(m)
+            for ph in ("o_proj", "attn_residual", "mlp", "mlp_residual"):
+                ledger.positionwise(f"l{i}.{ph}", m)
+        rows = db.b if logits == "last" else m
+        ledger.positionwise("final_norm", rows)
+        ledger.positionwise("lm_head", rows)
+        if lay.dedup and logits == "all":
+            ledger.index_copy(n)
+
+    @staticmethod
+    def _attention_pairs(db, lay, mode) -> float:
+        """Causal (query, key) pairs per head (host arithmetic, for FLOP accounting)."""
+        lens = np.diff(db.cu_host).astype(np.float64)
+        full = float(np.sum(lens * (lens + 1) / 2))
+        if mode != "suffix":
+            return full
+        cu_q = getattr(lay, "cu_q_host", None)
+        if cu_q is None:
+            return full
+        lcp = lens - np.diff(cu_q)
+        return float(np.sum(lens * (lens + 1) / 2 - lcp * (lcp + 1) / 2))
+
+    def _body(self, tok, gather, scatter, positions, cu32, cu64, cu_q32, m, n, b, n_compact, max_q, max_k,
+              mode, logits, stream):
+        """The layer stack as pure launches (CUDA-graph capturable)."""
+        import torch
+
+        cfg, T = self.config, self.w.t
         lib = _native.lib()
         st = _native.stream_handle(stream)
-        dev = db.tok.device
-        m, n = lay.m, db.n
+        dev = tok.device
         d, hd, H, KV = cfg.hidden_size, cfg.head_dim, cfg.num_heads, cfg.num_kv_heads
         qd, kvd = cfg.q_dim, cfg.kv_dim
         bf = torch.bfloat16
-        if lay.dedup:
-            ledger.index_copy(m)
-
         h = torch.empty(m, d, dtype=torch.float32, device=dev)
         hn = torch.empty(m, d, dtype=bf, device=dev)
         err = torch.zeros(1, dtype=torch.int32, device=dev)
-        code = lib.rdx_embed_rmsnorm(db.tok.data_ptr(), None if lay.gather is None else lay.gather.data_ptr(),
-                                     m, T["embed"].data_ptr(), cfg.vocab_size, d,
-                                     T["layers.0.ln1"].data_ptr(), cfg.norm_eps, h.data_ptr(),
-                                     hn.data_ptr(), err.data_ptr(), st)
-        _native.check(code, "rdx_embed_rmsnorm")
-        ledger.positionwise("embed", m)
+
+        def embed():
+            code = lib.rdx_embed_rmsnorm(tok.data_ptr(), None if gather is None else gather.data_ptr(), m,
+                                         T["embed"].data_ptr(), cfg.vocab_size, d, T["layers.0.ln1"].data_ptr(),
+                                         cfg.norm_eps, h.data_ptr(), hn.data_ptr(), err.data_ptr(), st)
+            _native.check(code, "rdx_embed_rmsnorm")
+
+        self._op("embed_rmsnorm", embed)
         rope = torch.empty(m, hd // 2, 2, dtype=torch.float32, device=dev)
-        _native.check(lib.rdx_rope_table(lay.positions.data_ptr(), m, hd, float(cfg.rope_theta),
-                                         rope.data_ptr(), st), "rdx_rope_table")
+
+        def rope_fn():
+            _native.check(lib.rdx_rope_table(positions.data_ptr(), m, hd, float(cfg.rope_theta), rope.data_ptr(),
+                                             st), "rdx_rope_table")
+
+        self._op("rope_table", rope_fn)
         qkv = torch.empty(m, qd + 2 * kvd, dtype=bf, device=dev)
         act = torch.empty(m, self.di_pad, dtype=bf, device=dev)
         scale = 1.0 / math.sqrt(hd)
         last_rows = None
         if logits == "last":
-            ends = db.cu[1:] - 1
-            last_rows = (lay.scatter[ends] if lay.dedup else ends).to(torch.int32).contiguous()
+            ends = cu64[1:] - 1
+            last_rows = (scatter[ends] if mode != "plain" else ends).to(torch.int32).contiguous()
+        att_flops = 4.0 * qd * getattr(self, "_att_pairs", 0.0)
 
         for i in range(cfg.num_layers):
             pre = f"layers.{i}."
-            ledger.positionwise(f"l{i}.ln1", m)
-            self._gemm("qkv", hn, T[pre + "w_qkv"], _native.EPI_QKV, qkv, m=m, stream=st, qkv=True,
-                       rope=rope, layer=pre)
-            ledger.positionwise(f"l{i}.qkv_proj", m)
-            ledger.positionwise(f"l{i}.qk_norm_rope", m)
-            if not lay.dedup:
-                a = _flash_varlen(qkv[:, :qd].view(m, H, hd), qkv[:, qd:qd + kvd].view(m, KV, hd),
-                                  qkv[:, qd + kvd:].view(m, KV, hd), db.cu32, db.cu32, db.max_len,
-                                  db.max_len, scale)
-                ledger.attention(n)
-            elif use_suffix:
-                kv_full = gather_rows_device(qkv[:, qd:], lay.scatter, stream=stream)
-                ledger.index_copy(2 * n)
-                a = _flash_varlen(qkv[:, :qd].view(m, H, hd), kv_full[:, :kvd].view(n, KV, hd),
-                                  kv_full[:, kvd:].view(n, KV, hd), lay.cu_q32, db.cu32, max(lay.max_q, 1),
-                                  db.max_len, scale)
-                if m > lay.n_compact:
-                    a[lay.n_compact:] = 0
-                ledger.attention(lay.n_compact)
+            self._gemm("qkv", hn, T[pre + "w_qkv"], _native.EPI_QKV, qkv, m=m, stream=st, qkv=True, rope=rope,
+                       layer=pre)
+            if mode == "plain":
+                a = self._attn(qkv[:, :qd].view(m, H, hd), qkv[:, qd:qd + kvd].view(m, KV, hd),
+                               qkv[:, qd + kvd:].view(m, KV, hd), cu32, cu32, max_k, max_k, scale, att_flops)
+            elif mode == "suffix":
+                kv_full = self._gather("scatter_kv", qkv[:, qd:], scatter, stream)
+                a = self._attn(qkv[:, :qd].view(m, H, hd), kv_full[:, :kvd].view(n, KV, hd),
+                               kv_full[:, kvd:].view(n, KV, hd), cu_q32, cu32, max(max_q, 1), max_k, scale,
+                               att_flops)
+                if m > n_compact:
+                    a[n_compact:] = 0
             else:
-                qkv_full = gather_rows_device(qkv, lay.scatter, stream=stream)
-                ledger.index_copy(3 * n)
-                a_full = _flash_varlen(qkv_full[:, :qd].view(n, H, hd), qkv_full[:, qd:qd + kvd].view(n, KV, hd),
-                                       qkv_full[:, qd + kvd:].view(n, KV, hd), db.cu32, db.cu32, db.max_len,
-                                       db.max_len, scale)
-                ledger.attention(n)
-                a = gather_rows_device(a_full.view(n, qd), lay.gather, stream=stream)
-                ledger.index_copy(m)
+                qkv_full = self._gather("scatter_qkv", qkv, scatter, stream)
+                a_full = self._attn(qkv_full[:, :qd].view(n, H, hd), qkv_full[:, qd:qd + kvd].view(n, KV, hd),
+                                    qkv_full[:, qd + kvd:].view(n, KV, hd), cu32, cu32, max_k, max_k, scale,
+                                    att_flops)
+                a = self._gather("gather_attn", a_full.view(n, qd), gather, stream)
             a = a.reshape(m, qd)
             self._gemm("o_proj", a, T[pre + "wo"], _native.EPI_RESID_F32, h, m=m, stream=st)
-            ledger.positionwise(f"l{i}.o_proj", m)
-            ledger.positionwise(f"l{i}.attn_residual", m)
             self._rmsnorm(h, T[pre + "ln2"], hn, stream=st)
             self._gemm("gate_up", hn, T[pre + "w_gu"], _native.EPI_SWIGLU, act, m=m, stream=st)
             self._gemm("down", act, T[pre + "w_down"], _native.EPI_RESID_F32, h, m=m, stream=st)
-            ledger.positionwise(f"l{i}.mlp", m)
-            ledger.positionwise(f"l{i}.mlp_residual", m)
             if i + 1 < cfg.num_layers:
                 self._rmsnorm(h, T[f"layers.{i + 1}.ln1"], hn, stream=st)
 
         vocab = cfg.vocab_size
         vpad = -(-vocab // 8) * 8  # 16-byte aligned logits rows
         if logits == "last":
-            hl = torch.empty(db.b, d, dtype=bf, device=dev)
-            self._rmsnorm(h, T["final_norm"], hl, rows=last_rows, n_rows=db.b, stream=st)
-            ledger.positionwise("final_norm", db.b)
-            out = torch.empty(db.b, vpad, dtype=torch.float32, device=dev)[:, :vocab]
-            self._gemm("lm_head", hl, T["lm_head"], _native.EPI_STORE_F32, out, m=db.b, stream=st)
-            ledger.positionwise("lm_head", db.b)
+            hl = torch.empty(b, d, dtype=bf, device=dev)
+            self._rmsnorm(h, T["final_norm"], hl, rows=last_rows, n_rows=b, stream=st)
+            out = torch.empty(b, vpad, dtype=torch.float32, device=dev)[:, :vocab]
+            self._gemm("lm_head", hl, T["lm_head"], _native.EPI_STORE_F32, out, m=b, stream=st)
             result = out if vpad == vocab else out.contiguous()
         else:
             self._rmsnorm(h, T["final_norm"], hn, stream=st)
-            ledger.positionwise("final_norm", m)
             out = torch.empty(m, vpad, dtype=torch.float32, device=dev)[:, :vocab]
             self._gemm("lm_head", hn, T["lm_head"], _native.EPI_STORE_F32, out, m=m, stream=st)
-            ledger.positionwise("lm_head", m)
-            if lay.dedup:
-                result = gather_rows_device(out, lay.scatter, stream=stream)
-                ledger.index_copy(n)
+            if mode != "plain":
+                result = self._gather("scatter_logits", out, scatter, stream)
             else:
                 result = out if vpad == vocab else out.contiguous()
-        if int(err.item()):
-            from .errors import IndexOutOfRange
-
-            raise IndexOutOfRange("token id outside [0, vocab_size)")
-        return result
+        return result, err
 
 
 _MODEL_CACHE: dict = {}
