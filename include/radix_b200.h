@@ -26,6 +26,8 @@
  *                            model.py:356-366 (q/k norm + RoPE), 387-389 (o-proj
  *                            + residual), 394-397 (SwiGLU), 397-399 (down +
  *                            residual)
+ *   rdx_attention         <- scatter_rows(q/k/v) + _attention_forward + gather_rows
+ *                            (model.py:368-383, 228-265), boundary fused into loads
  *   rdx_rerank_scores     <- last-token scoring contract (no reference
  *                            counterpart)
  */
@@ -166,6 +168,21 @@ typedef struct rdx_gemm_args {
 } rdx_gemm_args;
 
 int rdx_gemm(const rdx_gemm_args* args, void* stream);
+
+/* ---------------------------------------------------------------------
+ * Causal GQA prefill attention on tcgen05/TMEM with the RadixMLP attention
+ * boundary fused into its loads (replaces model.py:368-383 + 228-265):
+ *   query i of sequence s   = row cu_q[s] + i of qkv (compact), position
+ *                             lcp_s + i with lcp_s = L_s - (cu_q[s+1]-cu_q[s])
+ *   key/value j of s        = row scatter[cu[s] + j] of qkv (scatter == NULL:
+ *                             row cu[s] + j, i.e. plain / full layout)
+ *   out[cu_q[s] + i, head]  = softmax(q k^T * scale, causal) v   (bf16)
+ * qkv rows are [q heads | k heads | v heads] x head_dim (the QKV GEMM output);
+ * head_dim <= 128, multiple of 8; heads % kv_heads == 0.
+ * --------------------------------------------------------------------- */
+int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, const int32_t* scatter, const int32_t* cu,
+                  const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len, int32_t heads, int32_t kv_heads,
+                  int32_t head_dim, float softmax_scale, void* out_bf16, int64_t ld_out, void* stream);
 
 /* ---------------------------------------------------------------------
  * Reranker scores from last-token logits (fp32 [B, ld]):

@@ -27,10 +27,10 @@ namespace gemm {
 
 constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B atom row
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 8;   // 2 per TMEM lane quarter, each owning half of the tile's columns
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr int kSwigluUnit = 64;   // gate/up interleave unit (columns)
-constexpr int kEpiBoxBytes = 4096;  // 32 rows x 128 B staging box (SWIZZLE_128B)
+constexpr int kSwigluUnit = 64;     // gate/up interleave unit (columns)
+constexpr int kEpiBoxBytes = 4096;  // staging box: 32 rows x 32 cols (bf16: 64 B rows, f32: 128 B rows)
 
 struct EpiParams {
   const float* qn;
@@ -64,15 +64,13 @@ struct EpiWarp {
   int32_t row0;  // first global row of this warp's 32-row slab
 };
 
-// Write this lane's 128-byte row into the swizzled box and TMA-store it at (c0, row0).
-__device__ __forceinline__ void epi_emit(EpiWarp& e, const uint32_t (&w)[32], const CUtensorMap* map, int32_t c0,
-                                         bool reduce_add) {
-  if (e.lane == 0) bulk_wait_read<1>();  // the box written two emits ago has been read
+__device__ __forceinline__ uint32_t epi_acquire(EpiWarp& e) {
+  if (e.lane == 0) bulk_wait_read<1>();  // the box written two emits ago has been read by its TMA store
   __syncwarp();
-  const uint32_t base = smem_u32(e.buf[e.cur]) + e.lane * 128;
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    st_shared_v4(base + ((j ^ (e.lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  return smem_u32(e.buf[e.cur]);
+}
+
+__device__ __forceinline__ void epi_issue(EpiWarp& e, const CUtensorMap* map, int32_t c0, bool reduce_add) {
   fence_proxy_async_smem();
   __syncwarp();
   if (e.lane == 0) {
@@ -83,133 +81,169 @@ __device__ __forceinline__ void epi_emit(EpiWarp& e, const uint32_t (&w)[32], co
   e.cur ^= 1;
 }
 
-__device__ __forceinline__ void pack64(const float* v, uint32_t (&w)[32]) {
+// 32 bf16 columns of this lane's row -> 64 B row of a SWIZZLE_64B box -> TMA store at (c0, row0).
+__device__ __forceinline__ void emit_bf16x32(EpiWarp& e, const float* v, const CUtensorMap* map, int32_t c0) {
+  uint32_t w[16];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+  for (int j = 0; j < 16; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+  const uint32_t base = epi_acquire(e) + e.lane * 64;
+  const int sw = (e.lane >> 1) & 3;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) st_shared_v4(base + ((j ^ sw) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  epi_issue(e, map, c0, false);
 }
 
-__device__ __forceinline__ void bits32(const float* v, uint32_t (&w)[32]) {
+// 32 fp32 columns -> 128 B row of a SWIZZLE_128B box -> TMA store or reduce-add.
+__device__ __forceinline__ void emit_f32x32(EpiWarp& e, const float* v, const CUtensorMap* map, int32_t c0,
+                                            bool reduce_add) {
+  const uint32_t base = epi_acquire(e) + e.lane * 128;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
+  for (int j = 0; j < 8; ++j)
+    st_shared_v4(base + ((j ^ (e.lane & 7)) << 4), __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                 __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+  epi_issue(e, map, c0, reduce_add);
 }
 
-// q/k head: RMSNorm over HD (weight w from smem), then rotate-half RoPE.
-template <int HD>
-__device__ __forceinline__ void norm_rope(float* x, const float* w, const float2* __restrict__ rope, float eps) {
-  float ss = 0.f;
+// RoPE on a (first-half, second-half) pair of 32-column slices of a normalised head:
+// x1 = cols [c, c+32), x2 = cols [c+H, c+H+32) of a head of width 2H (model.py:363-365).
+__device__ __forceinline__ void rope_pair32(float* x1, float* x2, const float* w1, const float* w2, float inv,
+                                            const float2* __restrict__ cs) {
 #pragma unroll
-  for (int j = 0; j < HD; ++j) ss += x[j] * x[j];
-  const float inv = rsqrtf(ss / static_cast<float>(HD) + eps);
-  constexpr int H = HD / 2;
+  for (int j = 0; j < 32; j += 2) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(cs + j));
 #pragma unroll
-  for (int j = 0; j < H; j += 2) {
-    const float4 cs = __ldg(reinterpret_cast<const float4*>(rope + j));  // (cos_j, sin_j, cos_j+1, sin_j+1)
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const float c = t ? cs.z : cs.x, s = t ? cs.w : cs.y;
-      const float a = x[j + t] * inv * w[j + t];
-      const float b = x[j + t + H] * inv * w[j + t + H];
-      x[j + t] = a * c - b * s;
-      x[j + t + H] = b * c + a * s;
+    for (int u = 0; u < 2; ++u) {
+      const float c = u ? t.z : t.x, s = u ? t.w : t.y;
+      const float a = x1[j + u] * inv * w1[j + u];
+      const float b = x2[j + u] * inv * w2[j + u];
+      x1[j + u] = a * c - b * s;
+      x2[j + u] = b * c + a * s;
     }
   }
 }
 
+// QKV epilogue for this warp's column range [c_lo, c_hi) of the tile (multiple of HD).
 template <int HD>
-__device__ __forceinline__ void qkv_tile(EpiWarp& e, uint32_t taddr, int64_t n0, int64_t N, const EpiParams& ep,
-                                         const float* s_qn, const float* s_kn, const float2* rope_row,
-                                         const CUtensorMap* map, int BN) {
+__device__ __forceinline__ void qkv_cols(EpiWarp& e, uint32_t taddr, int64_t n0, int c_lo, int c_hi, int64_t N,
+                                         const EpiParams& ep, const float* s_qn, const float* s_kn,
+                                         const float2* rope_row, const CUtensorMap* map) {
   if constexpr (HD >= 64) {
-    for (int h0 = 0; h0 < BN; h0 += HD) {
+    constexpr int H = HD / 2;
+#pragma unroll 1
+    for (int h0 = c_lo; h0 < c_hi; h0 += HD) {
       const int64_t col0 = n0 + h0;
       if (col0 >= N) break;
-      float x[HD];
-#pragma unroll
-      for (int c = 0; c < HD; c += 32) tmem_ld32p(taddr + h0 + c, x + c);
-      tmem_wait_ld();
       const int kind = col0 < ep.q_dim ? 0 : (col0 < ep.q_dim + ep.kv_dim ? 1 : 2);
-      if (kind < 2) norm_rope<HD>(x, kind == 0 ? s_qn : s_kn, rope_row, ep.eps);
+      if (kind == 2) {
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          float v[32];
+          tmem_ld32p(taddr + h0 + c, v);
+          tmem_wait_ld();
+          emit_bf16x32(e, v, map, static_cast<int32_t>(col0 + c));
+        }
+        continue;
+      }
+      const float* w = kind == 0 ? s_qn : s_kn;
+      float ss = 0.f;
 #pragma unroll
-      for (int b = 0; b < HD; b += 64) {
-        uint32_t w[32];
-        pack64(x + b, w);
-        epi_emit(e, w, map, static_cast<int32_t>(col0 + b), false);
+      for (int c = 0; c < HD; c += 32) {
+        float v[32];
+        tmem_ld32p(taddr + h0 + c, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) ss += v[j] * v[j];
+      }
+      const float inv = rsqrtf(ss / static_cast<float>(HD) + ep.eps);
+#pragma unroll 1
+      for (int c = 0; c < H; c += 32) {
+        float x1[32], x2[32];
+        tmem_ld32p(taddr + h0 + c, x1);
+        tmem_ld32p(taddr + h0 + H + c, x2);
+        tmem_wait_ld();
+        rope_pair32(x1, x2, w + c, w + H + c, inv, rope_row + c);
+        emit_bf16x32(e, x1, map, static_cast<int32_t>(col0 + c));
+        emit_bf16x32(e, x2, map, static_cast<int32_t>(col0 + H + c));
       }
     }
   } else {
-    for (int b0 = 0; b0 < BN; b0 += 64) {
-      if (n0 + b0 >= N) break;
-      float x[64];
-#pragma unroll
-      for (int c = 0; c < 64; c += 32) tmem_ld32p(taddr + b0 + c, x + c);
+    // HD in {16, 32}: 32-column chunks hold whole heads (HD = 32) or two heads (HD = 16).
+#pragma unroll 1
+    for (int c0 = c_lo; c0 < c_hi; c0 += 32) {
+      const int64_t colc = n0 + c0;
+      if (colc >= N) break;
+      float x[32];
+      tmem_ld32p(taddr + c0, x);
       tmem_wait_ld();
 #pragma unroll
-      for (int h = 0; h < 64; h += HD) {
-        const int64_t col0 = n0 + b0 + h;
+      for (int h = 0; h < 32; h += HD) {
+        const int64_t col0 = colc + h;
         const int kind = col0 < ep.q_dim ? 0 : (col0 < ep.q_dim + ep.kv_dim ? 1 : 2);
-        if (kind < 2 && col0 < N) norm_rope<HD>(x + h, kind == 0 ? s_qn : s_kn, rope_row, ep.eps);
+        if (kind < 2 && col0 < N) {
+          const float* w = kind == 0 ? s_qn : s_kn;
+          float ss = 0.f;
+#pragma unroll
+          for (int j = 0; j < HD; ++j) ss += x[h + j] * x[h + j];
+          const float inv = rsqrtf(ss / static_cast<float>(HD) + ep.eps);
+          constexpr int H = HD / 2;
+#pragma unroll
+          for (int j = 0; j < H; ++j) {
+            const float2 cs = __ldg(rope_row + j);
+            const float a = x[h + j] * inv * w[j];
+            const float b = x[h + j + H] * inv * w[j + H];
+            x[h + j] = a * cs.x - b * cs.y;
+            x[h + j + H] = b * cs.x + a * cs.y;
+          }
+        }
       }
-      uint32_t w[32];
-      pack64(x, w);
-      epi_emit(e, w, map, static_cast<int32_t>(n0 + b0), false);
+      emit_bf16x32(e, x, map, static_cast<int32_t>(colc));
     }
   }
 }
 
+// This warp: 32 rows (lane quarter) x columns [ch*BN/2, (ch+1)*BN/2) of the tile.
 template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_tile(EpiWarp& e, uint32_t taddr, int64_t gm_lane, int64_t M, int64_t n_blk,
-                                              int64_t N, const EpiParams& ep, const float* s_qn,
+__device__ __forceinline__ void epilogue_tile(EpiWarp& e, uint32_t taddr, int ch, int64_t gm_lane, int64_t M,
+                                              int64_t n_blk, int64_t N, const EpiParams& ep, const float* s_qn,
                                               const float* s_kn, const CUtensorMap* map) {
   const int64_t n0 = n_blk * BN;
-  if constexpr (EPI == RDX_EPI_STORE_BF16) {
+  const int c_lo = ch * (BN / 2), c_hi = c_lo + BN / 2;
+  if constexpr (EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 64) {
-      if (n0 + c >= N) break;
-      float v[64];
-      tmem_ld32p(taddr + c, v);
-      tmem_ld32p(taddr + c + 32, v + 32);
-      tmem_wait_ld();
-      uint32_t w[32];
-      pack64(v, w);
-      epi_emit(e, w, map, static_cast<int32_t>(n0 + c), false);
-    }
-  } else if constexpr (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = c_lo; c < c_hi; c += 32) {
       if (n0 + c >= N) break;
       float v[32];
       tmem_ld32p(taddr + c, v);
       tmem_wait_ld();
-      uint32_t w[32];
-      bits32(v, w);
-      epi_emit(e, w, map, static_cast<int32_t>(n0 + c), EPI == RDX_EPI_RESID_F32);
+      if constexpr (EPI == RDX_EPI_STORE_BF16) emit_bf16x32(e, v, map, static_cast<int32_t>(n0 + c));
+      else emit_f32x32(e, v, map, static_cast<int32_t>(n0 + c), EPI == RDX_EPI_RESID_F32);
     }
   } else if constexpr (EPI == RDX_EPI_SWIGLU) {
+    // tile columns: [g(64) u(64)] x (BN/128); out col = n_blk*BN/2 + pair*64 + j
     const int64_t nout = N / 2;
 #pragma unroll 1
-    for (int p = 0; p < BN / (2 * kSwigluUnit); ++p) {
+    for (int p = c_lo / (2 * kSwigluUnit); p < c_hi / (2 * kSwigluUnit); ++p) {
       const int64_t ocol0 = n_blk * (BN / 2) + p * kSwigluUnit;
       if (ocol0 >= nout) break;
-      float g[64], u[64];
-      tmem_ld32p(taddr + p * 128, g);
-      tmem_ld32p(taddr + p * 128 + 32, g + 32);
-      tmem_ld32p(taddr + p * 128 + 64, u);
-      tmem_ld32p(taddr + p * 128 + 96, u + 32);
-      tmem_wait_ld();
+#pragma unroll 1
+      for (int c = 0; c < kSwigluUnit; c += 32) {
+        float g[32], u[32];
+        tmem_ld32p(taddr + p * 2 * kSwigluUnit + c, g);
+        tmem_ld32p(taddr + p * 2 * kSwigluUnit + kSwigluUnit + c, u);
+        tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 64; ++j) g[j] = g[j] / (1.f + __expf(-g[j])) * u[j];
-      uint32_t w[32];
-      pack64(g, w);
-      epi_emit(e, w, map, static_cast<int32_t>(ocol0), false);
+        for (int j = 0; j < 32; ++j) g[j] = __fdividef(g[j], 1.f + __expf(-g[j])) * u[j];
+        emit_bf16x32(e, g, map, static_cast<int32_t>(ocol0 + c));
+      }
     }
   } else if constexpr (EPI == RDX_EPI_QKV) {
     const int64_t r = gm_lane < M ? gm_lane : (M > 0 ? M - 1 : 0);
     const float2* rope_row = ep.rope + r * (ep.hd >> 1);
     switch (ep.hd) {
-      case 128: qkv_tile<128>(e, taddr, n0, N, ep, s_qn, s_kn, rope_row, map, BN); break;
-      case 64: qkv_tile<64>(e, taddr, n0, N, ep, s_qn, s_kn, rope_row, map, BN); break;
-      case 32: qkv_tile<32>(e, taddr, n0, N, ep, s_qn, s_kn, rope_row, map, BN); break;
-      default: qkv_tile<16>(e, taddr, n0, N, ep, s_qn, s_kn, rope_row, map, BN); break;
+      case 128: qkv_cols<128>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
+      case 64: qkv_cols<64>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
+      case 32: qkv_cols<32>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
+      default: qkv_cols<16>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
     }
   }
 }
@@ -343,6 +377,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   } else {
     const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    const int ch = ew >> 2;  // column half of the tile
     EpiWarp e;
     e.buf[0] = epi_smem + ew * 2 * kEpiBoxBytes;
     e.buf[1] = e.buf[0] + kEpiBoxBytes;
@@ -358,7 +393,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       e.row0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM + q * 32);
-      epilogue_tile<BN, EPI>(e, taddr, e.row0 + lane, M, n_blk, N, ep, s_norm, s_norm + 128, &tmC);
+      epilogue_tile<BN, EPI>(e, taddr, ch, e.row0 + lane, M, n_blk, N, ep, s_norm, s_norm + 128, &tmC);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -401,7 +436,8 @@ EncodeTiledFn encode_fn() {
 
 // 2-D row-major map: inner = columns (elements), outer = rows, box = box_inner x box_outer, 128B swizzle.
 int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* ptr, int64_t inner, int64_t outer,
-             int64_t ld_elems, int box_inner, int box_outer) {
+             int64_t ld_elems, int box_inner, int box_outer,
+             CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return RDX_ERR_UNSUPPORTED;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
@@ -409,7 +445,7 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* pt
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? RDX_OK : RDX_ERR_INVALID_ARGUMENT;
 }
 
@@ -432,7 +468,8 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
     st = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.out, a.n, a.m, a.ldo, 32, 32);
   } else {
     const int64_t ncols = EPI == RDX_EPI_SWIGLU ? a.n / 2 : a.n;
-    st = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.out, ncols, a.m, a.ldo, 64, 32);
+    st = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.out, ncols, a.m, a.ldo, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_64B);
   }
   if (st) return st;
   EpiParams ep;
@@ -475,7 +512,7 @@ void choose_shape(const rdx_gemm_args& a, int* bn_out, int* cg_out) {
   double best_cost = 1e30;
   for (int bn : {256, 128}) {
     if (a.block_n && bn != a.block_n) continue;
-    if (a.epi == RDX_EPI_QKV && (bn % a.head_dim)) continue;
+    if (a.epi == RDX_EPI_QKV && ((bn / 2) % a.head_dim) && a.head_dim > 32) continue;
     const int64_t tiles = ((a.m + BM * cg - 1) / (BM * cg)) * ((a.n + bn - 1) / bn);
     const int64_t units = num_sms() / cg;
     const int64_t rounds = (tiles + units - 1) / units;
@@ -525,7 +562,7 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
       if (a.n % (2 * kSwigluUnit) || a.ldo % 8 || a.ldo < a.n / 2) return RDX_ERR_SHAPE_MISMATCH;
       return dispatch<RDX_EPI_SWIGLU>(a, bn, cg, s);
     case RDX_EPI_QKV: {
-      if (bn % a.head_dim) return RDX_ERR_SHAPE_MISMATCH;
+      if (a.head_dim > 32 && (bn / 2) % a.head_dim) return RDX_ERR_SHAPE_MISMATCH;
       if (a.n != static_cast<int64_t>(a.q_heads + 2 * a.kv_heads) * a.head_dim) return RDX_ERR_SHAPE_MISMATCH;
       if (!a.q_norm_w || !a.k_norm_w || !a.rope_table) return RDX_ERR_INVALID_ARGUMENT;
       if (a.ldo % 8 || a.ldo < a.n) return RDX_ERR_SHAPE_MISMATCH;

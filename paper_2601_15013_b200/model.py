@@ -9,23 +9,23 @@ original ragged layout.  Here each stage is an sm_100a kernel behind the C ABI
 
   embed + ln1          rdx_embed_rmsnorm       (gathers tok[gather[j]])
   QKV + q/k-norm+RoPE  rdx_gemm EPI_QKV        (tcgen05, fused epilogue)
-  attention boundary   rdx_gather_rows (scatter K/V, or Q/K/V) + FlashAttention-2
-                       varlen (library kernel, the declared boundary)
-  O-proj + residual    rdx_gemm EPI_RESID_F32
+  attention boundary   rdx_attention           (tcgen05; K/V read through the
+                                                scatter map, Q/O stay compact)
+  O-proj + residual    rdx_gemm EPI_RESID_F32  (TMA reduce-add into h)
   ln2                  rdx_rmsnorm_rows
   gate|up + SiLU*mul   rdx_gemm EPI_SWIGLU
   down + residual      rdx_gemm EPI_RESID_F32
   final norm + head    rdx_rmsnorm_rows (+ last-token row select) + rdx_gemm
 
 Attention boundary modes:
-  ``attention="full"``   exactly the reference: scatter Q/K/V to N rows,
-                         attention over the original layout, gather N -> N'
-                         (model.py:368-383).
+  ``attention="full"``   exactly the reference: scatter Q/K/V to N rows
+                         (rdx_gather_rows), attention over the original
+                         layout, gather N -> N' (model.py:368-383).
   ``attention="suffix"`` (default) SURVEY §8f-1: compact rows of sequence s
                          are its suffix [lcp_s, L_s), so Q stays compact
-                         (cu_seqlens_q = cu_q), only K/V are scattered, and the
-                         causal mask is bottom-right aligned.  Mathematically
-                         identical; removes the Q scatter and the gather.
+                         (cu_seqlens_q = cu_q), K/V are read in place through
+                         the scatter map and the causal mask is bottom-right
+                         aligned.  Mathematically identical; no row copies.
 
 Numerics: weights/activations bf16, fp32 accumulation (TMEM), fp32 residual
 stream and norm statistics.  Parity vs the fp64 reference is a tolerance
@@ -308,15 +308,6 @@ class _Layout:
     cu_q_host: object = None
 
 
-def _flash_varlen(q, k, v, cu_q, cu_k, max_q, max_k, scale):
-    try:
-        from flash_attn.flash_attn_interface import flash_attn_varlen_func
-    except Exception as exc:  # pragma: no cover - image always has it
-        raise NativeLibraryError(f"attention boundary kernel unavailable: {exc}") from exc
-    return flash_attn_varlen_func(q, k, v, cu_q, cu_k, max_q, max_k, dropout_p=0.0,
-                                  softmax_scale=scale, causal=True)
-
-
 class _Graph:
     """One captured prefill body plus its static input buffers."""
 
@@ -395,8 +386,20 @@ class RadixQwen3:
     def _gather(self, name, x, idx, stream_obj):
         return self._op(name, lambda: gather_rows_device(x, idx, stream=stream_obj))
 
-    def _attn(self, q, k, v, cu_q, cu_k, max_q, max_k, scale, flops):
-        return self._op("attention", lambda: _flash_varlen(q, k, v, cu_q, cu_k, max_q, max_k, scale), flops)
+    def _attn(self, qkv, scatter, cu32, cu_q32, b, max_q, out, flops, stream):
+        """rdx_attention: Q compact rows, K/V read through ``scatter`` (None = plain layout)."""
+        cfg = self.config
+        lib = _native.lib()
+
+        def launch():
+            code = lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), None if scatter is None else scatter.data_ptr(),
+                                     cu32.data_ptr(), cu_q32.data_ptr(), b, max(int(max_q), 1), cfg.num_heads,
+                                     cfg.num_kv_heads, cfg.head_dim, 1.0 / math.sqrt(cfg.head_dim),
+                                     out.data_ptr(), out.stride(0), stream)
+            _native.check(code, "rdx_attention")
+
+        self._op("attention", launch, flops)
+        return out
 
     # ------------------------------------------------------------ layout
     def _layout(self, db: DeviceBatch, plan, attention: str) -> _Layout:
@@ -557,7 +560,9 @@ class RadixQwen3:
         self._op("rope_table", rope_fn)
         qkv = torch.empty(m, qd + 2 * kvd, dtype=bf, device=dev)
         act = torch.empty(m, self.di_pad, dtype=bf, device=dev)
-        scale = 1.0 / math.sqrt(hd)
+        attn_out = torch.empty(m, qd, dtype=bf, device=dev)
+        if mode == "suffix" and m > n_compact:
+            attn_out[n_compact:] = 0  # padded plan rows are never attention queries
         last_rows = None
         if logits == "last":
             ends = cu64[1:] - 1
@@ -569,21 +574,14 @@ class RadixQwen3:
             self._gemm("qkv", hn, T[pre + "w_qkv"], _native.EPI_QKV, qkv, m=m, stream=st, qkv=True, rope=rope,
                        layer=pre)
             if mode == "plain":
-                a = self._attn(qkv[:, :qd].view(m, H, hd), qkv[:, qd:qd + kvd].view(m, KV, hd),
-                               qkv[:, qd + kvd:].view(m, KV, hd), cu32, cu32, max_k, max_k, scale, att_flops)
+                a = self._attn(qkv, None, cu32, cu32, b, max_k, attn_out, att_flops, st)
             elif mode == "suffix":
-                kv_full = self._gather("scatter_kv", qkv[:, qd:], scatter, stream)
-                a = self._attn(qkv[:, :qd].view(m, H, hd), kv_full[:, :kvd].view(n, KV, hd),
-                               kv_full[:, kvd:].view(n, KV, hd), cu_q32, cu32, max(max_q, 1), max_k, scale,
-                               att_flops)
-                if m > n_compact:
-                    a[n_compact:] = 0
+                a = self._attn(qkv, scatter, cu32, cu_q32, b, max_q, attn_out, att_flops, st)
             else:
                 qkv_full = self._gather("scatter_qkv", qkv, scatter, stream)
-                a_full = self._attn(qkv_full[:, :qd].view(n, H, hd), qkv_full[:, qd:qd + kvd].view(n, KV, hd),
-                                    qkv_full[:, qd + kvd:].view(n, KV, hd), cu32, cu32, max_k, max_k, scale,
-                                    att_flops)
-                a = self._gather("gather_attn", a_full.view(n, qd), gather, stream)
+                a_full = torch.empty(n, qd, dtype=bf, device=dev)
+                self._attn(qkv_full, None, cu32, cu32, b, max_k, a_full, att_flops, st)
+                a = self._gather("gather_attn", a_full, gather, stream)
             a = a.reshape(m, qd)
             self._gemm("o_proj", a, T[pre + "wo"], _native.EPI_RESID_F32, h, m=m, stream=st)
             self._rmsnorm(h, T[pre + "ln2"], hn, stream=st)
