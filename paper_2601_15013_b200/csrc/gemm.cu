@@ -18,6 +18,8 @@
 // tile schedule (M fastest).  Each output row depends only on its own A row:
 // no split-K and an M-independent tile shape, so compact and full forwards
 // give bit-identical rows (the reference's _mm rule, model.py:124-144).
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -506,24 +508,48 @@ int dispatch(const rdx_gemm_args& a, int bn, int cg, cudaStream_t s) {
 }
 
 // Pick (CG, BN): fewest tile rounds x tile width, preferring the CTA pair.
+// Pick (CG, BN) minimising tile rounds x per-tile cost.  A 1-CTA tile streams
+// a third more operand bytes per FLOP than the pair tile, hence the penalty.
+// RDX_GEMM_SHAPE="cg,bn" (env) pins the choice for experiments.
 void choose_shape(const rdx_gemm_args& a, int* bn_out, int* cg_out) {
-  const int cg = a.m > BM ? 2 : 1;
-  int best_bn = 256;
+  static int forced_cg = -1, forced_bn = -1;
+  if (forced_cg < 0) {
+    forced_cg = 0;
+    if (const char* e = getenv("RDX_GEMM_SHAPE")) {
+      int c = 0, n = 0;
+      if (sscanf(e, "%d,%d", &c, &n) == 2 && (c == 1 || c == 2) && (n == 128 || n == 256)) {
+        forced_cg = c;
+        forced_bn = n;
+      }
+    }
+  }
+  int best_bn = 256, best_cg = a.m > BM ? 2 : 1;
   double best_cost = 1e30;
-  for (int bn : {256, 128}) {
-    if (a.block_n && bn != a.block_n) continue;
-    if (a.epi == RDX_EPI_QKV && ((bn / 2) % a.head_dim) && a.head_dim > 32) continue;
-    const int64_t tiles = ((a.m + BM * cg - 1) / (BM * cg)) * ((a.n + bn - 1) / bn);
-    const int64_t units = num_sms() / cg;
-    const int64_t rounds = (tiles + units - 1) / units;
-    const double cost = static_cast<double>(rounds) * (bn + 64);  // per-tile fixed cost ~ 64 columns
-    if (cost < best_cost) {
-      best_cost = cost;
-      best_bn = bn;
+  for (int cg : {2, 1}) {
+    if (cg == 2 && a.m <= BM) continue;
+    for (int bn : {256, 128}) {
+      if (a.block_n && bn != a.block_n) continue;
+      if (a.epi == RDX_EPI_QKV && ((bn / 2) % a.head_dim) && a.head_dim > 32) continue;
+      const int64_t tiles = ((a.m + BM * cg - 1) / (BM * cg)) * ((a.n + bn - 1) / bn);
+      const int64_t units = num_sms() / cg;
+      const int64_t rounds = (tiles + units - 1) / units;
+      const double cost = static_cast<double>(rounds) * (bn + 64) * (cg == 1 ? 1.15 : 1.0);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best_bn = bn;
+        best_cg = cg;
+      }
+    }
+  }
+  if (forced_cg > 0 && (forced_cg == 1 || a.m > BM)) {
+    const bool ok = !(a.epi == RDX_EPI_QKV && ((forced_bn / 2) % a.head_dim) && a.head_dim > 32);
+    if (ok && (!a.block_n || a.block_n == forced_bn)) {
+      best_cg = forced_cg;
+      best_bn = forced_bn;
     }
   }
   *bn_out = best_bn;
-  *cg_out = cg;
+  *cg_out = best_cg;
 }
 
 }  // namespace gemm
