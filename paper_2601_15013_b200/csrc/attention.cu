@@ -13,46 +13,55 @@
 //   * the output is written directly in compact layout.
 // Plain (no-dedup) mode is the same kernel with scatter == NULL, cu_q == cu.
 //
-// Persistent CTAs (one per SM) walk the (sequence, kv head) work items; each
-// item is every 128-row query block of that sequence/head, and all roles run
-// one continuous software pipeline over (item, query block, key tile) steps,
-// so the next item's loads overlap the current item's tail.  13 warps:
-//   warps 0-3   softmax: row t of S per thread (TMEM lane t), online softmax,
-//               P (bf16) -> smem, O rescale when the running max moves
-//   warps 4-7   epilogue: O / l -> bf16 -> global (compact rows)
-//   warps 8-11  loaders: cp.async 16-byte gathers of Q (2 buffers) and K/V
-//               (3-stage ring) into the 128-byte-swizzled UMMA layouts
-//   warp  12    TMEM allocator + MMA issuer:
-//               S = Q K^T   (M=128 rows = group heads x queries, N=64 keys, K=hd)
-//               O += P V    (M=128, N=hd, K=64 keys; V read MN-major, no transpose)
-//               S and O are double-buffered in TMEM (S(t+1) overlaps softmax(t),
-//               block b+1 accumulates while block b drains).
+// Tiling.  A query tile is 128 rows = (GQA group heads) x (128 / group
+// queries) of one (sequence, kv head), so one S MMA serves the whole group
+// against one K tile.  A work unit is a PAIR of consecutive query tiles
+// (h = 0, 1) of one (sequence, kv head); both stream the same 128-key K/V
+// tiles, which are loaded once.  Units are walked longest-first by
+// persistent CTAs (one per SM) in one continuous pipeline across units.
+//
+// TMEM (512 columns): S_h at [128h, 128h+128) fp32, with P_h (bf16 pairs)
+// written back over its first 64 columns; O_h at [256+128h, ...).  The P V
+// product reads P straight from TMEM (tcgen05.mma A-from-TMEM), so P never
+// touches shared memory.  The MMA issue order per key tile j is
+//     PV_0(j)  S_0(j+1)  PV_1(j)  S_1(j+1)
+// so the tensor pipe works on one tile while the other tile's softmax runs.
+// Softmax keeps a stale running max unless the tile max exceeds it by more
+// than 2^8 (exact: the final O / l uses the same max), so O is rescaled in
+// TMEM only on the rare large jumps.
+//
+// 16 warps (setmaxnreg re-balances registers toward the softmax groups):
+//   warps 0-3   softmax + epilogue of query tile 0 (row t = TMEM lane t)
+//   warps 4-7   softmax + epilogue of query tile 1
+//   warps 8-11  loaders: cp.async 16-byte gathers of Q and of K/V through the
+//               scatter map into 128-byte-swizzled UMMA layouts (4-slot ring
+//               of K and V tiles)
+//   warp  12    TMEM allocator + single-thread MMA issuer
+//   warps 13-15 idle (complete the warpgroup for setmaxnreg)
 #include "common.cuh"
 
 namespace rdx {
 namespace attn {
 
-constexpr int BQ = 128;        // tile rows (group heads x queries)
-constexpr int BKEY = 64;       // keys per K/V tile
-constexpr int kThreads = 416;  // 13 warps
-constexpr int P_BYTES = BQ * BKEY * 2;     // 16 KB: 128 rows x 128 B
-constexpr uint32_t TMEM_COLS = 512;        // S[2]: cols 0 / 64, O[2]: cols 128 / 256 (HDP each)
-constexpr uint32_t S_COL = 0, O_COL = 128;
+constexpr int BQ = 128;        // rows per query tile (group heads x queries)
+constexpr int BK = 128;        // keys per K/V tile
+constexpr int NSLOT = 4;       // K/V ring slots (K and V tiles alternate)
+constexpr int kThreads = 512;  // 16 warps
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t O_COL = 256;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
 
-// HDP = head dim padded to a whole number of 64-element (128 B) swizzle atoms;
-// the runtime head dim (16..HDP) is zero-padded in smem, which adds nothing to
-// Q K^T and only produces ignored output columns in P V.
 template <int HDP>
 struct Tile {
   static constexpr int HALVES = HDP / 64;
-  static constexpr int CHUNKS = HDP / 8;            // 16-byte chunks per row
-  static constexpr int Q_BYTES = BQ * HDP * 2;      // HALVES x 128 rows x 128 B
-  static constexpr int KV_BYTES = BKEY * HDP * 2;   // HALVES x 64 keys x 128 B
-  static constexpr int NS = 3;                      // K/V ring stages
-  static constexpr int SMEM = 2 * Q_BYTES + NS * 2 * KV_BYTES + P_BYTES + 1024 + 256;
-  // kind::f16, bf16 in, fp32 acc; S: A K-major, B K-major.  PV: A K-major, B MN-major.
-  static constexpr uint32_t IDESC_S = umma_idesc_bf16(BQ, BKEY);
-  static constexpr uint32_t IDESC_PV = umma_idesc_bf16(BQ, HDP) | (1u << 16);
+  static constexpr int CH = HDP / 8;               // 16-byte chunks per row
+  static constexpr int Q_BYTES = BQ * HDP * 2;     // HALVES x 128 rows x 128 B
+  static constexpr int T_BYTES = BK * HDP * 2;     // one K or V tile
+  static constexpr int BAR_OFF = 2 * Q_BYTES + NSLOT * T_BYTES;
+  static constexpr int ROWS_OFF = BAR_OFF + 256;   // int32 [2][BK] compact rows of the current key tile
+  static constexpr int SMEM = ROWS_OFF + 2 * BK * 4 + 1024;  // + alignment slack
+  static constexpr uint32_t IDESC_S = umma_idesc_bf16(BQ, BK);
+  static constexpr uint32_t IDESC_PV = umma_idesc_bf16(BQ, HDP) | (1u << 16);  // B (V) MN-major
 };
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
@@ -63,6 +72,17 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, ui
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(2) << 61;
   return d;
+}
+
+// D[tmem] (+)= A[tmem] * B[smem], kind::f16 (A = P in TMEM, bf16 pairs per 32-bit column).
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
@@ -82,6 +102,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // 16-byte async global -> shared copy (L2 only); src_bytes = 0 zero-fills.
@@ -93,6 +121,15 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 struct Args {
   const __nv_bfloat16* qkv;  // [rows, ld] compact (or full, plain mode)
   int64_t ld;                // elements
@@ -102,18 +139,11 @@ struct Args {
   __nv_bfloat16* out;        // [rows_q, ld_out]
   int64_t ld_out;
   int nseq, heads, kv_heads, hd;
+  int group, qpt;            // heads / kv_heads, queries per tile (BQ / group)
+  int max_pairs;             // query-tile pairs of the longest query range
+  int n_units;               // max_pairs * nseq * kv_heads
   float scale_log2;          // softmax scale * log2(e)
-  unsigned long long* trace; // optional per-CTA event timestamps (RDX_ATTN_TRACE), else NULL
 };
-
-#define RDX_TRACE(slot)                                                                     \
-  do {                                                                                      \
-    if (a.trace && blockIdx.x < 4096 && (slot) < 64) {                                      \
-      unsigned long long _t;                                                                \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                \
-      a.trace[static_cast<size_t>(blockIdx.x) * 64 + (slot)] = _t;                          \
-    }                                                                                       \
-  } while (0)
 
 // 16-byte chunk c of a head row -> swizzled smem offset in a
 // [halves][rows][128 B] tile (half stride = rows * 128).
@@ -128,73 +158,77 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// Work item geometry (identical in every role).
-struct Item {
-  int s, g, k0, L, q0, qlen, lcp, n_mb;
+// Unit geometry (identical in every role).  Units are ordered pair-index
+// descending so the longest key ranges are scheduled first.
+struct Unit {
+  int s, g, k0, L, q0, qlen, lcp, mb0;
+  int nkt[2];  // key tiles of query tile h (0 = tile absent)
+  int nkt_all;
 };
 
-__device__ __forceinline__ bool load_item(const Args& a, int item, int qpt, Item& it) {
-  it.s = item / a.kv_heads;
-  it.g = item % a.kv_heads;
+__device__ __forceinline__ bool load_unit(const Args& a, int u, Unit& it) {
+  const int per = a.nseq * a.kv_heads;
+  const int pair = a.max_pairs - 1 - u / per;
+  const int rem = u - (u / per) * per;
+  it.s = rem / a.kv_heads;
+  it.g = rem - it.s * a.kv_heads;
   it.k0 = a.cu[it.s];
   it.L = a.cu[it.s + 1] - it.k0;
   it.q0 = a.cu_q[it.s];
   it.qlen = a.cu_q[it.s + 1] - it.q0;
   it.lcp = it.L - it.qlen;
-  it.n_mb = (it.qlen + qpt - 1) / qpt;
-  return it.qlen > 0;
+  it.mb0 = 2 * pair;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int mb = it.mb0 + h;
+    it.nkt[h] = mb * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (mb + 1) * a.qpt) + BK - 1) / BK : 0;
+  }
+  it.nkt_all = max(it.nkt[0], it.nkt[1]);
+  return it.nkt[0] > 0;
 }
 
-// key tiles of query block mb: keys [0, lcp + min(qlen, (mb+1)*qpt))
-__device__ __forceinline__ int tiles_of(const Item& it, int mb, int qpt) {
-  return (it.lcp + min(it.qlen, (mb + 1) * qpt) + BKEY - 1) / BKEY;
+// Next valid unit of this CTA at or after u (returns n_units when done).
+__device__ __forceinline__ int next_unit(const Args& a, int u, Unit& it) {
+  for (; u < a.n_units; u += gridDim.x)
+    if (load_unit(a, u, it)) return u;
+  return a.n_units;
 }
 
 template <int HDP>
-__global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a, int n_items) {
+__global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a) {
   using T = Tile<HDP>;
-  constexpr int Q_BYTES = T::Q_BYTES, KV_BYTES = T::KV_BYTES, CH = T::CHUNKS, NS = T::NS;
-  constexpr int HD = HDP;  // smem row width (elements)
+  constexpr int Q_BYTES = T::Q_BYTES, T_BYTES = T::T_BYTES, CH = T::CH;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;  // 1024-aligned for the SWIZZLE_128B atoms
-  uint8_t* sQ0 = smem;
-  uint8_t* sKV0 = smem + 2 * Q_BYTES;  // stage i: K at sKV0 + i*2*KV_BYTES, V right after
-  uint8_t* sP = sKV0 + NS * 2 * KV_BYTES;
-  float* sL = reinterpret_cast<float*>(sP + P_BYTES);  // [2][128] row sums for the epilogue
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sL + 256);
-  uint64_t* q_full = bars + 0;            // [2]
-  uint64_t* q_free = bars + 2;            // [2]
-  uint64_t* kv_full = bars + 4;           // [NS]
-  uint64_t* kv_free = bars + 4 + NS;      // [NS]
-  uint64_t* s_full = bars + 4 + 2 * NS;   // [2]
-  uint64_t* s_free = bars + 6 + 2 * NS;   // [2]
-  uint64_t* p_full = bars + 8 + 2 * NS;
-  uint64_t* pv_done = bars + 9 + 2 * NS;
-  uint64_t* o_full = bars + 10 + 2 * NS;  // [2]
-  uint64_t* o_free = bars + 12 + 2 * NS;  // [2]
-  uint64_t* l_full = bars + 14 + 2 * NS;  // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 16 + 2 * NS);
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                  // [2][Q_BYTES]
+  uint8_t* sT = smem + 2 * Q_BYTES;    // [NSLOT][T_BYTES]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::BAR_OFF);
+  uint64_t* q_full = bars + 0;                 // [2]
+  uint64_t* q_free = bars + 2;                 // [2]
+  uint64_t* t_full = bars + 4;                 // [NSLOT]
+  uint64_t* t_free = bars + 4 + NSLOT;         // [NSLOT]
+  uint64_t* s_full = bars + 4 + 2 * NSLOT;     // [2]
+  uint64_t* p_full = bars + 6 + 2 * NSLOT;     // [2]
+  uint64_t* o_full = bars + 8 + 2 * NSLOT;     // [2]
+  uint64_t* o_free = bars + 10 + 2 * NSLOT;    // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 12 + 2 * NSLOT);
+  int32_t* s_rows = reinterpret_cast<int32_t*>(smem + T::ROWS_OFF);  // [2][BK]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int group = a.heads / a.kv_heads;
-  const int qpt = BQ / group;  // queries per tile
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 128);
       mbar_init(&q_free[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
+      mbar_init(&p_full[i], 128);
       mbar_init(&o_full[i], 1);
       mbar_init(&o_free[i], 128);
-      mbar_init(&l_full[i], 128);
     }
-    for (int i = 0; i < NS; ++i) {
-      mbar_init(&kv_full[i], 128);
-      mbar_init(&kv_free[i], 1);
+    for (int i = 0; i < NSLOT; ++i) {
+      mbar_init(&t_full[i], 128);
+      mbar_init(&t_free[i], 1);
     }
-    mbar_init(p_full, 128);
-    mbar_init(pv_done, 1);
     fence_mbar_init();
   }
   if (warp == 12) {
@@ -205,249 +239,260 @@ __global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a, int n_it
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  if (threadIdx.x == 0) RDX_TRACE(0);
 
-  if (warp >= 8 && warp < 12) {
-    // ---------------------------------------------------------------- loaders
-    // cp.async (LDGSTS) 16-byte copies that arrive on the stage barrier when
-    // they land: several tiles in flight without register staging.
-    const int t = threadIdx.x - 256;  // 0..127
-    constexpr int KCH = CH / 2;       // chunks per thread per K (or V) row
-    const int kr = t >> 1, kc0 = (t & 1) * KCH;
-    int step = 0, blk = 0;
-    Item it;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      if (!load_item(a, item, qpt, it)) continue;
-      const int64_t kcol = static_cast<int64_t>(a.heads) * a.hd + static_cast<int64_t>(it.g) * a.hd;
-      const int64_t vcol = kcol + static_cast<int64_t>(a.kv_heads) * a.hd;
-      for (int mb = 0; mb < it.n_mb; ++mb, ++blk) {
-        const int qb = blk & 1;
-        if (blk >= 2) mbar_wait(&q_free[qb], ((blk >> 1) - 1) & 1);
-        const uint32_t sq = smem_u32(sQ0 + qb * Q_BYTES);
+  if (warp >= 8) {
+    setmaxnreg_dec<80>();
+    if (warp < 12) {
+      // ---------------------------------------------------------------- loaders
+      const int t = threadIdx.x - 256;  // 0..127
+      int q_cnt[2] = {0, 0};
+      uint32_t seq = 0;  // K/V ring sequence number (K and V tiles alternate)
+      Unit it;
+      for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
+        // Q tiles of this unit
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          if (!it.nkt[h]) continue;
+          if (q_cnt[h] > 0) mbar_wait(&q_free[h], (q_cnt[h] - 1) & 1);
+          const uint32_t sq = smem_u32(sQ + h * Q_BYTES);
+          const int mb = it.mb0 + h;
 #pragma unroll
-        for (int k = 0; k < CH; ++k) {
-          const int idx = t + k * 128;
-          const int r = idx / CH, c = idx % CH;
-          const int hh = r / qpt, qi = mb * qpt + (r - hh * qpt);
-          const bool ok = qi < it.qlen && c * 8 < a.hd;
-          const __nv_bfloat16* src = ok ? a.qkv + static_cast<int64_t>(it.q0 + qi) * a.ld +
-                                              static_cast<int64_t>(it.g * group + hh) * a.hd + c * 8
-                                        : a.qkv;
-          cp_async16(sq + sw_off(r, c, BQ), src, ok ? 16u : 0u);
-        }
-        cp_async_arrive(&q_full[qb]);
-        const int n_kt = tiles_of(it, mb, qpt);
-        for (int kt = 0; kt < n_kt; ++kt, ++step) {
-          const int st = step % NS;
-          if (step >= NS) mbar_wait(&kv_free[st], ((step / NS) - 1) & 1);
-          const uint32_t sk = smem_u32(sKV0 + st * 2 * KV_BYTES), sv = sk + KV_BYTES;
-          const int j = kt * BKEY + kr;
-          const bool ok = j < it.L;
-          const int64_t row =
-              !ok ? 0 : (a.scatter ? static_cast<int64_t>(__ldg(a.scatter + it.k0 + j)) : static_cast<int64_t>(it.k0 + j));
-          const __nv_bfloat16* base = a.qkv + row * a.ld;
-#pragma unroll
-          for (int k = 0; k < KCH; ++k) {
-            const int c = kc0 + k;
-            const bool cok = ok && c * 8 < a.hd;
-            const uint32_t off = sw_off(kr, c, BKEY);
-            cp_async16(sk + off, cok ? base + kcol + c * 8 : a.qkv, cok ? 16u : 0u);
-            cp_async16(sv + off, cok ? base + vcol + c * 8 : a.qkv, cok ? 16u : 0u);
+          for (int k = 0; k < CH; ++k) {
+            const int idx = t + k * 128;
+            const int r = idx / CH, c = idx % CH;
+            const int hh = r / a.qpt, qi = mb * a.qpt + (r - hh * a.qpt);
+            const bool ok = qi < it.qlen && c * 8 < a.hd;
+            const __nv_bfloat16* src = ok ? a.qkv + static_cast<int64_t>(it.q0 + qi) * a.ld +
+                                                static_cast<int64_t>(it.g * a.group + hh) * a.hd + c * 8
+                                          : a.qkv;
+            cp_async16(sq + sw_off(r, c, BQ), src, ok ? 16u : 0u);
           }
-          cp_async_arrive(&kv_full[st]);
+          cp_async_arrive(&q_full[h]);
+          ++q_cnt[h];
+        }
+        const int64_t kcol = static_cast<int64_t>(a.heads) * a.hd + static_cast<int64_t>(it.g) * a.hd;
+        const int64_t vcol = kcol + static_cast<int64_t>(a.kv_heads) * a.hd;
+        // Row of key j*BK + t, resolved once per tile by thread t (one coalesced
+        // scatter read, prefetched a tile ahead) and shared through smem.
+        auto key_row = [&](int j) {
+          const int key = j * BK + t;
+          return key >= it.L ? -1 : (a.scatter ? __ldg(a.scatter + it.k0 + key) : it.k0 + key);
+        };
+        int row_next = key_row(0);
+#pragma unroll 1
+        for (int j = 0; j < it.nkt_all; ++j) {
+          int32_t* rows = s_rows + (seq & 2 ? BK : 0);  // seq advances by 2 per tile: alternate buffers
+          rows[t] = row_next;
+          named_bar_sync(1, 128);
+          if (j + 1 < it.nkt_all) row_next = key_row(j + 1);
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv, ++seq) {
+            const uint32_t slot = seq % NSLOT;
+            if (seq >= NSLOT) mbar_wait(&t_free[slot], ((seq / NSLOT) - 1) & 1);
+            const uint32_t st = smem_u32(sT + slot * T_BYTES);
+            const int64_t col = kv ? vcol : kcol;
+#pragma unroll 8
+            for (int k = 0; k < CH; ++k) {
+              const int idx = t + k * 128;
+              const int r = idx / CH, c = idx % CH;
+              const int row = rows[r];
+              const bool ok = row >= 0 && c * 8 < a.hd;
+              cp_async16(st + sw_off(r, c, BK), a.qkv + static_cast<int64_t>(ok ? row : 0) * a.ld + col + c * 8,
+                         ok ? 16u : 0u);
+            }
+            cp_async_arrive(&t_full[slot]);
+          }
         }
       }
-    }
-  } else if (warp == 12) {
-    // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t pa = smem_u32(sP);
-      int step = 0, blk = 0;
-      int prev_stage = -1, prev_blk = -1, prev_last = 0, prev_first = 0;
-      auto issue_pv = [&](int pstep) {
-        if (prev_first && prev_blk >= 2) mbar_wait(&o_free[prev_blk & 1], ((prev_blk >> 1) - 1) & 1);
-        mbar_wait(p_full, pstep & 1);
+    } else if (warp == 12 && lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      int s_cnt[2] = {0, 0};   // S tiles issued per h (== P tiles consumed)
+      int o_cnt[2] = {0, 0};   // units finished per h
+      int q_cnt[2] = {0, 0};   // Q tiles consumed per h
+      uint32_t gt = 0;         // global key-tile counter (K at seq 2gt, V at 2gt+1)
+
+      auto issue_S = [&](int h, const Unit& U, int j, uint32_t tile) {
+        if (j == 0) {
+          mbar_wait(&q_full[h], q_cnt[h] & 1);
+        }
+        const uint32_t kslot = (2 * tile) % NSLOT;
+        fence_proxy_async_smem();
         tc_fence_after();
-        const uint32_t va = smem_u32(sKV0 + prev_stage * 2 * KV_BYTES) + KV_BYTES;
-        const uint32_t o = tmem + O_COL + (prev_blk & 1) * 128;
+        const uint32_t qa = smem_u32(sQ + h * Q_BYTES), ka = smem_u32(sT + kslot * T_BYTES);
+        const uint32_t sacc = tmem + h * 128;
+        const uint64_t qd = sdesc(qa, 16, 1024), kd = sdesc(ka, 16, 1024);  // + (byte offset >> 4) per step
 #pragma unroll
-        for (int kk = 0; kk < BKEY / 16; ++kk)
-          umma_bf16(o, sdesc(pa + kk * 32, 16, 1024), sdesc(va + kk * 2048, BKEY * 128, 1024), T::IDESC_PV,
-                    (prev_first && kk == 0) ? 0u : 1u);
-        umma_commit(&kv_free[prev_stage]);
-        umma_commit(pv_done);
-        if (prev_last) umma_commit(&o_full[prev_blk & 1]);
+        for (int kk = 0; kk < HDP / 16; ++kk)
+          umma_bf16(sacc, qd + (((kk >> 2) * (BQ * 128) + (kk & 3) * 32) >> 4),
+                    kd + (((kk >> 2) * (BK * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
+        umma_commit(&s_full[h]);
+        ++s_cnt[h];
+        if (j == U.nkt[h] - 1) {
+          umma_commit(&q_free[h]);
+          ++q_cnt[h];
+        }
       };
-      Item it;
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        if (!load_item(a, item, qpt, it)) continue;
-        for (int mb = 0; mb < it.n_mb; ++mb, ++blk) {
-          const int qb = blk & 1;
-          mbar_wait(&q_full[qb], (blk >> 1) & 1);
-          fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 operand reads
-          tc_fence_after();
-          const uint32_t qa = smem_u32(sQ0 + qb * Q_BYTES);
-          const int n_kt = tiles_of(it, mb, qpt);
-          for (int kt = 0; kt < n_kt; ++kt, ++step) {
-            const int st = step % NS;
-            mbar_wait(&kv_full[st], (step / NS) & 1);
-            if (step < 8) RDX_TRACE(8 + step * 7 + 0);
-            if (step >= 2) mbar_wait(&s_free[step & 1], ((step >> 1) - 1) & 1);
-            if (step < 8) RDX_TRACE(8 + step * 7 + 1);
-            fence_proxy_async_smem();
-            tc_fence_after();
-            const uint32_t ka = smem_u32(sKV0 + st * 2 * KV_BYTES);
-            const uint32_t sacc = tmem + S_COL + (step & 1) * 64;
+      auto issue_PV = [&](int h, const Unit& U, int j, uint32_t tile) {
+        mbar_wait(&p_full[h], (s_cnt[h] - 1) & 1);  // P_h(j) published (S_h(j) was the last S of h)
+        if (j == 0 && o_cnt[h] > 0) mbar_wait(&o_free[h], (o_cnt[h] - 1) & 1);
+        fence_proxy_async_smem();  // cp.async (generic proxy) V writes -> tcgen05 operand reads
+        tc_fence_after();
+        const uint32_t va = smem_u32(sT + ((2 * tile + 1) % NSLOT) * T_BYTES);
+        const uint32_t o = tmem + O_COL + h * 128;
+        const uint64_t vd = sdesc(va, BK * 128, 1024);
 #pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk)
-              umma_bf16(sacc, sdesc(qa + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024),
-                        sdesc(ka + (kk >> 2) * (BKEY * 128) + (kk & 3) * 32, 16, 1024), T::IDESC_S,
-                        kk > 0 ? 1u : 0u);
-            umma_commit(&s_full[step & 1]);
-            if (kt == n_kt - 1) umma_commit(&q_free[qb]);  // last S of this block reads Q(qb)
-            if (prev_stage >= 0) issue_pv(step - 1);        // PV(step-1) overlaps S(step)
-            prev_stage = st;
-            prev_blk = blk;
-            prev_first = kt == 0;
-            prev_last = kt == n_kt - 1;
-          }
+        for (int kk = 0; kk < BK / 16; ++kk)
+          umma_ts(o, tmem + h * 128 + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+        if (j == U.nkt[h] - 1) {
+          umma_commit(&o_full[h]);
+          ++o_cnt[h];
         }
+      };
+      auto wait_tile = [&](uint32_t seqno) {
+        mbar_wait(&t_full[seqno % NSLOT], (seqno / NSLOT) & 1);
+      };
+
+      Unit cur, nxt;
+      int ucur = next_unit(a, blockIdx.x, cur);
+      int jcur = 0;
+      if (ucur < a.n_units) {
+        wait_tile(2 * gt);
+        if (cur.nkt[0] > 0) issue_S(0, cur, 0, gt);
+        if (cur.nkt[1] > 0) issue_S(1, cur, 0, gt);
+        umma_commit(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
       }
-      if (prev_stage >= 0) issue_pv(step - 1);
-    }
-  } else if (warp < 4) {
-    // ---------------------------------------------------------------- softmax (row t)
-    const int t = threadIdx.x;  // 0..127 == TMEM lane
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    int step = 0, blk = 0;
-    Item it;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      if (!load_item(a, item, qpt, it)) continue;
-      for (int mb = 0; mb < it.n_mb; ++mb, ++blk) {
-        const int qi = mb * qpt + (t % qpt);
-        const int pos = it.lcp + qi;                       // keys 0..pos visible
-        const int pos_min = __reduce_min_sync(0xffffffffu, pos);
-        const uint32_t o_base = lane_base + O_COL + (blk & 1) * 128;
-        float m_run = -INFINITY, l_run = 0.f;
-        const int n_kt = tiles_of(it, mb, qpt);
-        for (int kt = 0; kt < n_kt; ++kt, ++step) {
-          const uint32_t s_base = lane_base + S_COL + (step & 1) * 64;
-          mbar_wait(&s_full[step & 1], (step >> 1) & 1);
-          if (t == 0 && step < 8) RDX_TRACE(8 + step * 7 + 3);
-          tc_fence_after();
-          float sv[64];
-          tmem_ld32p(s_base, sv);
-          tmem_ld32p(s_base + 32, sv + 32);
-          tmem_wait_ld();
-          tc_fence_before();
-          mbar_arrive(&s_free[step & 1]);  // S buffer may be overwritten by S(step + 2)
-          const bool diag = kt * BKEY + BKEY - 1 > pos_min;  // warp-uniform: some key masked
-          float mx[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) mx[u] = -INFINITY;
-          if (diag) {
-#pragma unroll
-            for (int j = 0; j < 64; ++j) {
-              sv[j] = (kt * BKEY + j <= pos) ? sv[j] * a.scale_log2 : -INFINITY;
-              mx[j & 7] = fmaxf(mx[j & 7], sv[j]);
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 64; ++j) {
-              sv[j] *= a.scale_log2;
-              mx[j & 7] = fmaxf(mx[j & 7], sv[j]);
-            }
-          }
-          const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-          const float m_new = fmaxf(m_run, mt);
-          const float m_use = m_new == -INFINITY ? 0.f : m_new;
-          const float alpha = ex2(m_run - m_use);
-          m_run = m_new;
-          float ls[8];
-          uint32_t pw[32];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) ls[u] = 0.f;
-#pragma unroll
-          for (int j = 0; j < 64; j += 2) {
-            const float p0 = ex2(sv[j] - m_use), p1 = ex2(sv[j + 1] - m_use);
-            ls[(j >> 1) & 7] += p0 + p1;
-            pw[j >> 1] = pack_bf16x2(p0, p1);
-          }
-          l_run = l_run * alpha +
-                  (((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7])));
-          if (t == 0 && step < 8) RDX_TRACE(8 + step * 7 + 4);
-          if (step > 0) {
-            // PV(step - 1) done: O may be rescaled and P overwritten
-            mbar_wait(pv_done, (step - 1) & 1);
-            if (t == 0 && step < 8) RDX_TRACE(8 + step * 7 + 5);
-            tc_fence_after();
-            if (kt > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-              for (int c = 0; c < HD; c += 32) {
-                float ov[32];
-                tmem_ld32p(o_base + c, ov);
-                tmem_wait_ld();
-#pragma unroll
-                for (int j = 0; j < 32; ++j) ov[j] *= alpha;
-                tmem_st32(o_base + c, ov);
-              }
-              tmem_wait_st();
-            }
-          }
-          const uint32_t prow = smem_u32(sP) + t * 128;
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            st_shared_v4(prow + ((c ^ (t & 7)) << 4), pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
-          fence_proxy_async_smem();
-          tc_fence_before();
-          mbar_arrive(p_full);
-          if (t == 0 && step < 8) RDX_TRACE(8 + step * 7 + 6);
+      while (ucur < a.n_units) {
+        // successor step
+        int unxt = ucur, jnxt = jcur + 1;
+        if (jnxt >= cur.nkt_all) {
+          unxt = next_unit(a, ucur + gridDim.x, nxt);
+          jnxt = 0;
+        } else {
+          nxt = cur;
         }
-        if (blk >= 2) mbar_wait(&o_free[blk & 1], ((blk >> 1) - 1) & 1);  // epilogue of blk-2 read sL
-        sL[(blk & 1) * 128 + t] = l_run;
-        mbar_arrive(&l_full[blk & 1]);
+        const bool has_next = unxt < a.n_units;
+        const uint32_t tnext = gt + 1;
+        wait_tile(2 * gt + 1);  // V(cur)
+        if (jcur < cur.nkt[0]) issue_PV(0, cur, jcur, gt);
+        if (has_next) {
+          wait_tile(2 * tnext);  // K(next)
+          if (jnxt < nxt.nkt[0]) issue_S(0, nxt, jnxt, tnext);
+        }
+        if (jcur < cur.nkt[1]) issue_PV(1, cur, jcur, gt);
+        umma_commit(&t_free[(2 * gt + 1) % NSLOT]);  // V(cur) consumed by both PV
+        if (has_next) {
+          if (jnxt < nxt.nkt[1]) issue_S(1, nxt, jnxt, tnext);
+          umma_commit(&t_free[(2 * tnext) % NSLOT]);  // K(next) consumed by both S
+        }
+        ucur = unxt;
+        jcur = jnxt;
+        cur = nxt;
+        ++gt;
       }
     }
   } else {
-    // ---------------------------------------------------------------- epilogue (warps 4-7)
-    const int t = (warp & 3) * 32 + lane;  // TMEM lane of this thread's row
+    // ---------------------------------------------------------------- softmax + epilogue (tile h)
+    setmaxnreg_inc<176>();
+    const int h = warp >> 2;
+    const int t = threadIdx.x & 127;  // row of the tile == TMEM lane
     const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    int blk = 0;
-    Item it;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      if (!load_item(a, item, qpt, it)) continue;
-      for (int mb = 0; mb < it.n_mb; ++mb, ++blk) {
-        const int hh = t / qpt, qi = mb * qpt + (t - hh * qpt);
-        const uint32_t o_base = lane_base + O_COL + (blk & 1) * 128;
-        mbar_wait(&o_full[blk & 1], (blk >> 1) & 1);
-        mbar_wait(&l_full[blk & 1], (blk >> 1) & 1);
+    const uint32_t s_addr = lane_base + h * 128;
+    const uint32_t o_addr = lane_base + O_COL + h * 128;
+    int s_cnt = 0, o_cnt = 0;
+    Unit it;
+    for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
+      const int nkt_h = h ? it.nkt[1] : it.nkt[0];
+      if (!nkt_h) continue;
+      const int mb = it.mb0 + h;
+      const int hh = t / a.qpt, qi = mb * a.qpt + (t - hh * a.qpt);
+      const int pos = it.lcp + qi;  // keys 0..pos visible
+      const int pos_min = __reduce_min_sync(0xffffffffu, pos);
+      float m_run = -INFINITY, l_run = 0.f;
+#pragma unroll 1
+      for (int j = 0; j < nkt_h; ++j, ++s_cnt) {
+        mbar_wait(&s_full[h], s_cnt & 1);
         tc_fence_after();
-        const float l = sL[(blk & 1) * 128 + t];
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        const bool valid = qi < it.qlen;
-        __nv_bfloat16* orow = a.out + static_cast<int64_t>(it.q0 + (valid ? qi : 0)) * a.ld_out +
-                              static_cast<int64_t>(it.g * group + hh) * a.hd;
+        float sv[BK];
 #pragma unroll
-        for (int c = 0; c < HD; c += 32) {
-          if (c < a.hd) {
-            float ov[32];
-            tmem_ld32p(o_base + c, ov);
-            tmem_wait_ld();
-            if (valid) {
+        for (int c = 0; c < BK; c += 32) tmem_ld32p(s_addr + c, sv + c);
+        tmem_wait_ld();
+        const int kbase = j * BK;
+        if (kbase + BK - 1 > pos_min) {  // warp-uniform: some key of this warp's rows is masked
 #pragma unroll
-              for (int j = 0; j < 32; j += 8)
-                if (c + j < a.hd)
-                  st_global_v4(orow + c + j, pack_bf16x2(ov[j] * inv, ov[j + 1] * inv),
-                               pack_bf16x2(ov[j + 2] * inv, ov[j + 3] * inv),
-                               pack_bf16x2(ov[j + 4] * inv, ov[j + 5] * inv),
-                               pack_bf16x2(ov[j + 6] * inv, ov[j + 7] * inv));
+          for (int c = 0; c < BK; ++c) sv[c] = (kbase + c <= pos) ? sv[c] : -INFINITY;
+        }
+        float mx[8];
+#pragma unroll
+        for (int u8 = 0; u8 < 8; ++u8) mx[u8] = sv[u8];
+#pragma unroll
+        for (int c = 8; c < BK; ++c) mx[c & 7] = fmaxf(mx[c & 7], sv[c]);
+        const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * a.scale_log2;
+        const bool need = mt > m_run + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = need ? mt : m_run;
+          const float alpha = ex2(m_run - m_new);  // 0 on the first tile (m_run = -inf)
+          if (j > 0) {
+            // O_h holds PV_h(0..j-1): complete, since S_h(j) was issued after PV_h(j-1)
+#pragma unroll 1
+            for (int c = 0; c < HDP; c += 32) {
+              float ov[32];
+              tmem_ld32p(o_addr + c, ov);
+              tmem_wait_ld();
+#pragma unroll
+              for (int e = 0; e < 32; ++e) ov[e] *= alpha;
+              tmem_st32(o_addr + c, ov);
             }
           }
+          l_run *= alpha;
+          m_run = m_new;
         }
+        const float neg_m = -m_run;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < BK; c += 32) {
+          uint32_t pw[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float p0 = ex2(fmaf(sv[c + e], a.scale_log2, neg_m));
+            const float p1 = ex2(fmaf(sv[c + e + 1], a.scale_log2, neg_m));
+            ls[(e >> 1) & 3] += p0 + p1;
+            pw[e >> 1] = pack_bf16x2(p0, p1);
+          }
+          tmem_st16u(s_addr + c / 2, pw);  // P over the first 64 columns of S_h
+        }
+        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&o_free[blk & 1]);
+        mbar_arrive(&p_full[h]);
       }
+      // epilogue: O_h / l -> bf16 -> compact rows
+      mbar_wait(&o_full[h], o_cnt & 1);
+      tc_fence_after();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      const bool valid = qi < it.qlen;
+      __nv_bfloat16* orow = a.out + static_cast<int64_t>(it.q0 + (valid ? qi : 0)) * a.ld_out +
+                            static_cast<int64_t>(it.g * a.group + hh) * a.hd;
+#pragma unroll
+      for (int c = 0; c < HDP; c += 32) {
+        if (c < a.hd) {
+          float ov[32];
+          tmem_ld32p(o_addr + c, ov);
+          tmem_wait_ld();
+          if (valid) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 8)
+              if (c + e < a.hd)
+                st_global_v4(orow + c + e, pack_bf16x2(ov[e] * inv, ov[e + 1] * inv),
+                             pack_bf16x2(ov[e + 2] * inv, ov[e + 3] * inv),
+                             pack_bf16x2(ov[e + 4] * inv, ov[e + 5] * inv),
+                             pack_bf16x2(ov[e + 6] * inv, ov[e + 7] * inv));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&o_free[h]);
+      ++o_cnt;
     }
   }
   tc_fence_before();
@@ -458,35 +503,22 @@ __global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a, int n_it
   }
 }
 
-unsigned long long* g_trace = nullptr;  // debug: RDX_ATTN_TRACE=1 allocates 4096 x 64 timestamps
-
 template <int HDP>
-int launch(const Args& a, int64_t grid, cudaStream_t st) {
+int launch(const Args& a, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     RDX_CUDA_TRY(cudaFuncSetAttribute(attention_kernel<HDP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Tile<HDP>::SMEM));
     attr_set = true;
   }
-  const int64_t ctas = grid < num_sms() ? grid : num_sms();
-  attention_kernel<HDP><<<static_cast<unsigned>(ctas), kThreads, Tile<HDP>::SMEM, st>>>(a, static_cast<int>(grid));
+  const int ctas = a.n_units < num_sms() ? a.n_units : num_sms();
+  attention_kernel<HDP><<<static_cast<unsigned>(ctas), kThreads, Tile<HDP>::SMEM, st>>>(a);
   RDX_LAUNCH_CHECK();
   return RDX_OK;
 }
 
 }  // namespace attn
 }  // namespace rdx
-
-extern "C" int rdx_attention_trace(void* host_out, size_t bytes) {
-  using namespace rdx::attn;
-  if (!g_trace) {
-    if (cudaMalloc(&g_trace, 4096 * 64 * 8) != cudaSuccess) return RDX_ERR_CUDA;
-    cudaMemset(g_trace, 0, 4096 * 64 * 8);
-    return RDX_OK;
-  }
-  if (host_out) cudaMemcpy(host_out, g_trace, bytes < 4096 * 64 * 8 ? bytes : 4096 * 64 * 8, cudaMemcpyDeviceToHost);
-  return RDX_OK;
-}
 
 extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, const int32_t* scatter, const int32_t* cu,
                              const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len, int32_t heads, int32_t kv_heads,
@@ -510,9 +542,13 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, const int32_t
   a.heads = heads;
   a.kv_heads = kv_heads;
   a.hd = head_dim;
+  a.group = heads / kv_heads;
+  a.qpt = BQ / a.group;
+  const int64_t tiles = (static_cast<int64_t>(max_q_len) + a.qpt - 1) / a.qpt;
+  a.max_pairs = static_cast<int>((tiles + 1) / 2);
+  const int64_t units = static_cast<int64_t>(a.max_pairs) * n_seqs * kv_heads;
+  if (units >= (int64_t(1) << 31)) return RDX_ERR_CAPACITY_EXCEEDED;
+  a.n_units = static_cast<int>(units);
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  a.trace = g_trace;
-  const int64_t grid = n_seqs * kv_heads;
-  if (grid >= (int64_t(1) << 31)) return RDX_ERR_CAPACITY_EXCEEDED;
-  return head_dim <= 64 ? launch<64>(a, grid, as_stream(stream)) : launch<128>(a, grid, as_stream(stream));
+  return head_dim <= 64 ? launch<64>(a, as_stream(stream)) : launch<128>(a, as_stream(stream));
 }

@@ -1,35 +1,99 @@
-"""Scratch: time rdx_attention vs FA2 on the C2 suffix / plain shapes."""
-import math, os, sys
-import numpy as np, torch
+"""Time rdx_attention (suffix and plain layouts) on the C2 / C4 shapes; FA2 varlen beside it for context.
+
+  python scripts/attn_bench.py [c2|c4] [--no-fa2] [--iters N]
+"""
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2601_15013_b200 import build_plan, _native
-from paper_2601_15013_b200.plan import host_plan_cu_q
-from paper_2601_15013_b200.workloads import RerankSpec, msmarco_rerank_batch
-b = msmarco_rerank_batch(RerankSpec())
+from paper_2601_15013_b200 import _native, build_plan  # noqa: E402
+from paper_2601_15013_b200.plan import host_plan_cu_q  # noqa: E402
+from paper_2601_15013_b200.workloads import RerankSpec, long_prefix_batch, msmarco_rerank_batch  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "c2"
+iters = int(sys.argv[sys.argv.index("--iters") + 1]) if "--iters" in sys.argv else 20
+if cfg == "c2":
+    b, H, KV, hd = msmarco_rerank_batch(RerankSpec()), 16, 8, 128
+elif cfg == "c4":
+    b, H, KV, hd = long_prefix_batch(seed=0), 32, 8, 128
+else:
+    raise SystemExit(cfg)
 plan = build_plan(b)
-cu = b.cu_seqlens; cu_q = host_plan_cu_q(plan, cu)
+cu = b.cu_seqlens
+cu_q = host_plan_cu_q(plan, cu)
 m, n = plan.n_compact, b.num_tokens
-H, KV, hd = 16, 8, 128
-qkv = torch.randn(m, (H + 2 * KV) * hd, device="cuda").to(torch.bfloat16)
+g = torch.Generator(device="cuda").manual_seed(0)
+qkv = torch.randn(m, (H + 2 * KV) * hd, device="cuda", generator=g).to(torch.bfloat16)
 scatter = torch.from_numpy(np.array(plan.scatter_indices).view(np.int32)).cuda()
-cu32 = torch.tensor(cu, dtype=torch.int32, device="cuda"); cuq32 = torch.tensor(cu_q, dtype=torch.int32, device="cuda")
+cu32 = torch.tensor(cu, dtype=torch.int32, device="cuda")
+cuq32 = torch.tensor(cu_q, dtype=torch.int32, device="cuda")
 out = torch.empty(m, H * hd, dtype=torch.bfloat16, device="cuda")
-maxq = int(np.diff(cu_q).max()); maxk = int(np.diff(cu).max())
+maxq = int(np.diff(cu_q).max())
+maxk = int(np.diff(cu).max())
 lib = _native.lib()
+lens = np.diff(cu).astype(np.float64)
+lcp = lens - np.diff(cu_q)
+pairs_suffix = float(np.sum(lens * (lens + 1) / 2 - lcp * (lcp + 1) / 2))
+pairs_full = float(np.sum(lens * (lens + 1) / 2))
+
+
 def ours():
-    lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), scatter.data_ptr(), cu32.data_ptr(), cuq32.data_ptr(), len(cu)-1, maxq, H, KV, hd, 1/math.sqrt(hd), out.data_ptr(), out.stride(0), torch.cuda.current_stream().cuda_stream)
-qkv_full = torch.randn(n, (H + 2 * KV) * hd, device="cuda").to(torch.bfloat16)
+    lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), scatter.data_ptr(), cu32.data_ptr(), cuq32.data_ptr(),
+                      len(cu) - 1, maxq, H, KV, hd, 1 / math.sqrt(hd), out.data_ptr(), out.stride(0),
+                      torch.cuda.current_stream().cuda_stream)
+
+
+qkv_full = qkv[torch.from_numpy(np.array(plan.scatter_indices).astype(np.int64)).cuda()].contiguous()
 out_full = torch.empty(n, H * hd, dtype=torch.bfloat16, device="cuda")
+
+
 def ours_plain():
-    lib.rdx_attention(qkv_full.data_ptr(), qkv_full.stride(0), None, cu32.data_ptr(), cu32.data_ptr(), len(cu)-1, maxk, H, KV, hd, 1/math.sqrt(hd), out_full.data_ptr(), out_full.stride(0), torch.cuda.current_stream().cuda_stream)
-from flash_attn import flash_attn_varlen_func
-kvf = qkv_full[:, H*hd:]
-def fa2():
-    flash_attn_varlen_func(qkv[:, :H*hd].view(m, H, hd), kvf[:, :KV*hd].view(n, KV, hd), kvf[:, KV*hd:].view(n, KV, hd), cuq32, cu32, maxq, maxk, causal=True)
-def t(fn, it=50):
-    for _ in range(5): fn()
-    torch.cuda.synchronize(); s=torch.cuda.Event(enable_timing=True); e=torch.cuda.Event(enable_timing=True)
+    lib.rdx_attention(qkv_full.data_ptr(), qkv_full.stride(0), None, cu32.data_ptr(), cu32.data_ptr(), len(cu) - 1,
+                      maxk, H, KV, hd, 1 / math.sqrt(hd), out_full.data_ptr(), out_full.stride(0),
+                      torch.cuda.current_stream().cuda_stream)
+
+
+def t(fn, it=iters):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(it): fn()
-    e.record(); e.synchronize(); return s.elapsed_time(e)/it*1e3
-print("ours suffix us", round(t(ours),1), "ours plain us", round(t(ours_plain),1), "fa2 suffix us", round(t(fa2),1), flush=True)
+    for _ in range(it):
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / it * 1e3
+
+
+us_s = t(ours)
+us_p = t(ours_plain)
+tf_s = 4 * H * hd * pairs_suffix / (us_s * 1e-6) / 1e12
+tf_p = 4 * H * hd * pairs_full / (us_p * 1e-6) / 1e12
+print(f"{cfg}: N={n} N'={m} ours suffix {us_s:.1f} us ({tf_s:.0f} TF/s)  plain {us_p:.1f} us ({tf_p:.0f} TF/s)", flush=True)
+# parity of suffix vs plain (same math, different layouts)
+ours(); ours_plain(); torch.cuda.synchronize()
+sc = torch.from_numpy(np.array(plan.scatter_indices).astype(np.int64)).cuda()
+diff = (out[sc].float() - out_full.float()).abs().max().item()
+print(f"suffix-vs-plain max|diff| {diff:.3e}", flush=True)
+if "--no-fa2" not in sys.argv:
+    try:
+        from flash_attn import flash_attn_varlen_func
+
+        kvf = qkv_full[:, H * hd:]
+
+        def fa2():
+            flash_attn_varlen_func(qkv[:, :H * hd].view(m, H, hd), kvf[:, :KV * hd].view(n, KV, hd),
+                                   kvf[:, KV * hd:].view(n, KV, hd), cuq32, cu32, maxq, maxk, causal=True)
+
+        us_f = t(fa2)
+        print(f"fa2 suffix {us_f:.1f} us ({4 * H * hd * pairs_suffix / (us_f * 1e-6) / 1e12:.0f} TF/s)", flush=True)
+        ref = flash_attn_varlen_func(qkv[:, :H * hd].view(m, H, hd), kvf[:, :KV * hd].view(n, KV, hd),
+                                     kvf[:, KV * hd:].view(n, KV, hd), cuq32, cu32, maxq, maxk, causal=True)
+        print(f"ours-vs-fa2 max|diff| {(ref.reshape(m, -1).float() - out.float()).abs().max().item():.3e}")
+    except Exception as ex:  # library context only
+        print("fa2 unavailable:", ex)

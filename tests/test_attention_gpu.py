@@ -113,3 +113,44 @@ def test_long_prefix_c4_slice():
         torch.from_numpy(np.array(plan.gather_indices).astype(np.int64)).cuda()]
     err = (out.float() - ref).abs().max().item()
     assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("hd,H,KV,maxlen", [(128, 16, 8, 900), (128, 8, 1, 400), (64, 8, 8, 700), (96, 6, 3, 500)])
+def test_plain_long_and_ragged(hd, H, KV, maxlen):
+    """Many query-tile pairs per sequence, GQA groups 1..8, a non-power-of-two head dim,
+    and empty sequences in the batch (no work units, no output rows)."""
+    import torch
+
+    rng = np.random.default_rng(maxlen + H)
+    lens = rng.integers(1, maxlen, size=5)
+    lens[1] = 0
+    lens[3] = maxlen
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    n = int(cu[-1])
+    g = torch.Generator(device="cuda").manual_seed(4)
+    qkv = torch.randn(n, (H + 2 * KV) * hd, device="cuda", generator=g).to(torch.bfloat16)
+    out = _run(qkv, None, cu, cu, H, KV, hd, n)
+    ref = _reference(qkv, None, cu, H, KV, hd)
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
+
+
+def test_large_logit_range_rescale():
+    """Scores spanning > 2^8 between key tiles exercise the lazy O rescale path."""
+    import torch
+
+    H, KV, hd = 4, 2, 64
+    lens = np.array([700, 300])
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    n = int(cu[-1])
+    g = torch.Generator(device="cuda").manual_seed(5)
+    qkv = torch.randn(n, (H + 2 * KV) * hd, device="cuda", generator=g)
+    ramp = torch.linspace(0.1, 6.0, n, device="cuda")[:, None]  # later keys dominate more and more
+    qkv[:, H * hd:(H + KV) * hd] *= ramp
+    qkv[:, : H * hd] *= 3.0
+    qkv = qkv.to(torch.bfloat16)
+    out = _run(qkv, None, cu, cu, H, KV, hd, n)
+    ref = _reference(qkv, None, cu, H, KV, hd)
+    err = (out.float() - ref).abs().max().item()
+    assert torch.isfinite(out.float()).all()
+    assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
