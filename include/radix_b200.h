@@ -178,9 +178,10 @@ int rdx_gemm(const rdx_gemm_args* args, void* stream);
  *                             row cu[s] + j, i.e. plain / full layout)
  *   out[cu_q[s] + i, head]  = softmax(q k^T * scale, causal) v   (bf16)
  * qkv rows are [q heads | k heads | v heads] x head_dim (the QKV GEMM output);
- * head_dim <= 128, multiple of 8; heads % kv_heads == 0.
+ * head_dim <= 128, multiple of 8; heads % kv_heads == 0.  qkv_rows = rows of
+ * the qkv buffer (bounds the TMA tile loads; rows past it read as zeros).
  * --------------------------------------------------------------------- */
-int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, const int32_t* scatter, const int32_t* cu,
+int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const int32_t* scatter, const int32_t* cu,
                   const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len, int32_t heads, int32_t kv_heads,
                   int32_t head_dim, float softmax_scale, void* out_bf16, int64_t ld_out, void* stream);
 

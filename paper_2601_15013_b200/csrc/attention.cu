@@ -38,6 +38,8 @@
 //               of K and V tiles)
 //   warp  12    TMEM allocator + single-thread MMA issuer
 //   warps 13-15 idle (complete the warpgroup for setmaxnreg)
+#include <cstring>
+
 #include "common.cuh"
 
 namespace rdx {
@@ -142,6 +144,7 @@ struct Args {
   int group, qpt;            // heads / kv_heads, queries per tile (BQ / group)
   int max_pairs;             // query-tile pairs of the longest query range
   int n_units;               // max_pairs * nseq * kv_heads
+  int use_tma;               // head_dim % 64 == 0: whole 128-byte column boxes, TMA tile loads
   float scale_log2;          // softmax scale * log2(e)
 };
 
@@ -195,7 +198,8 @@ __device__ __forceinline__ int next_unit(const Args& a, int u, Unit& it) {
 }
 
 template <int HDP>
-__global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a) {
+__global__ void __launch_bounds__(kThreads, 1)
+attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q, Args a) {
   using T = Tile<HDP>;
   constexpr int Q_BYTES = T::Q_BYTES, T_BYTES = T::T_BYTES, CH = T::CH;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -256,6 +260,20 @@ __global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a) {
           if (q_cnt[h] > 0) mbar_wait(&q_free[h], (q_cnt[h] - 1) & 1);
           const uint32_t sq = smem_u32(sQ + h * Q_BYTES);
           const int mb = it.mb0 + h;
+          if (a.use_tma) {
+            // one box per (group head, 64-column half): qpt query rows of head g*group+hh
+            if (t == 0) {
+              mbar_arrive_expect_tx(&q_full[h], Q_BYTES);
+              for (int hh = 0; hh < a.group; ++hh)
+                for (int half = 0; half < T::HALVES; ++half)
+                  tma_load_2d(&map_q, sQ + h * Q_BYTES + half * (BQ * 128) + hh * a.qpt * 128, &q_full[h],
+                              (it.g * a.group + hh) * a.hd + half * 64, it.q0 + mb * a.qpt);
+            } else {
+              mbar_arrive(&q_full[h]);
+            }
+            ++q_cnt[h];
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < CH; ++k) {
             const int idx = t + k * 128;
@@ -284,6 +302,10 @@ __global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a) {
           int32_t* rows = s_rows + (seq & 2 ? BK : 0);  // seq advances by 2 per tile: alternate buffers
           rows[t] = row_next;
           named_bar_sync(1, 128);
+          const int row0 = rows[0];
+          // rows strictly increase along a trie path, but check every key: a contiguous
+          // run of compact rows is one TMA box per 64-column half, otherwise gather.
+          const bool contiguous = named_bar_and(1, 128, row_next < 0 || row_next == row0 + t) && a.use_tma;
           if (j + 1 < it.nkt_all) row_next = key_row(j + 1);
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv, ++seq) {
@@ -291,6 +313,18 @@ __global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a) {
             if (seq >= NSLOT) mbar_wait(&t_free[slot], ((seq / NSLOT) - 1) & 1);
             const uint32_t st = smem_u32(sT + slot * T_BYTES);
             const int64_t col = kv ? vcol : kcol;
+            if (contiguous) {
+              if (t == 0) {
+                mbar_arrive_expect_tx(&t_full[slot], T_BYTES);
+#pragma unroll
+                for (int half = 0; half < T::HALVES; ++half)
+                  tma_load_2d(&map_kv, sT + slot * T_BYTES + half * (BK * 128), &t_full[slot],
+                              static_cast<int32_t>(col) + half * 64, row0);
+              } else {
+                mbar_arrive(&t_full[slot]);
+              }
+              continue;
+            }
 #pragma unroll 8
             for (int k = 0; k < CH; ++k) {
               const int idx = t + k * 128;
@@ -504,15 +538,26 @@ __global__ void __launch_bounds__(kThreads, 1) attention_kernel(Args a) {
 }
 
 template <int HDP>
-int launch(const Args& a, cudaStream_t st) {
+int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     RDX_CUDA_TRY(cudaFuncSetAttribute(attention_kernel<HDP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Tile<HDP>::SMEM));
     attr_set = true;
   }
+  CUtensorMap map_kv, map_q;
+  std::memset(&map_kv, 0, sizeof(map_kv));
+  std::memset(&map_q, 0, sizeof(map_q));
+  if (a.use_tma) {
+    int e = gemm::make_map(&map_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, BK,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+    if (e) return e;
+    e = gemm::make_map(&map_q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, a.qpt,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+    if (e) return e;
+  }
   const int ctas = a.n_units < num_sms() ? a.n_units : num_sms();
-  attention_kernel<HDP><<<static_cast<unsigned>(ctas), kThreads, Tile<HDP>::SMEM, st>>>(a);
+  attention_kernel<HDP><<<static_cast<unsigned>(ctas), kThreads, Tile<HDP>::SMEM, st>>>(map_kv, map_q, a);
   RDX_LAUNCH_CHECK();
   return RDX_OK;
 }
@@ -520,7 +565,8 @@ int launch(const Args& a, cudaStream_t st) {
 }  // namespace attn
 }  // namespace rdx
 
-extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, const int32_t* scatter, const int32_t* cu,
+extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const int32_t* scatter,
+                             const int32_t* cu,
                              const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len, int32_t heads, int32_t kv_heads,
                              int32_t head_dim, float softmax_scale, void* out_bf16, int64_t ld_out, void* stream) {
   using namespace rdx;
@@ -550,5 +596,7 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, const int32_t
   if (units >= (int64_t(1) << 31)) return RDX_ERR_CAPACITY_EXCEEDED;
   a.n_units = static_cast<int>(units);
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  return head_dim <= 64 ? launch<64>(a, as_stream(stream)) : launch<128>(a, as_stream(stream));
+  a.use_tma = (head_dim % 64 == 0) && (reinterpret_cast<uintptr_t>(qkv_bf16) % 16 == 0) && qkv_rows > 0 &&
+              qkv_rows < (int64_t(1) << 31);
+  return head_dim <= 64 ? launch<64>(a, qkv_rows, as_stream(stream)) : launch<128>(a, qkv_rows, as_stream(stream));
 }

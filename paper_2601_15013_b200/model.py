@@ -392,7 +392,7 @@ class RadixQwen3:
         lib = _native.lib()
 
         def launch():
-            code = lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), None if scatter is None else scatter.data_ptr(),
+            code = lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), qkv.shape[0], None if scatter is None else scatter.data_ptr(),
                                      cu32.data_ptr(), cu_q32.data_ptr(), b, max(int(max_q), 1), cfg.num_heads,
                                      cfg.num_kv_heads, cfg.head_dim, 1.0 / math.sqrt(cfg.head_dim),
                                      out.data_ptr(), out.stride(0), stream)

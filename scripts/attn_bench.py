@@ -42,7 +42,7 @@ pairs_full = float(np.sum(lens * (lens + 1) / 2))
 
 
 def ours():
-    lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), scatter.data_ptr(), cu32.data_ptr(), cuq32.data_ptr(),
+    lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), qkv.shape[0], scatter.data_ptr(), cu32.data_ptr(), cuq32.data_ptr(),
                       len(cu) - 1, maxq, H, KV, hd, 1 / math.sqrt(hd), out.data_ptr(), out.stride(0),
                       torch.cuda.current_stream().cuda_stream)
 
@@ -52,7 +52,7 @@ out_full = torch.empty(n, H * hd, dtype=torch.bfloat16, device="cuda")
 
 
 def ours_plain():
-    lib.rdx_attention(qkv_full.data_ptr(), qkv_full.stride(0), None, cu32.data_ptr(), cu32.data_ptr(), len(cu) - 1,
+    lib.rdx_attention(qkv_full.data_ptr(), qkv_full.stride(0), qkv_full.shape[0], None, cu32.data_ptr(), cu32.data_ptr(), len(cu) - 1,
                       maxk, H, KV, hd, 1 / math.sqrt(hd), out_full.data_ptr(), out_full.stride(0),
                       torch.cuda.current_stream().cuda_stream)
 

@@ -43,7 +43,7 @@ def _run(qkv, scatter, cu, cu_q, H, KV, hd, m_out):
     cuq32 = torch.tensor(np.asarray(cu_q), dtype=torch.int32, device="cuda")
     out = torch.full((m_out, H * hd), float("nan"), dtype=torch.bfloat16, device="cuda")
     max_q = int(np.diff(np.asarray(cu_q)).max())
-    code = _native.lib().rdx_attention(qkv.data_ptr(), qkv.stride(0),
+    code = _native.lib().rdx_attention(qkv.data_ptr(), qkv.stride(0), qkv.shape[0],
                                        None if scatter is None else scatter.data_ptr(), cu32.data_ptr(),
                                        cuq32.data_ptr(), len(cu) - 1, max_q, H, KV, hd, 1.0 / math.sqrt(hd),
                                        out.data_ptr(), out.stride(0), _native.stream_handle())
