@@ -185,6 +185,12 @@ int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const 
                   const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len, int32_t heads, int32_t kv_heads,
                   int32_t head_dim, float softmax_scale, void* out_bf16, int64_t ld_out, void* stream);
 
+/* Debug: with RDX_ATTN_STATS=1 in the environment every rdx_attention launch
+ * sums per-role clock counters (MMA waits on K/V, P, Q, O; softmax waits on S,
+ * epilogue; loader waits on free slots; totals); this copies n slots to host
+ * and resets them. */
+int rdx_attention_debug_stats(unsigned long long* host, int n);
+
 /* ---------------------------------------------------------------------
  * Reranker scores from last-token logits (fp32 [B, ld]):
  *   score[b] = sigmoid(logits[b, yes_id] - logits[b, no_id])

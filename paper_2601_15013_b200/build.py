@@ -45,7 +45,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
     tmp = OUT + ".tmp"
-    cmd = [nvcc_path(), *ARCH_FLAGS, *NVCC_FLAGS, "-I", INCLUDE, "-o", tmp, *sources()]
+    extra = os.environ.get("RDX_NVCC_EXTRA", "").split()  # e.g. -DRDX_ATTN_STATS_BUILD=1 (debug counters)
+    cmd = [nvcc_path(), *ARCH_FLAGS, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-o", tmp, *sources()]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

@@ -38,6 +38,7 @@
 //               of K and V tiles)
 //   warp  12    TMEM allocator + single-thread MMA issuer
 //   warps 13-15 idle (complete the warpgroup for setmaxnreg)
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -52,6 +53,7 @@ constexpr int kThreads = 512;  // 16 warps
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
+constexpr uint32_t kEmulated = 0xA4u;      // pairs (mod 8) whose exp2 runs on the FMA pipe: 3 of 8
 
 template <int HDP>
 struct Tile {
@@ -84,6 +86,37 @@ __device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Warp-collective forms: every lane executes the asm with warp-uniform
+// operands, elect.sync picks the issuing lane (always the same one, so the
+// commits track that lane's MMAs).
+__device__ __forceinline__ void umma_ss_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
 }
 
@@ -146,7 +179,28 @@ struct Args {
   int n_units;               // max_pairs * nseq * kv_heads
   int use_tma;               // head_dim % 64 == 0: whole 128-byte column boxes, TMA tile loads
   float scale_log2;          // softmax scale * log2(e)
+  uint32_t emu_mask;         // pairs (mod 8) whose exp2 runs on the FMA pipe
+  unsigned long long* stats; // debug (RDX_ATTN_STATS=1): summed wait / busy clocks per role, else NULL
 };
+
+// Stats slots (summed over CTAs): see rdx_attention_debug_stats.
+enum { ST_MMA_TFULL, ST_MMA_PFULL, ST_MMA_QFULL, ST_MMA_OFREE, ST_MMA_TOTAL, ST_SM_SFULL, ST_SM_TOTAL,
+       ST_SM_EPI, ST_LD_FREE, ST_LD_TOTAL, ST_SM_RESCALE, ST_MMA_ISSUE,
+       ST_SM_LD, ST_SM_MAX, ST_SM_EXP, ST_SM_STW, ST_N };
+#ifndef RDX_ATTN_STATS_BUILD
+#define RDX_ATTN_STATS_BUILD 0  // 1: per-role clock counters (debug builds only)
+#endif
+#define RDX_STATS_ON (RDX_ATTN_STATS_BUILD && a.stats)
+#define RDX_TWAIT(bar, par, acc)                 \
+  do {                                           \
+    if (RDX_STATS_ON) {                          \
+      const long long _t0 = clock64();           \
+      mbar_wait(bar, par);                       \
+      acc += clock64() - _t0;                    \
+    } else {                                     \
+      mbar_wait(bar, par);                       \
+    }                                            \
+  } while (0)
 
 // 16-byte chunk c of a head row -> swizzled smem offset in a
 // [halves][rows][128 B] tile (half stride = rows * 128).
@@ -159,6 +213,49 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// Packed fp32 pairs (FFMA2 / FADD2 on sm_100).
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for a pair on the FMA pipe: x = j + f with j = rint(x), f in [-1/2, 1/2];
+// 2^f by a degree-3 fit (max relative error 7.7e-5, far below bf16's 2^-9),
+// 2^j added to the exponent field.  x is clamped at -126 (result ~1e-38, i.e.
+// zero at bf16 weight precision; -126 keeps the biased exponent >= 0 for
+// 2^f < 1); inputs are <= 8 (lazy max).
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  float x0, x1;
+  f2unpack(x, x0, x1);
+  const uint64_t xc = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+  const uint64_t t = fadd2(xc, f2pack(12582912.f, 12582912.f));  // 1.5 * 2^23: rint into the low bits
+  const uint64_t j = fadd2(t, f2pack(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(j, f2pack(-1.f, -1.f), xc);
+  uint64_t p = ffma2(f2pack(0.05508868f, 0.05508868f), f, f2pack(0.24260405f, 0.24260405f));
+  p = ffma2(p, f, f2pack(0.69327623f, 0.69327623f));
+  p = ffma2(p, f, f2pack(0.99992895f, 0.99992895f));
+  float p0, p1, t0, t1;
+  f2unpack(p, p0, p1);
+  f2unpack(t, t0, t1);
+  const uint32_t r0 = __float_as_uint(p0) + (__float_as_uint(t0) << 23);
+  const uint32_t r1 = __float_as_uint(p1) + (__float_as_uint(t1) << 23);
+  return f2pack(__uint_as_float(r0), __uint_as_float(r1));
 }
 
 // Unit geometry (identical in every role).  Units are ordered pair-index
@@ -197,7 +294,7 @@ __device__ __forceinline__ int next_unit(const Args& a, int u, Unit& it) {
   return a.n_units;
 }
 
-template <int HDP>
+template <int HDP, uint32_t EMU>
 __global__ void __launch_bounds__(kThreads, 1)
 attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q, Args a) {
   using T = Tile<HDP>;
@@ -249,6 +346,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
     if (warp < 12) {
       // ---------------------------------------------------------------- loaders
       const int t = threadIdx.x - 256;  // 0..127
+      long long st_free = 0;
+      const long long st_t0 = clock64();
       int q_cnt[2] = {0, 0};
       uint32_t seq = 0;  // K/V ring sequence number (K and V tiles alternate)
       Unit it;
@@ -257,7 +356,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
           if (!it.nkt[h]) continue;
-          if (q_cnt[h] > 0) mbar_wait(&q_free[h], (q_cnt[h] - 1) & 1);
+          if (q_cnt[h] > 0) RDX_TWAIT(&q_free[h], (q_cnt[h] - 1) & 1, st_free);
           const uint32_t sq = smem_u32(sQ + h * Q_BYTES);
           const int mb = it.mb0 + h;
           if (a.use_tma) {
@@ -310,7 +409,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv, ++seq) {
             const uint32_t slot = seq % NSLOT;
-            if (seq >= NSLOT) mbar_wait(&t_free[slot], ((seq / NSLOT) - 1) & 1);
+            if (seq >= NSLOT) RDX_TWAIT(&t_free[slot], ((seq / NSLOT) - 1) & 1, st_free);
             const uint32_t st = smem_u32(sT + slot * T_BYTES);
             const int64_t col = kv ? vcol : kcol;
             if (contiguous) {
@@ -338,90 +437,113 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           }
         }
       }
-    } else if (warp == 12 && lane == 0) {
+      if (RDX_STATS_ON && t == 0) {
+        atomicAdd(a.stats + ST_LD_FREE, static_cast<unsigned long long>(st_free));
+        atomicAdd(a.stats + ST_LD_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
+      }
+    } else if (warp == 12) {
       // ---------------------------------------------------------------- MMA issuer
-      int s_cnt[2] = {0, 0};   // S tiles issued per h (== P tiles consumed)
-      int o_cnt[2] = {0, 0};   // units finished per h
-      int q_cnt[2] = {0, 0};   // Q tiles consumed per h
-      uint32_t gt = 0;         // global key-tile counter (K at seq 2gt, V at 2gt+1)
+      // The whole warp walks the schedule (warp-uniform values stay in uniform
+      // registers); one elected lane issues each tcgen05 op.
+      long long st_t = 0, st_p = 0, st_q = 0, st_o = 0, st_iss = 0;
+      const long long st_t0 = clock64();
+      int s_cnt0 = 0, s_cnt1 = 0;  // S tiles issued per h (== P tiles consumed)
+      int o_cnt0 = 0, o_cnt1 = 0;  // units finished per h
+      int q_cnt0 = 0, q_cnt1 = 0;  // Q tiles consumed per h
+      uint32_t gt = 0;             // global key-tile counter (K at seq 2gt, V at 2gt+1)
 
-      auto issue_S = [&](int h, const Unit& U, int j, uint32_t tile) {
-        if (j == 0) {
-          mbar_wait(&q_full[h], q_cnt[h] & 1);
-        }
+      auto issue_S = [&](int h, int nkt_h, int j, uint32_t tile) {
+        int& q_cnt = h ? q_cnt1 : q_cnt0;
+        if (j == 0) RDX_TWAIT(&q_full[h], q_cnt & 1, st_q);
         const uint32_t kslot = (2 * tile) % NSLOT;
         fence_proxy_async_smem();
         tc_fence_after();
         const uint32_t qa = smem_u32(sQ + h * Q_BYTES), ka = smem_u32(sT + kslot * T_BYTES);
         const uint32_t sacc = tmem + h * 128;
         const uint64_t qd = sdesc(qa, 16, 1024), kd = sdesc(ka, 16, 1024);  // + (byte offset >> 4) per step
+        const long long st_i0 = RDX_STATS_ON ? clock64() : 0;
 #pragma unroll
         for (int kk = 0; kk < HDP / 16; ++kk)
-          umma_bf16(sacc, qd + (((kk >> 2) * (BQ * 128) + (kk & 3) * 32) >> 4),
-                    kd + (((kk >> 2) * (BK * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
-        umma_commit(&s_full[h]);
-        ++s_cnt[h];
-        if (j == U.nkt[h] - 1) {
-          umma_commit(&q_free[h]);
-          ++q_cnt[h];
+          umma_ss_elect(sacc, qd + (((kk >> 2) * (BQ * 128) + (kk & 3) * 32) >> 4),
+                        kd + (((kk >> 2) * (BK * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
+        commit_elect(&s_full[h]);
+        if (RDX_STATS_ON) st_iss += clock64() - st_i0;
+        if (h) ++s_cnt1; else ++s_cnt0;
+        if (j == nkt_h - 1) {
+          commit_elect(&q_free[h]);
+          ++q_cnt;
         }
       };
-      auto issue_PV = [&](int h, const Unit& U, int j, uint32_t tile) {
-        mbar_wait(&p_full[h], (s_cnt[h] - 1) & 1);  // P_h(j) published (S_h(j) was the last S of h)
-        if (j == 0 && o_cnt[h] > 0) mbar_wait(&o_free[h], (o_cnt[h] - 1) & 1);
+      auto issue_PV = [&](int h, int nkt_h, int j, uint32_t tile) {
+        int& o_cnt = h ? o_cnt1 : o_cnt0;
+        const int s_cnt = h ? s_cnt1 : s_cnt0;
+        RDX_TWAIT(&p_full[h], (s_cnt - 1) & 1, st_p);  // P_h(j) published (S_h(j) was the last S of h)
+        if (j == 0 && o_cnt > 0) RDX_TWAIT(&o_free[h], (o_cnt - 1) & 1, st_o);
         fence_proxy_async_smem();  // cp.async (generic proxy) V writes -> tcgen05 operand reads
         tc_fence_after();
         const uint32_t va = smem_u32(sT + ((2 * tile + 1) % NSLOT) * T_BYTES);
-        const uint32_t o = tmem + O_COL + h * 128;
+        const uint32_t o = tmem + O_COL + h * 128, pa = tmem + h * 128;
         const uint64_t vd = sdesc(va, BK * 128, 1024);
+        const long long st_i0 = RDX_STATS_ON ? clock64() : 0;
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk)
-          umma_ts(o, tmem + h * 128 + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
-        if (j == U.nkt[h] - 1) {
-          umma_commit(&o_full[h]);
-          ++o_cnt[h];
+          umma_ts_elect(o, pa + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+        if (RDX_STATS_ON) st_iss += clock64() - st_i0;
+        if (j == nkt_h - 1) {
+          commit_elect(&o_full[h]);
+          ++o_cnt;
         }
       };
-      auto wait_tile = [&](uint32_t seqno) {
-        mbar_wait(&t_full[seqno % NSLOT], (seqno / NSLOT) & 1);
-      };
+      auto wait_tile = [&](uint32_t seqno) { RDX_TWAIT(&t_full[seqno % NSLOT], (seqno / NSLOT) & 1, st_t); };
 
-      Unit cur, nxt;
-      int ucur = next_unit(a, blockIdx.x, cur);
+      Unit tmp;
+      int ucur = next_unit(a, blockIdx.x, tmp);
+      int c0 = tmp.nkt[0], c1 = tmp.nkt[1], call = tmp.nkt_all;  // key tiles of the current unit
       int jcur = 0;
       if (ucur < a.n_units) {
         wait_tile(2 * gt);
-        if (cur.nkt[0] > 0) issue_S(0, cur, 0, gt);
-        if (cur.nkt[1] > 0) issue_S(1, cur, 0, gt);
-        umma_commit(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
+        if (c0 > 0) issue_S(0, c0, 0, gt);
+        if (c1 > 0) issue_S(1, c1, 0, gt);
+        commit_elect(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
       }
       while (ucur < a.n_units) {
         // successor step
-        int unxt = ucur, jnxt = jcur + 1;
-        if (jnxt >= cur.nkt_all) {
-          unxt = next_unit(a, ucur + gridDim.x, nxt);
+        int unxt = ucur, jnxt = jcur + 1, n0 = c0, n1 = c1, nall = call;
+        if (jnxt >= call) {
+          unxt = next_unit(a, ucur + gridDim.x, tmp);
           jnxt = 0;
-        } else {
-          nxt = cur;
+          n0 = tmp.nkt[0];
+          n1 = tmp.nkt[1];
+          nall = tmp.nkt_all;
         }
         const bool has_next = unxt < a.n_units;
         const uint32_t tnext = gt + 1;
         wait_tile(2 * gt + 1);  // V(cur)
-        if (jcur < cur.nkt[0]) issue_PV(0, cur, jcur, gt);
+        if (jcur < c0) issue_PV(0, c0, jcur, gt);
         if (has_next) {
           wait_tile(2 * tnext);  // K(next)
-          if (jnxt < nxt.nkt[0]) issue_S(0, nxt, jnxt, tnext);
+          if (jnxt < n0) issue_S(0, n0, jnxt, tnext);
         }
-        if (jcur < cur.nkt[1]) issue_PV(1, cur, jcur, gt);
-        umma_commit(&t_free[(2 * gt + 1) % NSLOT]);  // V(cur) consumed by both PV
+        if (jcur < c1) issue_PV(1, c1, jcur, gt);
+        commit_elect(&t_free[(2 * gt + 1) % NSLOT]);  // V(cur) consumed by both PV
         if (has_next) {
-          if (jnxt < nxt.nkt[1]) issue_S(1, nxt, jnxt, tnext);
-          umma_commit(&t_free[(2 * tnext) % NSLOT]);  // K(next) consumed by both S
+          if (jnxt < n1) issue_S(1, n1, jnxt, tnext);
+          commit_elect(&t_free[(2 * tnext) % NSLOT]);  // K(next) consumed by both S
         }
         ucur = unxt;
         jcur = jnxt;
-        cur = nxt;
+        c0 = n0;
+        c1 = n1;
+        call = nall;
         ++gt;
+      }
+      if (RDX_STATS_ON && lane == 0) {
+        atomicAdd(a.stats + ST_MMA_TFULL, static_cast<unsigned long long>(st_t));
+        atomicAdd(a.stats + ST_MMA_PFULL, static_cast<unsigned long long>(st_p));
+        atomicAdd(a.stats + ST_MMA_QFULL, static_cast<unsigned long long>(st_q));
+        atomicAdd(a.stats + ST_MMA_OFREE, static_cast<unsigned long long>(st_o));
+        atomicAdd(a.stats + ST_MMA_ISSUE, static_cast<unsigned long long>(st_iss));
+        atomicAdd(a.stats + ST_MMA_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
       }
     }
   } else {
@@ -433,6 +555,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
     const uint32_t s_addr = lane_base + h * 128;
     const uint32_t o_addr = lane_base + O_COL + h * 128;
     int s_cnt = 0, o_cnt = 0;
+    long long st_s = 0, st_epi = 0, st_resc = 0, st_ld = 0, st_max = 0, st_exp = 0, st_stw = 0;
+    const long long st_t0 = clock64();
     Unit it;
     for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
       const int nkt_h = h ? it.nkt[1] : it.nkt[0];
@@ -444,16 +568,19 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       float m_run = -INFINITY, l_run = 0.f;
 #pragma unroll 1
       for (int j = 0; j < nkt_h; ++j, ++s_cnt) {
-        mbar_wait(&s_full[h], s_cnt & 1);
+        RDX_TWAIT(&s_full[h], s_cnt & 1, st_s);
+        const long long st_a = RDX_STATS_ON ? clock64() : 0;
         tc_fence_after();
         float sv[BK];
 #pragma unroll
         for (int c = 0; c < BK; c += 32) tmem_ld32p(s_addr + c, sv + c);
         tmem_wait_ld();
+        if (RDX_STATS_ON) st_ld += clock64() - st_a;
         const int kbase = j * BK;
         if (kbase + BK - 1 > pos_min) {  // warp-uniform: some key of this warp's rows is masked
+          const int nvis = pos - kbase + 1;  // visible keys of this row in the tile
 #pragma unroll
-          for (int c = 0; c < BK; ++c) sv[c] = (kbase + c <= pos) ? sv[c] : -INFINITY;
+          for (int c = 0; c < BK; ++c) sv[c] = c < nvis ? sv[c] : -INFINITY;
         }
         float mx[8];
 #pragma unroll
@@ -467,6 +594,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           const float m_new = need ? mt : m_run;
           const float alpha = ex2(m_run - m_new);  // 0 on the first tile (m_run = -inf)
           if (j > 0) {
+            if (RDX_STATS_ON) ++st_resc;
             // O_h holds PV_h(0..j-1): complete, since S_h(j) was issued after PV_h(j-1)
 #pragma unroll 1
             for (int c = 0; c < HDP; c += 32) {
@@ -481,26 +609,49 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           l_run *= alpha;
           m_run = m_new;
         }
-        const float neg_m = -m_run;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        const long long st_b = RDX_STATS_ON ? clock64() : 0;
+        if (RDX_STATS_ON) st_max += st_b - st_a;
+        const uint64_t scale2 = f2pack(a.scale_log2, a.scale_log2), negm2 = f2pack(-m_run, -m_run);
+        uint64_t ls[4] = {0, 0, 0, 0};  // pairs of fp32 partial row sums (+0.0f bits)
 #pragma unroll
         for (int c = 0; c < BK; c += 32) {
           uint32_t pw[16];
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            const float p0 = ex2(fmaf(sv[c + e], a.scale_log2, neg_m));
-            const float p1 = ex2(fmaf(sv[c + e + 1], a.scale_log2, neg_m));
-            ls[(e >> 1) & 3] += p0 + p1;
+            const uint64_t x = ffma2(f2pack(sv[c + e], sv[c + e + 1]), scale2, negm2);
+            uint64_t p;
+            if (EMU & (1u << ((e >> 1) & 7))) {
+              p = exp2_poly2(x);  // FMA-pipe exp2: offloads the MUFU unit
+            } else {
+              float x0, x1;
+              f2unpack(x, x0, x1);
+              p = f2pack(ex2(x0), ex2(x1));
+            }
+            ls[(e >> 1) & 3] = fadd2(ls[(e >> 1) & 3], p);
+            float p0, p1;
+            f2unpack(p, p0, p1);
             pw[e >> 1] = pack_bf16x2(p0, p1);
           }
           tmem_st16u(s_addr + c / 2, pw);  // P over the first 64 columns of S_h
         }
-        l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        {
+          float s0, s1, s2, s3;
+          f2unpack(fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3])), s0, s1);
+          (void)s2;
+          (void)s3;
+          l_run += s0 + s1;
+        }
+        const long long st_c = RDX_STATS_ON ? clock64() : 0;
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[h]);
+        if (RDX_STATS_ON) {
+          st_exp += st_c - st_b;
+          st_stw += clock64() - st_c;
+        }
       }
       // epilogue: O_h / l -> bf16 -> compact rows
+      const long long st_e0 = RDX_STATS_ON ? clock64() : 0;
       mbar_wait(&o_full[h], o_cnt & 1);
       tc_fence_after();
       const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -527,6 +678,17 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       tc_fence_before();
       mbar_arrive(&o_free[h]);
       ++o_cnt;
+      if (RDX_STATS_ON) st_epi += clock64() - st_e0;
+    }
+    if (RDX_STATS_ON && t == 0) {
+      atomicAdd(a.stats + ST_SM_SFULL, static_cast<unsigned long long>(st_s));
+      atomicAdd(a.stats + ST_SM_EPI, static_cast<unsigned long long>(st_epi));
+      atomicAdd(a.stats + ST_SM_RESCALE, static_cast<unsigned long long>(st_resc));
+      atomicAdd(a.stats + ST_SM_LD, static_cast<unsigned long long>(st_ld));
+      atomicAdd(a.stats + ST_SM_MAX, static_cast<unsigned long long>(st_max));
+      atomicAdd(a.stats + ST_SM_EXP, static_cast<unsigned long long>(st_exp));
+      atomicAdd(a.stats + ST_SM_STW, static_cast<unsigned long long>(st_stw));
+      atomicAdd(a.stats + ST_SM_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
     }
   }
   tc_fence_before();
@@ -537,11 +699,13 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
   }
 }
 
-template <int HDP>
+unsigned long long* g_stats = nullptr;  // debug counters (RDX_ATTN_STATS=1)
+
+template <int HDP, uint32_t EMU>
 int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    RDX_CUDA_TRY(cudaFuncSetAttribute(attention_kernel<HDP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    RDX_CUDA_TRY(cudaFuncSetAttribute(attention_kernel<HDP, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Tile<HDP>::SMEM));
     attr_set = true;
   }
@@ -557,7 +721,7 @@ int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
     if (e) return e;
   }
   const int ctas = a.n_units < num_sms() ? a.n_units : num_sms();
-  attention_kernel<HDP><<<static_cast<unsigned>(ctas), kThreads, Tile<HDP>::SMEM, st>>>(map_kv, map_q, a);
+  attention_kernel<HDP, EMU><<<static_cast<unsigned>(ctas), kThreads, Tile<HDP>::SMEM, st>>>(map_kv, map_q, a);
   RDX_LAUNCH_CHECK();
   return RDX_OK;
 }
@@ -596,7 +760,40 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
   if (units >= (int64_t(1) << 31)) return RDX_ERR_CAPACITY_EXCEEDED;
   a.n_units = static_cast<int>(units);
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
+  a.emu_mask = kEmulated;
+  if (const char* e = std::getenv("RDX_ATTN_EMU")) a.emu_mask = static_cast<uint32_t>(std::strtoul(e, nullptr, 16));
+  a.stats = nullptr;
+  if (const char* e = std::getenv("RDX_ATTN_STATS")) {
+    if (e[0] == '1') {
+      if (!g_stats) {
+        RDX_CUDA_TRY(cudaMalloc(&g_stats, ST_N * sizeof(unsigned long long)));
+        RDX_CUDA_TRY(cudaMemset(g_stats, 0, ST_N * sizeof(unsigned long long)));
+      }
+      a.stats = g_stats;
+    }
+  }
   a.use_tma = (head_dim % 64 == 0) && (reinterpret_cast<uintptr_t>(qkv_bf16) % 16 == 0) && qkv_rows > 0 &&
               qkv_rows < (int64_t(1) << 31);
-  return head_dim <= 64 ? launch<64>(a, qkv_rows, as_stream(stream)) : launch<128>(a, qkv_rows, as_stream(stream));
+  if (head_dim <= 64) return launch<64, kEmulated>(a, qkv_rows, as_stream(stream));
+#if RDX_ATTN_STATS_BUILD
+  switch (a.emu_mask) {  // debug builds: exp2 split experiments (RDX_ATTN_EMU=hex)
+    case 0x00: return launch<128, 0x00>(a, qkv_rows, as_stream(stream));
+    case 0xAA: return launch<128, 0xAA>(a, qkv_rows, as_stream(stream));
+    case 0xEE: return launch<128, 0xEE>(a, qkv_rows, as_stream(stream));
+    case 0xFF: return launch<128, 0xFF>(a, qkv_rows, as_stream(stream));
+    default: break;
+  }
+#endif
+  return launch<128, kEmulated>(a, qkv_rows, as_stream(stream));
+}
+
+// Debug: copy (and reset) the summed per-role clock counters of every launch
+// since the last call; n >= 11 slots (order: enum ST_* above).
+extern "C" int rdx_attention_debug_stats(unsigned long long* host, int n) {
+  using namespace rdx::attn;
+  if (!g_stats) return RDX_ERR_INVALID_ARGUMENT;
+  const int m = n < ST_N ? n : ST_N;
+  RDX_CUDA_TRY(cudaMemcpy(host, g_stats, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  RDX_CUDA_TRY(cudaMemset(g_stats, 0, ST_N * sizeof(unsigned long long)));
+  return RDX_OK;
 }

@@ -97,3 +97,19 @@ if "--no-fa2" not in sys.argv:
         print(f"ours-vs-fa2 max|diff| {(ref.reshape(m, -1).float() - out.float()).abs().max().item():.3e}")
     except Exception as ex:  # library context only
         print("fa2 unavailable:", ex)
+if os.environ.get("RDX_ATTN_STATS") == "1":
+    import ctypes
+
+    names = ["mma_wait_kv", "mma_wait_p", "mma_wait_q", "mma_wait_ofree", "mma_total", "sm_wait_s", "sm_total",
+             "sm_epilogue", "ld_wait_free", "ld_total", "sm_rescales", "mma_issue", "sm_ld", "sm_ld+max", "sm_exp", "sm_stwait"]
+    for label, fn in (("suffix", ours), ("plain", ours_plain)):
+        buf = (ctypes.c_ulonglong * 16)()
+        lib.rdx_attention_debug_stats(buf, 16)  # reset
+        fn()
+        torch.cuda.synchronize()
+        lib.rdx_attention_debug_stats(buf, 16)
+        v = list(buf)
+        print(label, "per-role clocks (fraction of role total):",
+              {n: round(x / max(v[4] if n.startswith("mma") else v[6] if n.startswith("sm") else v[9], 1), 3)
+               for n, x in zip(names, v)}, "sm_rescales", v[10], "mma_issue", round(v[11] / max(v[4], 1), 3),
+              "softmax parts", [round(x / max(v[6], 1), 3) for x in v[12:16]], flush=True)
