@@ -59,32 +59,42 @@ struct Cfg {
 };
 
 // ------------------------------------------------------------------ epilogue plumbing
+// Each epilogue warp owns kEpiWarpBytes of staging smem, used as a ring of
+// TMA-store boxes (32 rows x 32 columns): four 2 KB boxes for bf16 outputs,
+// two 4 KB boxes for fp32, so a warp keeps 3 (1) stores in flight.
+constexpr int kEpiWarpBytes = 2 * kEpiBoxBytes;
+
+template <int NB>
 struct EpiWarp {
-  uint8_t* buf[2];
+  uint8_t* base;
   int cur;
   int lane;
   int32_t row0;  // first global row of this warp's 32-row slab
 };
 
-__device__ __forceinline__ uint32_t epi_acquire(EpiWarp& e) {
-  if (e.lane == 0) bulk_wait_read<1>();  // the box written two emits ago has been read by its TMA store
+template <int NB>
+__device__ __forceinline__ uint32_t epi_acquire(EpiWarp<NB>& e) {
+  if (e.lane == 0) bulk_wait_read<NB - 1>();  // the box written NB emits ago has been read by its TMA store
   __syncwarp();
-  return smem_u32(e.buf[e.cur]);
+  return smem_u32(e.base + e.cur * (kEpiWarpBytes / NB));
 }
 
-__device__ __forceinline__ void epi_issue(EpiWarp& e, const CUtensorMap* map, int32_t c0, bool reduce_add) {
+template <int NB>
+__device__ __forceinline__ void epi_issue(EpiWarp<NB>& e, const CUtensorMap* map, int32_t c0, bool reduce_add) {
   fence_proxy_async_smem();
   __syncwarp();
   if (e.lane == 0) {
-    if (reduce_add) tma_reduce_add_2d(map, e.buf[e.cur], c0, e.row0);
-    else tma_store_2d(map, e.buf[e.cur], c0, e.row0);
+    const uint8_t* box = e.base + e.cur * (kEpiWarpBytes / NB);
+    if (reduce_add) tma_reduce_add_2d(map, box, c0, e.row0);
+    else tma_store_2d(map, box, c0, e.row0);
     bulk_commit();
   }
-  e.cur ^= 1;
+  e.cur = (e.cur + 1) % NB;
 }
 
 // 32 bf16 columns of this lane's row -> 64 B row of a SWIZZLE_64B box -> TMA store at (c0, row0).
-__device__ __forceinline__ void emit_bf16x32(EpiWarp& e, const float* v, const CUtensorMap* map, int32_t c0) {
+template <int NB>
+__device__ __forceinline__ void emit_bf16x32(EpiWarp<NB>& e, const float* v, const CUtensorMap* map, int32_t c0) {
   uint32_t w[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
@@ -96,7 +106,8 @@ __device__ __forceinline__ void emit_bf16x32(EpiWarp& e, const float* v, const C
 }
 
 // 32 fp32 columns -> 128 B row of a SWIZZLE_128B box -> TMA store or reduce-add.
-__device__ __forceinline__ void emit_f32x32(EpiWarp& e, const float* v, const CUtensorMap* map, int32_t c0,
+template <int NB>
+__device__ __forceinline__ void emit_f32x32(EpiWarp<NB>& e, const float* v, const CUtensorMap* map, int32_t c0,
                                             bool reduce_add) {
   const uint32_t base = epi_acquire(e) + e.lane * 128;
 #pragma unroll
@@ -125,8 +136,8 @@ __device__ __forceinline__ void rope_pair32(float* x1, float* x2, const float* w
 }
 
 // QKV epilogue for this warp's column range [c_lo, c_hi) of the tile (multiple of HD).
-template <int HD>
-__device__ __forceinline__ void qkv_cols(EpiWarp& e, uint32_t taddr, int64_t n0, int c_lo, int c_hi, int64_t N,
+template <int HD, int NB>
+__device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t n0, int c_lo, int c_hi, int64_t N,
                                          const EpiParams& ep, const float* s_qn, const float* s_kn,
                                          const float2* rope_row, const CUtensorMap* map) {
   if constexpr (HD >= 64) {
@@ -204,43 +215,57 @@ __device__ __forceinline__ void qkv_cols(EpiWarp& e, uint32_t taddr, int64_t n0,
 }
 
 // This warp: 32 rows (lane quarter) x columns [ch*BN/2, (ch+1)*BN/2) of the tile.
-template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_tile(EpiWarp& e, uint32_t taddr, int ch, int64_t gm_lane, int64_t M,
+// All of the warp's accumulator columns are read from TMEM with one wait,
+// then transformed in registers and emitted box by box.
+template <int BN, int EPI, int NB>
+__device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, int ch, int64_t gm_lane, int64_t M,
                                               int64_t n_blk, int64_t N, const EpiParams& ep, const float* s_qn,
                                               const float* s_kn, const CUtensorMap* map) {
+  constexpr int HALF = BN / 2;
   const int64_t n0 = n_blk * BN;
-  const int c_lo = ch * (BN / 2), c_hi = c_lo + BN / 2;
+  const int c_lo = ch * HALF;
+  float v[HALF];
+  if constexpr (EPI == RDX_EPI_SWIGLU) {
+    // warp ch owns outputs [ch*BN/4, (ch+1)*BN/4) of the tile's BN/2: output o of
+    // pair p = o/64 reads gate column p*128 + o%64 and up column +64
+#pragma unroll
+    for (int q = 0; q < HALF / 2; q += 32) {
+      const int o = ch * (HALF / 2) + q;
+      const int gcol = (o / kSwigluUnit) * 2 * kSwigluUnit + o % kSwigluUnit;
+      tmem_ld32p(taddr + gcol, v + q);
+      tmem_ld32p(taddr + gcol + kSwigluUnit, v + HALF / 2 + q);
+    }
+  } else if constexpr (EPI != RDX_EPI_QKV) {
+#pragma unroll
+    for (int c = 0; c < HALF; c += 32) tmem_ld32p(taddr + c_lo + c, v + c);
+  }
+  if constexpr (EPI != RDX_EPI_QKV) tmem_wait_ld();
   if constexpr (EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
-#pragma unroll 1
-    for (int c = c_lo; c < c_hi; c += 32) {
-      if (n0 + c >= N) break;
-      float v[32];
-      tmem_ld32p(taddr + c, v);
-      tmem_wait_ld();
-      if constexpr (EPI == RDX_EPI_STORE_BF16) emit_bf16x32(e, v, map, static_cast<int32_t>(n0 + c));
-      else emit_f32x32(e, v, map, static_cast<int32_t>(n0 + c), EPI == RDX_EPI_RESID_F32);
+#pragma unroll
+    for (int c = 0; c < HALF; c += 32) {
+      if (n0 + c_lo + c < N) {
+        if constexpr (EPI == RDX_EPI_STORE_BF16) emit_bf16x32(e, v + c, map, static_cast<int32_t>(n0 + c_lo + c));
+        else emit_f32x32(e, v + c, map, static_cast<int32_t>(n0 + c_lo + c), EPI == RDX_EPI_RESID_F32);
+      }
     }
   } else if constexpr (EPI == RDX_EPI_SWIGLU) {
-    // tile columns: [g(64) u(64)] x (BN/128); out col = n_blk*BN/2 + pair*64 + j
     const int64_t nout = N / 2;
-#pragma unroll 1
-    for (int p = c_lo / (2 * kSwigluUnit); p < c_hi / (2 * kSwigluUnit); ++p) {
-      const int64_t ocol0 = n_blk * (BN / 2) + p * kSwigluUnit;
-      if (ocol0 >= nout) break;
-#pragma unroll 1
-      for (int c = 0; c < kSwigluUnit; c += 32) {
-        float g[32], u[32];
-        tmem_ld32p(taddr + p * 2 * kSwigluUnit + c, g);
-        tmem_ld32p(taddr + p * 2 * kSwigluUnit + kSwigluUnit + c, u);
-        tmem_wait_ld();
+#pragma unroll
+    for (int q = 0; q < HALF / 2; q += 32) {
+      const int64_t ocol = n_blk * (BN / 2) + ch * (HALF / 2) + q;
+      if (ocol < nout) {
+        float* g = v + q;
+        const float* u = v + HALF / 2 + q;
 #pragma unroll
         for (int j = 0; j < 32; ++j) g[j] = __fdividef(g[j], 1.f + __expf(-g[j])) * u[j];
-        emit_bf16x32(e, g, map, static_cast<int32_t>(ocol0 + c));
+        emit_bf16x32(e, g, map, static_cast<int32_t>(ocol));
       }
     }
   } else if constexpr (EPI == RDX_EPI_QKV) {
+    // chunked: TMEM loads interleaved with the norm / RoPE math and the stores
     const int64_t r = gm_lane < M ? gm_lane : (M > 0 ? M - 1 : 0);
     const float2* rope_row = ep.rope + r * (ep.hd >> 1);
+    const int c_hi = c_lo + HALF;
     switch (ep.hd) {
       case 128: qkv_cols<128>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
       case 64: qkv_cols<64>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
@@ -342,7 +367,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // whole warp walks the schedule; one elected lane issues
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -360,18 +385,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // +32 B per K=16 step inside the 128 B swizzle atom (encoded >> 4)
-            if constexpr (CG == 2) umma_bf16_cg2(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
-            else umma_bf16(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
+            if constexpr (CG == 2) umma_bf16_cg2_elect(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
+            else umma_bf16_elect(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
           }
-          if constexpr (CG == 2) umma_commit_cg2_mc(&empty[stage], 0x3);
-          else umma_commit(&empty[stage]);
+          if constexpr (CG == 2) umma_commit_cg2_mc_elect(&empty[stage], 0x3);
+          else umma_commit_elect(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if constexpr (CG == 2) umma_commit_cg2_mc(&tfull[acc], 0x3);
-        else umma_commit(&tfull[acc]);
+        if constexpr (CG == 2) umma_commit_cg2_mc_elect(&tfull[acc], 0x3);
+        else umma_commit_elect(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -380,9 +405,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int ch = ew >> 2;  // column half of the tile
-    EpiWarp e;
-    e.buf[0] = epi_smem + ew * 2 * kEpiBoxBytes;
-    e.buf[1] = e.buf[0] + kEpiBoxBytes;
+    constexpr int NB = (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) ? 2 : 4;
+    EpiWarp<NB> e;
+    e.base = epi_smem + ew * kEpiWarpBytes;
     e.cur = 0;
     e.lane = lane;
     const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
@@ -395,7 +420,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       e.row0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM + q * 32);
-      epilogue_tile<BN, EPI>(e, taddr, ch, e.row0 + lane, M, n_blk, N, ep, s_norm, s_norm + 128, &tmC);
+      epilogue_tile<BN, EPI, NB>(e, taddr, ch, e.row0 + lane, M, n_blk, N, ep, s_norm, s_norm + 128, &tmC);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
