@@ -322,6 +322,127 @@ def cpu_sample(config, batch, seqs=8, layers=(1, 2)):
             "seconds": round(ts[1] + ts[2] + t_plan, 2)}
 
 
+# ------------------------------------------------------------------ C5 microbenchmark
+def _event_time(fn, iters=10, warm=2, flush=None):
+    """Median CUDA-event time (ms) of fn on the current stream, L2 flushed before each call."""
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        if flush:
+            flush()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        e.synchronize()
+        ts.append(s.elapsed_time(e))
+    return statistics.median(ts)
+
+
+def run_micro(args):
+    """BASELINE configs[4]: index build and gather/scatter over ragged batches of
+    1K-1M tokens (prefix-sharing ratios 0..1, multi-level tries): GPU planner
+    time vs the CPU restatement of the reference trie (1 thread, as the
+    reference's numba build), and row gather/scatter GB/s vs measured HBM."""
+    import ctypes
+
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2601_15013_b200 import _native
+    from paper_2601_15013_b200.plan import _WORKSPACE, build_plan_device, upload_batch
+    from paper_2601_15013_b200.ops import gather_rows_device
+    from paper_2601_15013_b200.workloads import multilevel_batch, prefix_ratio_batch
+
+    torch.cuda.set_device(0)
+    peaks, peaks_src = load_peaks()
+    hbm = peaks["hbm_gbs"]
+    lib = _native.lib()
+    flush = L2Flusher()
+    sizes = [1 << 10, 1 << 14, 1 << 17, 1 << 20]
+    cases = [(f"ratio{r:.2f}", n, lambda n=n, r=r: prefix_ratio_batch(n, r)) for n in sizes
+             for r in (0.0, 0.25, 0.5, 0.75, 1.0)]
+    cases += [("multilevel", n, lambda n=n: multilevel_batch(n)) for n in sizes]
+    plans = []
+    for name, n, make in cases:
+        batch = make()
+        tok, pos, cu = upload_batch(batch)
+        b = int(cu.shape[0]) - 1
+        nn = int(tok.shape[0])
+        gather = torch.empty(nn, dtype=torch.int32, device="cuda")
+        scatter = torch.empty_like(gather)
+        cpos = torch.empty_like(gather)
+        info = torch.empty(4 + b + 1, dtype=torch.int32, device="cuda")
+        lcp = torch.empty(max(b, 1), dtype=torch.int32, device="cuda")
+        scratch = _WORKSPACE.get(tok.device, int(lib.rdx_plan_scratch_bytes(nn, b)))
+        st = _native.stream_handle()
+
+        def kernel_only():
+            _native.check(lib.rdx_plan_build(tok.data_ptr(), pos.data_ptr(), cu.data_ptr(), b, nn, 0,
+                                             gather.data_ptr(), scatter.data_ptr(), cpos.data_ptr(),
+                                             info.data_ptr() + 16, lcp.data_ptr(), info.data_ptr(),
+                                             scratch.data_ptr(), ctypes.c_size_t(scratch.numel()), st),
+                          "rdx_plan_build")
+
+        ms_kernel = _event_time(kernel_only, flush=flush)
+        ms_api = _event_time(lambda: build_plan_device(tok, pos, cu), flush=flush)
+        plan = build_plan_device(tok, pos, cu)
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            g, sc, cp, m = orc.build_plan_oracle(batch.token_ids, batch.position_ids, batch.cu_seqlens)
+            reps += 1
+            if time.perf_counter() - t0 > 0.2 or reps >= 20:
+                break
+        cpu_ms = (time.perf_counter() - t0) * 1e3 / reps
+        ok = (m == plan.n_compact and np.array_equal(plan.scatter.cpu().numpy().view(np.uint32), sc))
+        nbytes = 12 * nn + 8 * plan.n_compact + 8 * (b + 1)
+        plans.append({"case": name, "N": nn, "B": b, "N_compact": plan.n_compact,
+                      "gamma": round(plan.n_compact / max(nn, 1), 4), "gpu_kernel_us": round(ms_kernel * 1e3, 1),
+                      "gpu_api_us": round(ms_api * 1e3, 1), "cpu_ref_port_us": round(cpu_ms * 1e3, 1),
+                      "speedup_kernel_vs_cpu": round(cpu_ms / ms_kernel, 1),
+                      "index_gbs": round(nbytes / (ms_kernel * 1e-3) / 1e9, 1), "bit_exact_vs_oracle": bool(ok)})
+        if name == "ratio0.50" or name == "multilevel":
+            plans[-1]["_dev"] = (plan, nn)
+    rows = []
+    for rec in plans:
+        dev = rec.pop("_dev", None)
+        if dev is None or rec["N"] < (1 << 14):
+            continue
+        plan, nn = dev
+        for d in (1024, 2560, 4096, 6144):
+            x = torch.randn(plan.n_compact, d, device="cuda").to(torch.bfloat16)
+            full = torch.empty(nn, d, dtype=torch.bfloat16, device="cuda")
+            comp = torch.empty(plan.n_compact, d, dtype=torch.bfloat16, device="cuda")
+            ms_s = _event_time(lambda: gather_rows_device(x, plan.scatter, out=full), flush=flush)
+            ms_g = _event_time(lambda: gather_rows_device(full, plan.gather, out=comp), flush=flush)
+            rb = 2 * d
+            alg_s = nn * (2 * rb + 4)
+            alg_g = plan.n_compact * (2 * rb + 4)
+            uniq_s = plan.n_compact * rb + nn * rb + 4 * nn  # each compact row read once from DRAM
+            rows.append({"case": rec["case"], "N": nn, "N_compact": plan.n_compact, "d": d,
+                         "scatter_us": round(ms_s * 1e3, 1), "scatter_gbs": round(alg_s / (ms_s * 1e-3) / 1e9, 1),
+                         "scatter_dram_gbs": round(uniq_s / (ms_s * 1e-3) / 1e9, 1),
+                         "gather_us": round(ms_g * 1e3, 1), "gather_gbs": round(alg_g / (ms_g * 1e-3) / 1e9, 1)})
+            del x, full, comp
+    gather = gather_microbench(hbm)
+    best = max(r["gather_gbs"] for r in rows) if rows else gather["gbs"]
+    line = {"metric": "C5 index build + row gather/scatter microbenchmark", "value": round(best, 1),
+            "unit": "GB/s", "n_gpus": 1, "higher_is_better": True, "dtype": "u32 indices / bf16 rows",
+            "data": "synthetic", "config": {"workload": "c5: 1K-1M tokens, seq 512, prefix ratio 0..1, multi-level",
+                                            "l2": "L2 flushed (256 MiB write) before each timed call"},
+            "hbm_peak_gbs": hbm, "peak_source": peaks_src,
+            "bytes_convention": "gather/scatter: 2*rows_out*row_bytes + 4*rows_out; index: 12N + 8N' + 8(B+1)",
+            "index_build": plans, "row_ops": rows, "gather_table6": gather,
+            "cpu_baseline": {"kind": "port", "cores": 1,
+                             "sample": "oracle/trie_oracle.c (C restatement of trie.py:73-122), full batch"}}
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ arms
 def run_reference(args):
     rank, world, local = dist_env()
@@ -467,7 +588,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--profile", action="store_true", help="radix steps only, for ncu")
@@ -475,7 +596,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
-    if args.impl == "reference":
+    if args.config == "c5" and args.impl == "ours":
+        run_micro(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -145,3 +145,41 @@ def long_prefix_batch(B: int = 128, prefix_len: int = 2048, suffix_len: int = 25
     """C4: SyntheticSpec(B, 2048, 256, vocab 151936) -> N'=P+B*S exactly."""
     return make_synthetic_batch(SyntheticSpec(B=B, prefix_len=prefix_len, suffix_len=suffix_len,
                                               vocab=vocab, seed=seed))
+
+
+def prefix_ratio_batch(n_tokens: int, ratio: float, seq_len: int = 512, vocab: int = 151936,
+                       seed: int = 0) -> RaggedBatch:
+    """C5 (Table 5 of the paper): n_tokens / seq_len sequences of
+    seq_len tokens whose first round(ratio * seq_len) tokens are shared."""
+    b = max(1, n_tokens // seq_len)
+    p = int(round(ratio * seq_len))
+    return make_synthetic_batch(SyntheticSpec(B=b, prefix_len=p, suffix_len=seq_len - p, vocab=vocab, seed=seed))
+
+
+def multilevel_batch(n_tokens: int, levels=((64, 1), (64, 4), (128, 4)), leaf_len: int = 256,
+                     vocab: int = 151936, seed: int = 0) -> RaggedBatch:
+    """C5 multi-level trie: a tree whose level i has `fanout` children of `length`
+    tokens each (each child diverges at its first token); every root-to-leaf
+    path gets its own leaf_len-token unique tail.  Paths repeat the tree until
+    n_tokens is reached (distinct trees per repetition)."""
+    rng = np.random.default_rng(seed)
+    seq_len = sum(length for length, _ in levels) + leaf_len
+    seqs = []
+    while sum(len(s) for s in seqs) + seq_len <= max(n_tokens, seq_len):
+        paths = [np.zeros(0, dtype=np.uint32)]
+        for length, fanout in levels:
+            nxt = []
+            for pth in paths:
+                firsts = rng.permutation(vocab)[:fanout]
+                for f in firsts:
+                    seg = rng.integers(0, vocab, size=length, dtype=np.uint32)
+                    seg[0] = f
+                    nxt.append(np.concatenate([pth, seg]))
+            paths = nxt
+        for pth in paths:
+            seqs.append(np.concatenate([pth, rng.integers(0, vocab, size=leaf_len, dtype=np.uint32)]))
+            if sum(len(s) for s in seqs) + seq_len > max(n_tokens, seq_len):
+                break
+    tokens = np.concatenate(seqs).astype(np.uint32)
+    cu = np.cumsum([0] + [len(x) for x in seqs]).astype(np.int64)
+    return RaggedBatch(tokens, default_positions(cu), cu)
