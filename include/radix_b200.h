@@ -180,10 +180,13 @@ int rdx_gemm(const rdx_gemm_args* args, void* stream);
  * qkv rows are [q heads | k heads | v heads] x head_dim (the QKV GEMM output);
  * head_dim <= 128, multiple of 8; heads % kv_heads == 0.  qkv_rows = rows of
  * the qkv buffer (bounds the TMA tile loads; rows past it read as zeros).
+ * max_q_len / max_k_len = longest query range / sequence (max_k_len only
+ * selects the tile pipeline; 0 = unknown).
  * --------------------------------------------------------------------- */
 int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const int32_t* scatter, const int32_t* cu,
-                  const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len, int32_t heads, int32_t kv_heads,
-                  int32_t head_dim, float softmax_scale, void* out_bf16, int64_t ld_out, void* stream);
+                  const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len, int32_t max_k_len, int32_t heads,
+                  int32_t kv_heads, int32_t head_dim, float softmax_scale, void* out_bf16, int64_t ld_out,
+                  void* stream);
 
 /* Debug: with RDX_ATTN_STATS=1 in the environment every rdx_attention launch
  * sums per-role clock counters (MMA waits on K/V, P, Q, O; softmax waits on S,

@@ -94,7 +94,8 @@ _SIGNATURES = {
     "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmArgs), _vp]),
     "rdx_rerank_scores": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
-    "rdx_attention": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _f32, _vp, _i64, _vp]),
+    "rdx_attention": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i64,
+                                      _vp]),
     "rdx_attention_debug_stats": (ctypes.c_int, [_vp, _i32]),
     "rdx_num_sms": (ctypes.c_int, []),
 }

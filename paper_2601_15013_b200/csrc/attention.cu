@@ -30,14 +30,22 @@
 // than 2^8 (exact: the final O / l uses the same max), so O is rescaled in
 // TMEM only on the rare large jumps.
 //
+// Loads.  One loader warp.  Q tiles: one TMA box per (group head, 64-column
+// half).  K/V tiles: a 128-key tile whose compact rows form one contiguous
+// run (always in plain layout and for long shared prefixes) is one TMA box
+// per half; otherwise each 16-key group that is a contiguous run is one
+// 16-row box and the other groups use TMA gather4 (4 arbitrary rows per
+// instruction).  Head dims that are not a multiple of 64 fall back to
+// cp.async 16-byte copies.  Short units (few key tiles) double-buffer Q so
+// the next unit's Q streams in while the current one computes.
+//
 // 16 warps (setmaxnreg re-balances registers toward the softmax groups):
-//   warps 0-3   softmax + epilogue of query tile 0 (row t = TMEM lane t)
-//   warps 4-7   softmax + epilogue of query tile 1
-//   warps 8-11  loaders: cp.async 16-byte gathers of Q and of K/V through the
-//               scatter map into 128-byte-swizzled UMMA layouts (4-slot ring
-//               of K and V tiles)
-//   warp  12    TMEM allocator + single-thread MMA issuer
-//   warps 13-15 idle (complete the warpgroup for setmaxnreg)
+//   warps 0-3    softmax of query tile 0 (row t = TMEM lane t)
+//   warps 4-7    softmax of query tile 1
+//   warp  8      loader
+//   warps 9-12   epilogue: O_h / l -> bf16 compact rows (TMEM lane quarters 1,2,3,0)
+//   warp  13     TMEM allocator + MMA issuer (warp-uniform, elect.sync issue)
+//   warps 14-15  idle (complete the warpgroup for setmaxnreg)
 #include <cstdlib>
 #include <cstring>
 
@@ -48,22 +56,26 @@ namespace attn {
 
 constexpr int BQ = 128;        // rows per query tile (group heads x queries)
 constexpr int BK = 128;        // keys per K/V tile
-constexpr int NSLOT = 4;       // K/V ring slots (K and V tiles alternate)
 constexpr int kThreads = 512;  // 16 warps
+constexpr int kLoaderWarp = 8, kMmaWarp = 13;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
 constexpr uint32_t kEmulated = 0xA4u;      // pairs (mod 8) whose exp2 runs on the FMA pipe: 3 of 8
+constexpr int kShortUnitTiles = 4;         // <= this many key tiles per unit: double-buffered Q
 
-template <int HDP>
+// NQB = Q buffers per query tile, NSLOT = K/V ring slots (K and V tiles alternate).
+template <int HDP, int NQB, int NSLOT>
 struct Tile {
   static constexpr int HALVES = HDP / 64;
   static constexpr int CH = HDP / 8;               // 16-byte chunks per row
   static constexpr int Q_BYTES = BQ * HDP * 2;     // HALVES x 128 rows x 128 B
   static constexpr int T_BYTES = BK * HDP * 2;     // one K or V tile
-  static constexpr int BAR_OFF = 2 * Q_BYTES + NSLOT * T_BYTES;
-  static constexpr int ROWS_OFF = BAR_OFF + 256;   // int32 [2][BK] compact rows of the current key tile
-  static constexpr int SMEM = ROWS_OFF + 2 * BK * 4 + 1024;  // + alignment slack
+  static constexpr int T_OFF = 2 * NQB * Q_BYTES;
+  static constexpr int L_OFF = T_OFF + NSLOT * T_BYTES;  // fp32 [2 h][2 slots][128] row sums
+  static constexpr int BAR_OFF = L_OFF + 2 * 2 * BQ * 4;
+  static constexpr int SMEM = BAR_OFF + 256;
+  static_assert(SMEM <= 232448, "shared memory budget");
   static constexpr uint32_t IDESC_S = umma_idesc_bf16(BQ, BK);
   static constexpr uint32_t IDESC_PV = umma_idesc_bf16(BQ, HDP) | (1u << 16);  // B (V) MN-major
 };
@@ -78,19 +90,8 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo_bytes, ui
   return d;
 }
 
-// D[tmem] (+)= A[tmem] * B[smem], kind::f16 (A = P in TMEM, bf16 pairs per 32-bit column).
-__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// Warp-collective forms: every lane executes the asm with warp-uniform
-// operands, elect.sync picks the issuing lane (always the same one, so the
+// Warp-collective tcgen05 issue (every lane runs the asm with warp-uniform
+// operands; elect.sync picks the issuing lane, always the same one, so the
 // commits track that lane's MMAs).
 __device__ __forceinline__ void umma_ss_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                               uint32_t accumulate) {
@@ -102,6 +103,7 @@ __device__ __forceinline__ void umma_ss_elect(uint32_t d_tmem, uint64_t a_desc, 
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem]: A = P in TMEM, bf16 pairs per 32-bit column.
 __device__ __forceinline__ void umma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                               uint32_t accumulate) {
   asm volatile(
@@ -146,7 +148,6 @@ __device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t* v) {
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
 // 16-byte async global -> shared copy (L2 only); src_bytes = 0 zero-fills.
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
@@ -155,7 +156,6 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-
 template <uint32_t N>
 __device__ __forceinline__ void setmaxnreg_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
@@ -164,51 +164,6 @@ template <uint32_t N>
 __device__ __forceinline__ void setmaxnreg_dec() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
-
-struct Args {
-  const __nv_bfloat16* qkv;  // [rows, ld] compact (or full, plain mode)
-  int64_t ld;                // elements
-  const int32_t* scatter;    // [N] original -> compact row; NULL = identity (plain mode)
-  const int32_t* cu;         // [B+1] original offsets
-  const int32_t* cu_q;       // [B+1] query-row offsets (= cu in plain mode)
-  __nv_bfloat16* out;        // [rows_q, ld_out]
-  int64_t ld_out;
-  int nseq, heads, kv_heads, hd;
-  int group, qpt;            // heads / kv_heads, queries per tile (BQ / group)
-  int max_pairs;             // query-tile pairs of the longest query range
-  int n_units;               // max_pairs * nseq * kv_heads
-  int use_tma;               // head_dim % 64 == 0: whole 128-byte column boxes, TMA tile loads
-  float scale_log2;          // softmax scale * log2(e)
-  uint32_t emu_mask;         // pairs (mod 8) whose exp2 runs on the FMA pipe
-  unsigned long long* stats; // debug (RDX_ATTN_STATS=1): summed wait / busy clocks per role, else NULL
-};
-
-// Stats slots (summed over CTAs): see rdx_attention_debug_stats.
-enum { ST_MMA_TFULL, ST_MMA_PFULL, ST_MMA_QFULL, ST_MMA_OFREE, ST_MMA_TOTAL, ST_SM_SFULL, ST_SM_TOTAL,
-       ST_SM_EPI, ST_LD_FREE, ST_LD_TOTAL, ST_SM_RESCALE, ST_MMA_ISSUE,
-       ST_SM_LD, ST_SM_MAX, ST_SM_EXP, ST_SM_STW, ST_N };
-#ifndef RDX_ATTN_STATS_BUILD
-#define RDX_ATTN_STATS_BUILD 0  // 1: per-role clock counters (debug builds only)
-#endif
-#define RDX_STATS_ON (RDX_ATTN_STATS_BUILD && a.stats)
-#define RDX_TWAIT(bar, par, acc)                 \
-  do {                                           \
-    if (RDX_STATS_ON) {                          \
-      const long long _t0 = clock64();           \
-      mbar_wait(bar, par);                       \
-      acc += clock64() - _t0;                    \
-    } else {                                     \
-      mbar_wait(bar, par);                       \
-    }                                            \
-  } while (0)
-
-// 16-byte chunk c of a head row -> swizzled smem offset in a
-// [halves][rows][128 B] tile (half stride = rows * 128).
-__device__ __forceinline__ uint32_t sw_off(int row, int c, int rows) {
-  const int half = c >> 3, cc = c & 7;
-  return half * rows * 128 + row * 128 + ((cc ^ (row & 7)) << 4);
-}
-
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -258,12 +213,63 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
   return f2pack(__uint_as_float(r0), __uint_as_float(r1));
 }
 
+// TMA gather4: rows r0..r3 (64 columns each, box {64, 1}) -> 4 consecutive 128-byte smem rows.
+__device__ __forceinline__ void tma_gather4(const CUtensorMap* map, uint32_t dst, uint64_t* bar, int32_t col,
+                                            int32_t r0, int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
+struct Args {
+  const __nv_bfloat16* qkv;  // [rows, ld] compact (or full, plain mode)
+  int64_t ld;                // elements
+  const int32_t* scatter;    // [N] original -> compact row; NULL = identity (plain mode)
+  const int32_t* cu;         // [B+1] original offsets
+  const int32_t* cu_q;       // [B+1] query-row offsets (= cu in plain mode)
+  __nv_bfloat16* out;        // [rows_q, ld_out]
+  int64_t ld_out;
+  int nseq, heads, kv_heads, hd;
+  int group, qpt;            // heads / kv_heads, queries per tile (BQ / group)
+  int max_pairs;             // query-tile pairs of the longest query range
+  int n_units;               // max_pairs * nseq * kv_heads
+  int use_tma;               // head_dim % 64 == 0: whole 128-byte column boxes, TMA tile loads
+  float scale_log2;          // softmax scale * log2(e)
+  unsigned long long* stats; // debug (RDX_ATTN_STATS_BUILD + RDX_ATTN_STATS=1): summed clocks per role
+};
+
+// Stats slots (summed over CTAs): see rdx_attention_debug_stats.
+enum { ST_MMA_TFULL, ST_MMA_PFULL, ST_MMA_QFULL, ST_MMA_OFREE, ST_MMA_TOTAL, ST_SM_SFULL, ST_SM_TOTAL,
+       ST_EPI_WAIT, ST_LD_FREE, ST_LD_TOTAL, ST_SM_RESCALE, ST_MMA_ISSUE, ST_EPI_TOTAL, ST_SM_EXP, ST_N };
+#ifndef RDX_ATTN_STATS_BUILD
+#define RDX_ATTN_STATS_BUILD 0  // 1: per-role clock counters (debug builds only)
+#endif
+#define RDX_STATS_ON (RDX_ATTN_STATS_BUILD && a.stats)
+#define RDX_TWAIT(bar, par, acc)       \
+  do {                                 \
+    if (RDX_STATS_ON) {                \
+      const long long _t0 = clock64(); \
+      mbar_wait(bar, par);             \
+      acc += clock64() - _t0;          \
+    } else {                           \
+      mbar_wait(bar, par);             \
+    }                                  \
+  } while (0)
+
+// 16-byte chunk c of a head row -> swizzled smem offset in a
+// [halves][rows][128 B] tile (half stride = rows * 128).
+__device__ __forceinline__ uint32_t sw_off(int row, int c, int rows) {
+  const int half = c >> 3, cc = c & 7;
+  return half * rows * 128 + row * 128 + ((cc ^ (row & 7)) << 4);
+}
+
 // Unit geometry (identical in every role).  Units are ordered pair-index
 // descending so the longest key ranges are scheduled first.
 struct Unit {
   int s, g, k0, L, q0, qlen, lcp, mb0;
-  int nkt[2];  // key tiles of query tile h (0 = tile absent)
-  int nkt_all;
+  int nkt0, nkt1;  // key tiles of query tile h (0 = tile absent)
 };
 
 __device__ __forceinline__ bool load_unit(const Args& a, int u, Unit& it) {
@@ -278,13 +284,10 @@ __device__ __forceinline__ bool load_unit(const Args& a, int u, Unit& it) {
   it.qlen = a.cu_q[it.s + 1] - it.q0;
   it.lcp = it.L - it.qlen;
   it.mb0 = 2 * pair;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int mb = it.mb0 + h;
-    it.nkt[h] = mb * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (mb + 1) * a.qpt) + BK - 1) / BK : 0;
-  }
-  it.nkt_all = max(it.nkt[0], it.nkt[1]);
-  return it.nkt[0] > 0;
+  const int mb1 = it.mb0 + 1;
+  it.nkt0 = it.mb0 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (it.mb0 + 1) * a.qpt) + BK - 1) / BK : 0;
+  it.nkt1 = mb1 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (mb1 + 1) * a.qpt) + BK - 1) / BK : 0;
+  return it.nkt0 > 0;
 }
 
 // Next valid unit of this CTA at or after u (returns n_units when done).
@@ -294,45 +297,52 @@ __device__ __forceinline__ int next_unit(const Args& a, int u, Unit& it) {
   return a.n_units;
 }
 
-template <int HDP, uint32_t EMU>
+template <int HDP, int NQB, int NSLOT, uint32_t EMU>
 __global__ void __launch_bounds__(kThreads, 1)
-attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q, Args a) {
-  using T = Tile<HDP>;
+attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
+                 const __grid_constant__ CUtensorMap map_g4, const __grid_constant__ CUtensorMap map_r16, Args a) {
+  using T = Tile<HDP, NQB, NSLOT>;
   constexpr int Q_BYTES = T::Q_BYTES, T_BYTES = T::T_BYTES, CH = T::CH;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                  // [2][Q_BYTES]
-  uint8_t* sT = smem + 2 * Q_BYTES;    // [NSLOT][T_BYTES]
+  extern __shared__ __align__(1024) uint8_t smem[];  // dynamic smem starts 1024-aligned (no static smem)
+  uint8_t* sQ = smem;                                // [2 h][NQB][Q_BYTES]
+  uint8_t* sT = smem + T::T_OFF;                     // [NSLOT][T_BYTES]
+  float* sL = reinterpret_cast<float*>(smem + T::L_OFF);  // [2 h][2][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::BAR_OFF);
-  uint64_t* q_full = bars + 0;                 // [2]
-  uint64_t* q_free = bars + 2;                 // [2]
-  uint64_t* t_full = bars + 4;                 // [NSLOT]
-  uint64_t* t_free = bars + 4 + NSLOT;         // [NSLOT]
-  uint64_t* s_full = bars + 4 + 2 * NSLOT;     // [2]
-  uint64_t* p_full = bars + 6 + 2 * NSLOT;     // [2]
-  uint64_t* o_full = bars + 8 + 2 * NSLOT;     // [2]
-  uint64_t* o_free = bars + 10 + 2 * NSLOT;    // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 12 + 2 * NSLOT);
-  int32_t* s_rows = reinterpret_cast<int32_t*>(smem + T::ROWS_OFF);  // [2][BK]
+  uint64_t* q_full = bars + 0;                   // [2][NQB]
+  uint64_t* q_free = bars + 2 * NQB;             // [2][NQB]
+  uint64_t* t_full = bars + 4 * NQB;             // [NSLOT]
+  uint64_t* t_free = t_full + NSLOT;             // [NSLOT]
+  uint64_t* s_full = t_free + NSLOT;             // [2]
+  uint64_t* p_full = s_full + 2;                 // [2]
+  uint64_t* o_full = p_full + 2;                 // [2]
+  uint64_t* o_free = o_full + 2;                 // [2]
+  uint64_t* l_full = o_free + 2;                 // [2 h][2 slots]: one barrier per sL slot, so the
+                                                 // softmax can never run two phases ahead of a waiter
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(l_full + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 128);
+    if (smem_u32(smem) & 1023) __trap();  // the swizzled tiles need a 1024-byte aligned base
+    for (int i = 0; i < 2 * NQB; ++i) {
+      mbar_init(&q_full[i], 32);
       mbar_init(&q_free[i], 1);
+    }
+    for (int i = 0; i < NSLOT; ++i) {
+      mbar_init(&t_full[i], 32);
+      mbar_init(&t_free[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
       mbar_init(&o_full[i], 1);
       mbar_init(&o_free[i], 128);
-    }
-    for (int i = 0; i < NSLOT; ++i) {
-      mbar_init(&t_full[i], 128);
-      mbar_init(&t_free[i], 1);
+      mbar_init(&l_full[2 * i], 128);
+      mbar_init(&l_full[2 * i + 1], 128);
     }
     fence_mbar_init();
   }
-  if (warp == 12) {
+  if (warp == kMmaWarp) {
     tmem_alloc(tmem_holder, TMEM_COLS);
     tmem_relinquish();
   }
@@ -343,108 +353,132 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 
   if (warp >= 8) {
     setmaxnreg_dec<80>();
-    if (warp < 12) {
-      // ---------------------------------------------------------------- loaders
-      const int t = threadIdx.x - 256;  // 0..127
+    if (warp == kLoaderWarp) {
+      // ---------------------------------------------------------------- loader (one warp)
       long long st_free = 0;
       const long long st_t0 = clock64();
-      int q_cnt[2] = {0, 0};
+      int q_cnt0 = 0, q_cnt1 = 0;
       uint32_t seq = 0;  // K/V ring sequence number (K and V tiles alternate)
       Unit it;
       for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
         // Q tiles of this unit
-#pragma unroll 1
+#pragma unroll
         for (int h = 0; h < 2; ++h) {
-          if (!it.nkt[h]) continue;
-          if (q_cnt[h] > 0) RDX_TWAIT(&q_free[h], (q_cnt[h] - 1) & 1, st_free);
-          const uint32_t sq = smem_u32(sQ + h * Q_BYTES);
+          if (!(h ? it.nkt1 : it.nkt0)) continue;
+          int& q_cnt = h ? q_cnt1 : q_cnt0;
+          const int qb = q_cnt % NQB;
+          if (q_cnt >= NQB) RDX_TWAIT(&q_free[h * NQB + qb], ((q_cnt / NQB) - 1) & 1, st_free);
+          uint8_t* dstq = sQ + (h * NQB + qb) * Q_BYTES;
+          uint64_t* bar = &q_full[h * NQB + qb];
           const int mb = it.mb0 + h;
           if (a.use_tma) {
-            // one box per (group head, 64-column half): qpt query rows of head g*group+hh
-            if (t == 0) {
-              mbar_arrive_expect_tx(&q_full[h], Q_BYTES);
+            if (lane == 0) {
+              mbar_arrive_expect_tx(bar, Q_BYTES);
               for (int hh = 0; hh < a.group; ++hh)
+#pragma unroll
                 for (int half = 0; half < T::HALVES; ++half)
-                  tma_load_2d(&map_q, sQ + h * Q_BYTES + half * (BQ * 128) + hh * a.qpt * 128, &q_full[h],
+                  tma_load_2d(&map_q, dstq + half * (BQ * 128) + hh * a.qpt * 128, bar,
                               (it.g * a.group + hh) * a.hd + half * 64, it.q0 + mb * a.qpt);
             } else {
-              mbar_arrive(&q_full[h]);
+              mbar_arrive(bar);
             }
-            ++q_cnt[h];
-            continue;
+          } else {
+            const uint32_t sq = smem_u32(dstq);
+#pragma unroll 4
+            for (int k = 0; k < 4 * CH; ++k) {
+              const int idx = lane + k * 32;
+              const int r = idx / CH, c = idx % CH;
+              const int hh = r / a.qpt, qi = mb * a.qpt + (r - hh * a.qpt);
+              const bool ok = qi < it.qlen && c * 8 < a.hd;
+              const __nv_bfloat16* src = ok ? a.qkv + static_cast<int64_t>(it.q0 + qi) * a.ld +
+                                                  static_cast<int64_t>(it.g * a.group + hh) * a.hd + c * 8
+                                            : a.qkv;
+              cp_async16(sq + sw_off(r, c, BQ), src, ok ? 16u : 0u);
+            }
+            cp_async_arrive(bar);
           }
-#pragma unroll
-          for (int k = 0; k < CH; ++k) {
-            const int idx = t + k * 128;
-            const int r = idx / CH, c = idx % CH;
-            const int hh = r / a.qpt, qi = mb * a.qpt + (r - hh * a.qpt);
-            const bool ok = qi < it.qlen && c * 8 < a.hd;
-            const __nv_bfloat16* src = ok ? a.qkv + static_cast<int64_t>(it.q0 + qi) * a.ld +
-                                                static_cast<int64_t>(it.g * a.group + hh) * a.hd + c * 8
-                                          : a.qkv;
-            cp_async16(sq + sw_off(r, c, BQ), src, ok ? 16u : 0u);
-          }
-          cp_async_arrive(&q_full[h]);
-          ++q_cnt[h];
+          ++q_cnt;
         }
-        const int64_t kcol = static_cast<int64_t>(a.heads) * a.hd + static_cast<int64_t>(it.g) * a.hd;
-        const int64_t vcol = kcol + static_cast<int64_t>(a.kv_heads) * a.hd;
-        // Row of key j*BK + t, resolved once per tile by thread t (one coalesced
-        // scatter read, prefetched a tile ahead) and shared through smem.
-        auto key_row = [&](int j) {
-          const int key = j * BK + t;
-          return key >= it.L ? -1 : (a.scatter ? __ldg(a.scatter + it.k0 + key) : it.k0 + key);
+        const int32_t kcol = a.heads * a.hd + it.g * a.hd;
+        const int32_t vcol = kcol + a.kv_heads * a.hd;
+        const int nkt = max(it.nkt0, it.nkt1);
+        // rows of keys 4*lane .. 4*lane+3 of tile j (-1 past the sequence end)
+        auto key_rows = [&](int j, int (&r)[4]) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int key = j * BK + 4 * lane + i;
+            r[i] = key >= it.L ? -1 : (a.scatter ? __ldg(a.scatter + it.k0 + key) : it.k0 + key);
+          }
         };
-        int row_next = key_row(0);
+        int rn[4];
+        key_rows(0, rn);
 #pragma unroll 1
-        for (int j = 0; j < it.nkt_all; ++j) {
-          int32_t* rows = s_rows + (seq & 2 ? BK : 0);  // seq advances by 2 per tile: alternate buffers
-          rows[t] = row_next;
-          named_bar_sync(1, 128);
-          const int row0 = rows[0];
-          // rows strictly increase along a trie path, but check every key: a contiguous
-          // run of compact rows is one TMA box per 64-column half, otherwise gather.
-          const bool contiguous = named_bar_and(1, 128, row_next < 0 || row_next == row0 + t) && a.use_tma;
-          if (j + 1 < it.nkt_all) row_next = key_row(j + 1);
+        for (int j = 0; j < nkt; ++j) {
+          int r[4] = {rn[0], rn[1], rn[2], rn[3]};
+          if (j + 1 < nkt) key_rows(j + 1, rn);  // prefetch the next tile's rows
+          const int row0 = __shfl_sync(0xffffffffu, r[0], 0);
+          bool run = true;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) run = run && (r[i] < 0 || r[i] == row0 + 4 * lane + i);
+          const bool contiguous = __all_sync(0xffffffffu, run);
+          // 16-key groups (lanes 4g..4g+3) that are contiguous runs of compact rows
+          const int grow0 = __shfl_sync(0xffffffffu, r[0], lane & ~3);
+          bool grun = true;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) grun = grun && (r[i] < 0 || r[i] == grow0 + 4 * (lane & 3) + i);
+          const uint32_t gbits = __ballot_sync(0xffffffffu, grun);
+          const bool group_run = ((gbits >> (lane & ~3)) & 0xFu) == 0xFu && grow0 >= 0;
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv, ++seq) {
             const uint32_t slot = seq % NSLOT;
             if (seq >= NSLOT) RDX_TWAIT(&t_free[slot], ((seq / NSLOT) - 1) & 1, st_free);
-            const uint32_t st = smem_u32(sT + slot * T_BYTES);
-            const int64_t col = kv ? vcol : kcol;
-            if (contiguous) {
-              if (t == 0) {
-                mbar_arrive_expect_tx(&t_full[slot], T_BYTES);
+            uint8_t* dst = sT + slot * T_BYTES;
+            uint64_t* bar = &t_full[slot];
+            const int32_t col = kv ? vcol : kcol;
+            if (a.use_tma) {
+              if (lane == 0) mbar_arrive_expect_tx(bar, T_BYTES);
+              if (contiguous) {
+                if (lane == 0) {
+#pragma unroll
+                  for (int half = 0; half < T::HALVES; ++half)
+                    tma_load_2d(&map_kv, dst + half * (BK * 128), bar, col + half * 64, row0);
+                }
+              } else if (group_run) {
+                // one 16-row box per contiguous 16-key group, issued by the group's first lane
+                if ((lane & 3) == 0) {
+#pragma unroll
+                  for (int half = 0; half < T::HALVES; ++half)
+                    tma_load_2d(&map_r16, dst + half * (BK * 128) + 4 * lane * 128, bar, col + half * 64, grow0);
+                }
+              } else {
 #pragma unroll
                 for (int half = 0; half < T::HALVES; ++half)
-                  tma_load_2d(&map_kv, sT + slot * T_BYTES + half * (BK * 128), &t_full[slot],
-                              static_cast<int32_t>(col) + half * 64, row0);
-              } else {
-                mbar_arrive(&t_full[slot]);
+                  tma_gather4(&map_g4, smem_u32(dst + half * (BK * 128) + 4 * lane * 128), bar, col + half * 64,
+                              max(r[0], 0), max(r[1], 0), max(r[2], 0), max(r[3], 0));
               }
-              continue;
+              if (lane != 0) mbar_arrive(bar);
+            } else {
+              const uint32_t st = smem_u32(dst);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                  const bool ok = r[i] >= 0 && c * 8 < a.hd;
+                  cp_async16(st + sw_off(4 * lane + i, c, BK),
+                             a.qkv + static_cast<int64_t>(ok ? r[i] : 0) * a.ld + col + c * 8, ok ? 16u : 0u);
+                }
+              }
+              cp_async_arrive(bar);
             }
-#pragma unroll 8
-            for (int k = 0; k < CH; ++k) {
-              const int idx = t + k * 128;
-              const int r = idx / CH, c = idx % CH;
-              const int row = rows[r];
-              const bool ok = row >= 0 && c * 8 < a.hd;
-              cp_async16(st + sw_off(r, c, BK), a.qkv + static_cast<int64_t>(ok ? row : 0) * a.ld + col + c * 8,
-                         ok ? 16u : 0u);
-            }
-            cp_async_arrive(&t_full[slot]);
           }
         }
       }
-      if (RDX_STATS_ON && t == 0) {
+      if (RDX_STATS_ON && lane == 0) {
         atomicAdd(a.stats + ST_LD_FREE, static_cast<unsigned long long>(st_free));
         atomicAdd(a.stats + ST_LD_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
       }
-    } else if (warp == 12) {
-      // ---------------------------------------------------------------- MMA issuer
-      // The whole warp walks the schedule (warp-uniform values stay in uniform
-      // registers); one elected lane issues each tcgen05 op.
+    } else if (warp == kMmaWarp) {
+      // ---------------------------------------------------------------- MMA issuer (whole warp)
       long long st_t = 0, st_p = 0, st_q = 0, st_o = 0, st_iss = 0;
       const long long st_t0 = clock64();
       int s_cnt0 = 0, s_cnt1 = 0;  // S tiles issued per h (== P tiles consumed)
@@ -454,11 +488,12 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 
       auto issue_S = [&](int h, int nkt_h, int j, uint32_t tile) {
         int& q_cnt = h ? q_cnt1 : q_cnt0;
-        if (j == 0) RDX_TWAIT(&q_full[h], q_cnt & 1, st_q);
+        const int qb = q_cnt % NQB;
+        if (j == 0) RDX_TWAIT(&q_full[h * NQB + qb], (q_cnt / NQB) & 1, st_q);
         const uint32_t kslot = (2 * tile) % NSLOT;
-        fence_proxy_async_smem();
+        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 operand reads
         tc_fence_after();
-        const uint32_t qa = smem_u32(sQ + h * Q_BYTES), ka = smem_u32(sT + kslot * T_BYTES);
+        const uint32_t qa = smem_u32(sQ + (h * NQB + qb) * Q_BYTES), ka = smem_u32(sT + kslot * T_BYTES);
         const uint32_t sacc = tmem + h * 128;
         const uint64_t qd = sdesc(qa, 16, 1024), kd = sdesc(ka, 16, 1024);  // + (byte offset >> 4) per step
         const long long st_i0 = RDX_STATS_ON ? clock64() : 0;
@@ -470,7 +505,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         if (RDX_STATS_ON) st_iss += clock64() - st_i0;
         if (h) ++s_cnt1; else ++s_cnt0;
         if (j == nkt_h - 1) {
-          commit_elect(&q_free[h]);
+          commit_elect(&q_free[h * NQB + qb]);
           ++q_cnt;
         }
       };
@@ -479,7 +514,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         const int s_cnt = h ? s_cnt1 : s_cnt0;
         RDX_TWAIT(&p_full[h], (s_cnt - 1) & 1, st_p);  // P_h(j) published (S_h(j) was the last S of h)
         if (j == 0 && o_cnt > 0) RDX_TWAIT(&o_free[h], (o_cnt - 1) & 1, st_o);
-        fence_proxy_async_smem();  // cp.async (generic proxy) V writes -> tcgen05 operand reads
+        fence_proxy_async_smem();
         tc_fence_after();
         const uint32_t va = smem_u32(sT + ((2 * tile + 1) % NSLOT) * T_BYTES);
         const uint32_t o = tmem + O_COL + h * 128, pa = tmem + h * 128;
@@ -498,7 +533,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 
       Unit tmp;
       int ucur = next_unit(a, blockIdx.x, tmp);
-      int c0 = tmp.nkt[0], c1 = tmp.nkt[1], call = tmp.nkt_all;  // key tiles of the current unit
+      int c0 = tmp.nkt0, c1 = tmp.nkt1, call = max(tmp.nkt0, tmp.nkt1);  // key tiles of the current unit
       int jcur = 0;
       if (ucur < a.n_units) {
         wait_tile(2 * gt);
@@ -507,14 +542,13 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         commit_elect(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
       }
       while (ucur < a.n_units) {
-        // successor step
         int unxt = ucur, jnxt = jcur + 1, n0 = c0, n1 = c1, nall = call;
         if (jnxt >= call) {
           unxt = next_unit(a, ucur + gridDim.x, tmp);
           jnxt = 0;
-          n0 = tmp.nkt[0];
-          n1 = tmp.nkt[1];
-          nall = tmp.nkt_all;
+          n0 = tmp.nkt0;
+          n1 = tmp.nkt1;
+          nall = max(tmp.nkt0, tmp.nkt1);
         }
         const bool has_next = unxt < a.n_units;
         const uint32_t tnext = gt + 1;
@@ -545,21 +579,72 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         atomicAdd(a.stats + ST_MMA_ISSUE, static_cast<unsigned long long>(st_iss));
         atomicAdd(a.stats + ST_MMA_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
       }
+    } else if (warp >= 9 && warp <= 12) {
+      // ---------------------------------------------------------------- epilogue: O_h / l -> bf16 compact rows
+      const int q4 = warp & 3;            // TMEM lane quarter of this warp
+      const int t = q4 * 32 + lane;       // tile row == TMEM lane
+      const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
+      long long st_w = 0;
+      const long long st_t0 = clock64();
+      int cnt0 = 0, cnt1 = 0;
+      Unit it;
+      for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          if (!(h ? it.nkt1 : it.nkt0)) continue;
+          int& cnt = h ? cnt1 : cnt0;
+          const int mb = it.mb0 + h;
+          const int hh = t / a.qpt, qi = mb * a.qpt + (t - hh * a.qpt);
+          RDX_TWAIT(&l_full[2 * h + (cnt & 1)], (cnt >> 1) & 1, st_w);
+          RDX_TWAIT(&o_full[h], cnt & 1, st_w);
+          tc_fence_after();
+          const float l = sL[(h * 2 + (cnt & 1)) * BQ + t];
+          const float inv = l > 0.f ? 1.f / l : 0.f;
+          const bool valid = qi < it.qlen;
+          __nv_bfloat16* orow = a.out + static_cast<int64_t>(it.q0 + (valid ? qi : 0)) * a.ld_out +
+                                static_cast<int64_t>(it.g * a.group + hh) * a.hd;
+          const uint32_t o_addr = lane_base + O_COL + h * 128;
+#pragma unroll
+          for (int c = 0; c < HDP; c += 32) {
+            if (c < a.hd) {
+              float ov[32];
+              tmem_ld32p(o_addr + c, ov);
+              tmem_wait_ld();
+              if (valid) {
+#pragma unroll
+                for (int e = 0; e < 32; e += 8)
+                  if (c + e < a.hd)
+                    st_global_v4(orow + c + e, pack_bf16x2(ov[e] * inv, ov[e + 1] * inv),
+                                 pack_bf16x2(ov[e + 2] * inv, ov[e + 3] * inv),
+                                 pack_bf16x2(ov[e + 4] * inv, ov[e + 5] * inv),
+                                 pack_bf16x2(ov[e + 6] * inv, ov[e + 7] * inv));
+              }
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&o_free[h]);
+          ++cnt;
+        }
+      }
+      if (RDX_STATS_ON && t == 0) {
+        atomicAdd(a.stats + ST_EPI_WAIT, static_cast<unsigned long long>(st_w));
+        atomicAdd(a.stats + ST_EPI_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
+      }
     }
   } else {
-    // ---------------------------------------------------------------- softmax + epilogue (tile h)
+    // ---------------------------------------------------------------- softmax (query tile h, row t)
     setmaxnreg_inc<176>();
     const int h = warp >> 2;
     const int t = threadIdx.x & 127;  // row of the tile == TMEM lane
     const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const uint32_t s_addr = lane_base + h * 128;
     const uint32_t o_addr = lane_base + O_COL + h * 128;
-    int s_cnt = 0, o_cnt = 0;
-    long long st_s = 0, st_epi = 0, st_resc = 0, st_ld = 0, st_max = 0, st_exp = 0, st_stw = 0;
+    int s_cnt = 0, u_cnt = 0;
+    long long st_s = 0, st_resc = 0, st_exp = 0;
     const long long st_t0 = clock64();
     Unit it;
     for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
-      const int nkt_h = h ? it.nkt[1] : it.nkt[0];
+      const int nkt_h = h ? it.nkt1 : it.nkt0;
       if (!nkt_h) continue;
       const int mb = it.mb0 + h;
       const int hh = t / a.qpt, qi = mb * a.qpt + (t - hh * a.qpt);
@@ -569,13 +654,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 #pragma unroll 1
       for (int j = 0; j < nkt_h; ++j, ++s_cnt) {
         RDX_TWAIT(&s_full[h], s_cnt & 1, st_s);
-        const long long st_a = RDX_STATS_ON ? clock64() : 0;
         tc_fence_after();
         float sv[BK];
 #pragma unroll
         for (int c = 0; c < BK; c += 32) tmem_ld32p(s_addr + c, sv + c);
         tmem_wait_ld();
-        if (RDX_STATS_ON) st_ld += clock64() - st_a;
         const int kbase = j * BK;
         if (kbase + BK - 1 > pos_min) {  // warp-uniform: some key of this warp's rows is masked
           const int nvis = pos - kbase + 1;  // visible keys of this row in the tile
@@ -610,7 +693,6 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           m_run = m_new;
         }
         const long long st_b = RDX_STATS_ON ? clock64() : 0;
-        if (RDX_STATS_ON) st_max += st_b - st_a;
         const uint64_t scale2 = f2pack(a.scale_log2, a.scale_log2), negm2 = f2pack(-m_run, -m_run);
         uint64_t ls[4] = {0, 0, 0, 0};  // pairs of fp32 partial row sums (+0.0f bits)
 #pragma unroll
@@ -635,65 +717,31 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           tmem_st16u(s_addr + c / 2, pw);  // P over the first 64 columns of S_h
         }
         {
-          float s0, s1, s2, s3;
+          float s0, s1;
           f2unpack(fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3])), s0, s1);
-          (void)s2;
-          (void)s3;
           l_run += s0 + s1;
         }
-        const long long st_c = RDX_STATS_ON ? clock64() : 0;
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[h]);
-        if (RDX_STATS_ON) {
-          st_exp += st_c - st_b;
-          st_stw += clock64() - st_c;
-        }
+        if (RDX_STATS_ON) st_exp += clock64() - st_b;
       }
-      // epilogue: O_h / l -> bf16 -> compact rows
-      const long long st_e0 = RDX_STATS_ON ? clock64() : 0;
-      mbar_wait(&o_full[h], o_cnt & 1);
-      tc_fence_after();
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      const bool valid = qi < it.qlen;
-      __nv_bfloat16* orow = a.out + static_cast<int64_t>(it.q0 + (valid ? qi : 0)) * a.ld_out +
-                            static_cast<int64_t>(it.g * a.group + hh) * a.hd;
-#pragma unroll
-      for (int c = 0; c < HDP; c += 32) {
-        if (c < a.hd) {
-          float ov[32];
-          tmem_ld32p(o_addr + c, ov);
-          tmem_wait_ld();
-          if (valid) {
-#pragma unroll
-            for (int e = 0; e < 32; e += 8)
-              if (c + e < a.hd)
-                st_global_v4(orow + c + e, pack_bf16x2(ov[e] * inv, ov[e + 1] * inv),
-                             pack_bf16x2(ov[e + 2] * inv, ov[e + 3] * inv),
-                             pack_bf16x2(ov[e + 4] * inv, ov[e + 5] * inv),
-                             pack_bf16x2(ov[e + 6] * inv, ov[e + 7] * inv));
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&o_free[h]);
-      ++o_cnt;
-      if (RDX_STATS_ON) st_epi += clock64() - st_e0;
+      // hand the row sum to the epilogue warps (slot u_cnt & 1: the epilogue of
+      // unit u_cnt - 2 finished before PV_h(u_cnt - 1) could start)
+      sL[(h * 2 + (u_cnt & 1)) * BQ + t] = l_run;
+      mbar_arrive(&l_full[2 * h + (u_cnt & 1)]);
+      ++u_cnt;
     }
     if (RDX_STATS_ON && t == 0) {
       atomicAdd(a.stats + ST_SM_SFULL, static_cast<unsigned long long>(st_s));
-      atomicAdd(a.stats + ST_SM_EPI, static_cast<unsigned long long>(st_epi));
       atomicAdd(a.stats + ST_SM_RESCALE, static_cast<unsigned long long>(st_resc));
-      atomicAdd(a.stats + ST_SM_LD, static_cast<unsigned long long>(st_ld));
-      atomicAdd(a.stats + ST_SM_MAX, static_cast<unsigned long long>(st_max));
       atomicAdd(a.stats + ST_SM_EXP, static_cast<unsigned long long>(st_exp));
-      atomicAdd(a.stats + ST_SM_STW, static_cast<unsigned long long>(st_stw));
       atomicAdd(a.stats + ST_SM_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 12) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
@@ -701,17 +749,20 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 
 unsigned long long* g_stats = nullptr;  // debug counters (RDX_ATTN_STATS=1)
 
-template <int HDP, uint32_t EMU>
+template <int HDP, int NQB, int NSLOT, uint32_t EMU>
 int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
+  using T = Tile<HDP, NQB, NSLOT>;
+  auto kern = attention_kernel<HDP, NQB, NSLOT, EMU>;
   static bool attr_set = false;
   if (!attr_set) {
-    RDX_CUDA_TRY(cudaFuncSetAttribute(attention_kernel<HDP, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Tile<HDP>::SMEM));
+    RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
     attr_set = true;
   }
-  CUtensorMap map_kv, map_q;
+  CUtensorMap map_kv, map_q, map_g4, map_r16;
+  std::memset(&map_r16, 0, sizeof(map_r16));
   std::memset(&map_kv, 0, sizeof(map_kv));
   std::memset(&map_q, 0, sizeof(map_q));
+  std::memset(&map_g4, 0, sizeof(map_g4));
   if (a.use_tma) {
     int e = gemm::make_map(&map_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, BK,
                            CU_TENSOR_MAP_SWIZZLE_128B);
@@ -719,9 +770,15 @@ int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
     e = gemm::make_map(&map_q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, a.qpt,
                        CU_TENSOR_MAP_SWIZZLE_128B);
     if (e) return e;
+    e = gemm::make_map(&map_g4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, 1,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+    if (e) return e;
+    e = gemm::make_map(&map_r16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, 16,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+    if (e) return e;
   }
   const int ctas = a.n_units < num_sms() ? a.n_units : num_sms();
-  attention_kernel<HDP, EMU><<<static_cast<unsigned>(ctas), kThreads, Tile<HDP>::SMEM, st>>>(map_kv, map_q, a);
+  kern<<<static_cast<unsigned>(ctas), kThreads, T::SMEM, st>>>(map_kv, map_q, map_g4, map_r16, a);
   RDX_LAUNCH_CHECK();
   return RDX_OK;
 }
@@ -730,9 +787,9 @@ int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
 }  // namespace rdx
 
 extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const int32_t* scatter,
-                             const int32_t* cu,
-                             const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len, int32_t heads, int32_t kv_heads,
-                             int32_t head_dim, float softmax_scale, void* out_bf16, int64_t ld_out, void* stream) {
+                             const int32_t* cu, const int32_t* cu_q, int64_t n_seqs, int32_t max_q_len,
+                             int32_t max_k_len, int32_t heads, int32_t kv_heads, int32_t head_dim,
+                             float softmax_scale, void* out_bf16, int64_t ld_out, void* stream) {
   using namespace rdx;
   using namespace rdx::attn;
   if (head_dim <= 0 || head_dim > 128 || head_dim % 8) return RDX_ERR_UNSUPPORTED;
@@ -760,8 +817,8 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
   if (units >= (int64_t(1) << 31)) return RDX_ERR_CAPACITY_EXCEEDED;
   a.n_units = static_cast<int>(units);
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  a.emu_mask = kEmulated;
-  if (const char* e = std::getenv("RDX_ATTN_EMU")) a.emu_mask = static_cast<uint32_t>(std::strtoul(e, nullptr, 16));
+  a.use_tma = (head_dim % 64 == 0) && (reinterpret_cast<uintptr_t>(qkv_bf16) % 16 == 0) && qkv_rows > 0 &&
+              qkv_rows < (int64_t(1) << 31) && ld_qkv < (int64_t(1) << 31);
   a.stats = nullptr;
   if (const char* e = std::getenv("RDX_ATTN_STATS")) {
     if (e[0] == '1') {
@@ -772,23 +829,16 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
       a.stats = g_stats;
     }
   }
-  a.use_tma = (head_dim % 64 == 0) && (reinterpret_cast<uintptr_t>(qkv_bf16) % 16 == 0) && qkv_rows > 0 &&
-              qkv_rows < (int64_t(1) << 31);
-  if (head_dim <= 64) return launch<64, kEmulated>(a, qkv_rows, as_stream(stream));
-#if RDX_ATTN_STATS_BUILD
-  switch (a.emu_mask) {  // debug builds: exp2 split experiments (RDX_ATTN_EMU=hex)
-    case 0x00: return launch<128, 0x00>(a, qkv_rows, as_stream(stream));
-    case 0xAA: return launch<128, 0xAA>(a, qkv_rows, as_stream(stream));
-    case 0xEE: return launch<128, 0xEE>(a, qkv_rows, as_stream(stream));
-    case 0xFF: return launch<128, 0xFF>(a, qkv_rows, as_stream(stream));
-    default: break;
-  }
-#endif
-  return launch<128, kEmulated>(a, qkv_rows, as_stream(stream));
+  // short units (few key tiles): double-buffer Q; long units: deeper K/V ring
+  const bool short_units = max_k_len > 0 && (max_k_len + BK - 1) / BK <= kShortUnitTiles;
+  cudaStream_t s = as_stream(stream);
+  if (head_dim <= 64)
+    return short_units ? launch<64, 2, 4, kEmulated>(a, qkv_rows, s) : launch<64, 1, 6, kEmulated>(a, qkv_rows, s);
+  return short_units ? launch<128, 2, 3, kEmulated>(a, qkv_rows, s) : launch<128, 1, 4, kEmulated>(a, qkv_rows, s);
 }
 
 // Debug: copy (and reset) the summed per-role clock counters of every launch
-// since the last call; n >= 11 slots (order: enum ST_* above).
+// since the last call; n >= ST_N slots (order: enum ST_* above).
 extern "C" int rdx_attention_debug_stats(unsigned long long* host, int n) {
   using namespace rdx::attn;
   if (!g_stats) return RDX_ERR_INVALID_ARGUMENT;

@@ -386,14 +386,15 @@ class RadixQwen3:
     def _gather(self, name, x, idx, stream_obj):
         return self._op(name, lambda: gather_rows_device(x, idx, stream=stream_obj))
 
-    def _attn(self, qkv, scatter, cu32, cu_q32, b, max_q, out, flops, stream):
+    def _attn(self, qkv, scatter, cu32, cu_q32, b, max_q, max_k, out, flops, stream):
         """rdx_attention: Q compact rows, K/V read through ``scatter`` (None = plain layout)."""
         cfg = self.config
         lib = _native.lib()
 
         def launch():
-            code = lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), qkv.shape[0], None if scatter is None else scatter.data_ptr(),
-                                     cu32.data_ptr(), cu_q32.data_ptr(), b, max(int(max_q), 1), cfg.num_heads,
+            code = lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), qkv.shape[0],
+                                     None if scatter is None else scatter.data_ptr(), cu32.data_ptr(),
+                                     cu_q32.data_ptr(), b, max(int(max_q), 1), int(max_k), cfg.num_heads,
                                      cfg.num_kv_heads, cfg.head_dim, 1.0 / math.sqrt(cfg.head_dim),
                                      out.data_ptr(), out.stride(0), stream)
             _native.check(code, "rdx_attention")
@@ -574,13 +575,13 @@ class RadixQwen3:
             self._gemm("qkv", hn, T[pre + "w_qkv"], _native.EPI_QKV, qkv, m=m, stream=st, qkv=True, rope=rope,
                        layer=pre)
             if mode == "plain":
-                a = self._attn(qkv, None, cu32, cu32, b, max_k, attn_out, att_flops, st)
+                a = self._attn(qkv, None, cu32, cu32, b, max_k, max_k, attn_out, att_flops, st)
             elif mode == "suffix":
-                a = self._attn(qkv, scatter, cu32, cu_q32, b, max_q, attn_out, att_flops, st)
+                a = self._attn(qkv, scatter, cu32, cu_q32, b, max_q, max_k, attn_out, att_flops, st)
             else:
                 qkv_full = self._gather("scatter_qkv", qkv, scatter, stream)
                 a_full = torch.empty(n, qd, dtype=bf, device=dev)
-                self._attn(qkv_full, None, cu32, cu32, b, max_k, a_full, att_flops, st)
+                self._attn(qkv_full, None, cu32, cu32, b, max_k, max_k, a_full, att_flops, st)
                 a = self._gather("gather_attn", a_full, gather, stream)
             a = a.reshape(m, qd)
             self._gemm("o_proj", a, T[pre + "wo"], _native.EPI_RESID_F32, h, m=m, stream=st)

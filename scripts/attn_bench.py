@@ -34,6 +34,7 @@ cuq32 = torch.tensor(cu_q, dtype=torch.int32, device="cuda")
 out = torch.empty(m, H * hd, dtype=torch.bfloat16, device="cuda")
 maxq = int(np.diff(cu_q).max())
 maxk = int(np.diff(cu).max())
+maxk_arg = 0 if os.environ.get("ATTN_LONG") == "1" else maxk  # 0: force the long-unit pipeline
 lib = _native.lib()
 lens = np.diff(cu).astype(np.float64)
 lcp = lens - np.diff(cu_q)
@@ -43,7 +44,7 @@ pairs_full = float(np.sum(lens * (lens + 1) / 2))
 
 def ours():
     lib.rdx_attention(qkv.data_ptr(), qkv.stride(0), qkv.shape[0], scatter.data_ptr(), cu32.data_ptr(), cuq32.data_ptr(),
-                      len(cu) - 1, maxq, H, KV, hd, 1 / math.sqrt(hd), out.data_ptr(), out.stride(0),
+                      len(cu) - 1, maxq, maxk_arg, H, KV, hd, 1 / math.sqrt(hd), out.data_ptr(), out.stride(0),
                       torch.cuda.current_stream().cuda_stream)
 
 
@@ -53,7 +54,7 @@ out_full = torch.empty(n, H * hd, dtype=torch.bfloat16, device="cuda")
 
 def ours_plain():
     lib.rdx_attention(qkv_full.data_ptr(), qkv_full.stride(0), qkv_full.shape[0], None, cu32.data_ptr(), cu32.data_ptr(), len(cu) - 1,
-                      maxk, H, KV, hd, 1 / math.sqrt(hd), out_full.data_ptr(), out_full.stride(0),
+                      maxk, maxk_arg, H, KV, hd, 1 / math.sqrt(hd), out_full.data_ptr(), out_full.stride(0),
                       torch.cuda.current_stream().cuda_stream)
 
 
@@ -101,7 +102,7 @@ if os.environ.get("RDX_ATTN_STATS") == "1":
     import ctypes
 
     names = ["mma_wait_kv", "mma_wait_p", "mma_wait_q", "mma_wait_ofree", "mma_total", "sm_wait_s", "sm_total",
-             "sm_epilogue", "ld_wait_free", "ld_total", "sm_rescales", "mma_issue", "sm_ld", "sm_ld+max", "sm_exp", "sm_stwait"]
+             "epi_wait", "ld_wait_free", "ld_total", "sm_rescales", "mma_issue", "epi_total", "sm_exp"]
     for label, fn in (("suffix", ours), ("plain", ours_plain)):
         buf = (ctypes.c_ulonglong * 16)()
         lib.rdx_attention_debug_stats(buf, 16)  # reset
@@ -109,7 +110,7 @@ if os.environ.get("RDX_ATTN_STATS") == "1":
         torch.cuda.synchronize()
         lib.rdx_attention_debug_stats(buf, 16)
         v = list(buf)
-        print(label, "per-role clocks (fraction of role total):",
-              {n: round(x / max(v[4] if n.startswith("mma") else v[6] if n.startswith("sm") else v[9], 1), 3)
-               for n, x in zip(names, v)}, "sm_rescales", v[10], "mma_issue", round(v[11] / max(v[4], 1), 3),
-              "softmax parts", [round(x / max(v[6], 1), 3) for x in v[12:16]], flush=True)
+        den = {"mma": v[4], "sm": v[6], "ld": v[9], "epi": v[12]}
+        print(label, "per-role clock fractions:",
+              {n: round(x / max(den[n.split("_")[0]], 1), 3) for n, x in zip(names, v) if n != "sm_rescales"},
+              "sm_rescales", v[10], flush=True)

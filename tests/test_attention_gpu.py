@@ -34,7 +34,8 @@ def _reference(qkv, scatter, cu, H, KV, hd):
     return out.reshape(n, H * hd)
 
 
-def _run(qkv, scatter, cu, cu_q, H, KV, hd, m_out):
+def _run(qkv, scatter, cu, cu_q, H, KV, hd, m_out, max_k=None):
+    """max_k=None: the true longest sequence (short-unit pipeline when <= 512 keys); 0: long-unit pipeline."""
     import torch
 
     from paper_2601_15013_b200 import _native
@@ -43,9 +44,10 @@ def _run(qkv, scatter, cu, cu_q, H, KV, hd, m_out):
     cuq32 = torch.tensor(np.asarray(cu_q), dtype=torch.int32, device="cuda")
     out = torch.full((m_out, H * hd), float("nan"), dtype=torch.bfloat16, device="cuda")
     max_q = int(np.diff(np.asarray(cu_q)).max())
+    max_k = int(np.diff(np.asarray(cu)).max()) if max_k is None else max_k
     code = _native.lib().rdx_attention(qkv.data_ptr(), qkv.stride(0), qkv.shape[0],
                                        None if scatter is None else scatter.data_ptr(), cu32.data_ptr(),
-                                       cuq32.data_ptr(), len(cu) - 1, max_q, H, KV, hd, 1.0 / math.sqrt(hd),
+                                       cuq32.data_ptr(), len(cu) - 1, max_q, max_k, H, KV, hd, 1.0 / math.sqrt(hd),
                                        out.data_ptr(), out.stride(0), _native.stream_handle())
     _native.check(code, "rdx_attention")
     torch.cuda.synchronize()
@@ -68,8 +70,9 @@ def test_plain_layout(hd, H, KV):
     assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
 
 
+@pytest.mark.parametrize("pipeline", ["auto", "long"])
 @pytest.mark.parametrize("hd,H,KV", [(128, 16, 8), (128, 32, 8), (64, 4, 2), (16, 4, 2)])
-def test_suffix_queries_through_scatter(hd, H, KV):
+def test_suffix_queries_through_scatter(hd, H, KV, pipeline):
     """Compact Q rows + K/V gathered through the plan's scatter map == full-layout attention."""
     import torch
 
@@ -85,7 +88,7 @@ def test_suffix_queries_through_scatter(hd, H, KV):
     g = torch.Generator(device="cuda").manual_seed(2)
     qkv = torch.randn(m, (H + 2 * KV) * hd, device="cuda", generator=g).to(torch.bfloat16)
     scatter = torch.from_numpy(np.array(plan.scatter_indices).view(np.int32)).cuda()
-    out = _run(qkv, scatter, b.cu_seqlens, cu_q, H, KV, hd, m)
+    out = _run(qkv, scatter, b.cu_seqlens, cu_q, H, KV, hd, m, max_k=None if pipeline == "auto" else 0)
     ref_full = _reference(qkv, scatter, b.cu_seqlens, H, KV, hd)
     gather = torch.from_numpy(np.array(plan.gather_indices).astype(np.int64)).cuda()
     ref = ref_full[gather]
