@@ -193,6 +193,9 @@ int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const 
  * epilogue; loader waits on free slots; totals); this copies n slots to host
  * and resets them. */
 int rdx_attention_debug_stats(unsigned long long* host, int n);
+/* Debug: event log of CTA 0 of the last launch in the same mode:
+ * [count, (clock, code) x min(count, 4096)] as 32-bit words. */
+int rdx_attention_debug_trace(uint32_t* host, int n_words);
 
 /* ---------------------------------------------------------------------
  * Reranker scores from last-token logits (fp32 [B, ld]):

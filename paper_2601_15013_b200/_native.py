@@ -16,6 +16,10 @@ import threading
 from .errors import NativeLibraryError, raise_for_status
 
 SO_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_rdx.so")
+# Developer experiments only: RDX_LIB_VARIANT=<tag> loads the in-tree _rdx_<tag>.so
+# built by build_library(variant=<tag>) (same sources, extra compile flags).
+if os.environ.get("RDX_LIB_VARIANT"):
+    SO_PATH = os.path.join(os.path.dirname(SO_PATH), f"_rdx_{os.environ['RDX_LIB_VARIANT']}.so")
 
 # Every symbol include/radix_b200.h declares (tests check the export list).
 EXPORTS = (
@@ -31,6 +35,7 @@ EXPORTS = (
     "rdx_gemm",
     "rdx_attention",
     "rdx_attention_debug_stats",
+    "rdx_attention_debug_trace",
     "rdx_rerank_scores",
     "rdx_num_sms",
 )
@@ -97,6 +102,7 @@ _SIGNATURES = {
     "rdx_attention": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i64,
                                       _vp]),
     "rdx_attention_debug_stats": (ctypes.c_int, [_vp, _i32]),
+    "rdx_attention_debug_trace": (ctypes.c_int, [_vp, _i32]),
     "rdx_num_sms": (ctypes.c_int, []),
 }
 

@@ -40,18 +40,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > out_t for p in deps)
 
 
-def build_library(force: bool = False, verbose: bool = False) -> str:
-    """Compile every csrc/*.cu for sm_100a into _rdx.so; returns its path."""
-    if not force and not _stale():
+def build_library(force: bool = False, verbose: bool = False, variant: str | None = None,
+                  extra_flags: list[str] | None = None) -> str:
+    """Compile every csrc/*.cu for sm_100a into _rdx.so (or _rdx_<variant>.so); returns its path."""
+    out = OUT if variant is None else os.path.join(HERE, f"_rdx_{variant}.so")
+    if variant is None and not force and not _stale():
         return OUT
-    tmp = OUT + ".tmp"
-    extra = os.environ.get("RDX_NVCC_EXTRA", "").split()  # e.g. -DRDX_ATTN_STATS_BUILD=1 (debug counters)
+    tmp = out + ".tmp"
+    extra = os.environ.get("RDX_NVCC_EXTRA", "").split() + list(extra_flags or [])  # e.g. -DRDX_ATTN_STATS_BUILD=1
     cmd = [nvcc_path(), *ARCH_FLAGS, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-o", tmp, *sources()]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -61,7 +61,10 @@ constexpr int kLoaderWarp = 8, kMmaWarp = 13;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t O_COL = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when the max grows by > 2^8
-constexpr uint32_t kEmulated = 0xA4u;      // pairs (mod 8) whose exp2 runs on the FMA pipe: 3 of 8
+#ifndef RDX_ATTN_EMU
+#define RDX_ATTN_EMU 0x00u
+#endif
+constexpr uint32_t kEmulated = RDX_ATTN_EMU;  // pairs (mod 8) whose exp2 runs on the FMA pipe (bitmask)
 constexpr int kShortUnitTiles = 4;         // <= this many key tiles per unit: double-buffered Q
 
 // NQB = Q buffers per query tile, NSLOT = K/V ring slots (K and V tiles alternate).
@@ -238,6 +241,7 @@ struct Args {
   int use_tma;               // head_dim % 64 == 0: whole 128-byte column boxes, TMA tile loads
   float scale_log2;          // softmax scale * log2(e)
   unsigned long long* stats; // debug (RDX_ATTN_STATS_BUILD + RDX_ATTN_STATS=1): summed clocks per role
+  uint32_t* trace;           // debug: CTA 0 event log [count, (clock, code) x 4096]
 };
 
 // Stats slots (summed over CTAs): see rdx_attention_debug_stats.
@@ -256,6 +260,33 @@ enum { ST_MMA_TFULL, ST_MMA_PFULL, ST_MMA_QFULL, ST_MMA_OFREE, ST_MMA_TOTAL, ST_
     } else {                           \
       mbar_wait(bar, par);             \
     }                                  \
+  } while (0)
+
+// Debug event log of CTA 0 (stats builds): code = role << 12 | event << 8 | payload.
+// Events go to a per-thread local buffer (no atomics on the timed path) and
+// are flushed to a.trace when the role finishes.
+struct EvLog {
+  uint32_t tm[96], code[96];
+  int n;
+};
+#define RDX_EV(role, ev, payload)                                                    \
+  do {                                                                               \
+    if (RDX_STATS_ON && a.trace && blockIdx.x == 0 && evl.n < 96) {                  \
+      evl.tm[evl.n] = static_cast<uint32_t>(clock64());                              \
+      evl.code[evl.n] = ((role) << 12) | ((ev) << 8) | ((payload) & 0xFF);           \
+      ++evl.n;                                                                       \
+    }                                                                                \
+  } while (0)
+#define RDX_EV_FLUSH()                                                               \
+  do {                                                                               \
+    if (RDX_STATS_ON && a.trace && blockIdx.x == 0 && evl.n > 0) {                   \
+      const uint32_t _b = atomicAdd(a.trace, static_cast<uint32_t>(evl.n));          \
+      for (int _i = 0; _i < evl.n; ++_i)                                             \
+        if (_b + _i < 4096) {                                                        \
+          a.trace[2 + 2 * (_b + _i)] = evl.tm[_i];                                   \
+          a.trace[3 + 2 * (_b + _i)] = evl.code[_i];                                 \
+        }                                                                            \
+    }                                                                                \
   } while (0)
 
 // 16-byte chunk c of a head row -> swizzled smem offset in a
@@ -278,10 +309,10 @@ __device__ __forceinline__ bool load_unit(const Args& a, int u, Unit& it) {
   const int rem = u - (u / per) * per;
   it.s = rem / a.kv_heads;
   it.g = rem - it.s * a.kv_heads;
-  it.k0 = a.cu[it.s];
-  it.L = a.cu[it.s + 1] - it.k0;
-  it.q0 = a.cu_q[it.s];
-  it.qlen = a.cu_q[it.s + 1] - it.q0;
+  it.k0 = __ldg(a.cu + it.s);
+  it.L = __ldg(a.cu + it.s + 1) - it.k0;
+  it.q0 = __ldg(a.cu_q + it.s);
+  it.qlen = __ldg(a.cu_q + it.s + 1) - it.q0;
   it.lcp = it.L - it.qlen;
   it.mb0 = 2 * pair;
   const int mb1 = it.mb0 + 1;
@@ -357,6 +388,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       // ---------------------------------------------------------------- loader (one warp)
       long long st_free = 0;
       const long long st_t0 = clock64();
+      EvLog evl;
+      evl.n = 0;
       int q_cnt0 = 0, q_cnt1 = 0;
       uint32_t seq = 0;  // K/V ring sequence number (K and V tiles alternate)
       Unit it;
@@ -457,6 +490,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
                               max(r[0], 0), max(r[1], 0), max(r[2], 0), max(r[3], 0));
               }
               if (lane != 0) mbar_arrive(bar);
+              if (lane == 0) RDX_EV(0, 1 + kv, (j & 15) | (contiguous ? 0x80 : (group_run ? 0x40 : 0)));
             } else {
               const uint32_t st = smem_u32(dst);
 #pragma unroll
@@ -473,6 +507,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           }
         }
       }
+      if (lane == 0) RDX_EV_FLUSH();
       if (RDX_STATS_ON && lane == 0) {
         atomicAdd(a.stats + ST_LD_FREE, static_cast<unsigned long long>(st_free));
         atomicAdd(a.stats + ST_LD_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
@@ -481,6 +516,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       // ---------------------------------------------------------------- MMA issuer (whole warp)
       long long st_t = 0, st_p = 0, st_q = 0, st_o = 0, st_iss = 0;
       const long long st_t0 = clock64();
+      EvLog evl;
+      evl.n = 0;
       int s_cnt0 = 0, s_cnt1 = 0;  // S tiles issued per h (== P tiles consumed)
       int o_cnt0 = 0, o_cnt1 = 0;  // units finished per h
       int q_cnt0 = 0, q_cnt1 = 0;  // Q tiles consumed per h
@@ -491,7 +528,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         const int qb = q_cnt % NQB;
         if (j == 0) RDX_TWAIT(&q_full[h * NQB + qb], (q_cnt / NQB) & 1, st_q);
         const uint32_t kslot = (2 * tile) % NSLOT;
-        fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 operand reads
+        if (!a.use_tma) fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tcgen05 operand reads
         tc_fence_after();
         const uint32_t qa = smem_u32(sQ + (h * NQB + qb) * Q_BYTES), ka = smem_u32(sT + kslot * T_BYTES);
         const uint32_t sacc = tmem + h * 128;
@@ -502,6 +539,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           umma_ss_elect(sacc, qd + (((kk >> 2) * (BQ * 128) + (kk & 3) * 32) >> 4),
                         kd + (((kk >> 2) * (BK * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
         commit_elect(&s_full[h]);
+        if (lane == 0) RDX_EV(1, 1, h * 16 + j);  // MMA: S_h(j) issued
         if (RDX_STATS_ON) st_iss += clock64() - st_i0;
         if (h) ++s_cnt1; else ++s_cnt0;
         if (j == nkt_h - 1) {
@@ -513,8 +551,9 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         int& o_cnt = h ? o_cnt1 : o_cnt0;
         const int s_cnt = h ? s_cnt1 : s_cnt0;
         RDX_TWAIT(&p_full[h], (s_cnt - 1) & 1, st_p);  // P_h(j) published (S_h(j) was the last S of h)
+        if (lane == 0) RDX_EV(1, 2, h * 16 + j);  // MMA: P_h(j) seen
         if (j == 0 && o_cnt > 0) RDX_TWAIT(&o_free[h], (o_cnt - 1) & 1, st_o);
-        fence_proxy_async_smem();
+        if (!a.use_tma) fence_proxy_async_smem();
         tc_fence_after();
         const uint32_t va = smem_u32(sT + ((2 * tile + 1) % NSLOT) * T_BYTES);
         const uint32_t o = tmem + O_COL + h * 128, pa = tmem + h * 128;
@@ -571,6 +610,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         call = nall;
         ++gt;
       }
+      if (lane == 0) RDX_EV_FLUSH();
       if (RDX_STATS_ON && lane == 0) {
         atomicAdd(a.stats + ST_MMA_TFULL, static_cast<unsigned long long>(st_t));
         atomicAdd(a.stats + ST_MMA_PFULL, static_cast<unsigned long long>(st_p));
@@ -586,6 +626,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
       long long st_w = 0;
       const long long st_t0 = clock64();
+      EvLog evl;
+      evl.n = 0;
       int cnt0 = 0, cnt1 = 0;
       Unit it;
       for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
@@ -597,6 +639,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           const int hh = t / a.qpt, qi = mb * a.qpt + (t - hh * a.qpt);
           RDX_TWAIT(&l_full[2 * h + (cnt & 1)], (cnt >> 1) & 1, st_w);
           RDX_TWAIT(&o_full[h], cnt & 1, st_w);
+          if (t == 0) RDX_EV(3, 1, h);  // epilogue: O_h ready
           tc_fence_after();
           const float l = sL[(h * 2 + (cnt & 1)) * BQ + t];
           const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -623,9 +666,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           }
           tc_fence_before();
           mbar_arrive(&o_free[h]);
+          if (t == 0) RDX_EV(3, 2, h);  // epilogue: O_h stored
           ++cnt;
         }
       }
+      if (t == 0) RDX_EV_FLUSH();
       if (RDX_STATS_ON && t == 0) {
         atomicAdd(a.stats + ST_EPI_WAIT, static_cast<unsigned long long>(st_w));
         atomicAdd(a.stats + ST_EPI_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
@@ -642,23 +687,29 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
     int s_cnt = 0, u_cnt = 0;
     long long st_s = 0, st_resc = 0, st_exp = 0;
     const long long st_t0 = clock64();
+    EvLog evl;
+    evl.n = 0;
     Unit it;
     for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
       const int nkt_h = h ? it.nkt1 : it.nkt0;
       if (!nkt_h) continue;
       const int mb = it.mb0 + h;
       const int hh = t / a.qpt, qi = mb * a.qpt + (t - hh * a.qpt);
-      const int pos = it.lcp + qi;  // keys 0..pos visible
+      // keys 0..pos visible; rows past the query range (never stored) see key 0 only
+      const int pos = qi < it.qlen ? it.lcp + qi : 0;
       const int pos_min = __reduce_min_sync(0xffffffffu, pos);
+      const int pos_max = __reduce_max_sync(0xffffffffu, pos);
       float m_run = -INFINITY, l_run = 0.f;
 #pragma unroll 1
       for (int j = 0; j < nkt_h; ++j, ++s_cnt) {
         RDX_TWAIT(&s_full[h], s_cnt & 1, st_s);
+        if (t == 0) RDX_EV(2, 1, h * 16 + j);  // softmax: S_h(j) ready
         tc_fence_after();
         float sv[BK];
 #pragma unroll
         for (int c = 0; c < BK; c += 32) tmem_ld32p(s_addr + c, sv + c);
         tmem_wait_ld();
+        if (t == 0) RDX_EV(2, 3, static_cast<int>(sv[0] != 12345.f));  // softmax: S in registers
         const int kbase = j * BK;
         if (kbase + BK - 1 > pos_min) {  // warp-uniform: some key of this warp's rows is masked
           const int nvis = pos - kbase + 1;  // visible keys of this row in the tile
@@ -693,11 +744,19 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           m_run = m_new;
         }
         const long long st_b = RDX_STATS_ON ? clock64() : 0;
+        if (t == 0) RDX_EV(2, 4, h * 16 + j);  // softmax: max done
         const uint64_t scale2 = f2pack(a.scale_log2, a.scale_log2), negm2 = f2pack(-m_run, -m_run);
         uint64_t ls[4] = {0, 0, 0, 0};  // pairs of fp32 partial row sums (+0.0f bits)
+        const int vis_warp = pos_max - kbase + 1;  // columns >= vis_warp are masked for the whole warp
 #pragma unroll
         for (int c = 0; c < BK; c += 32) {
           uint32_t pw[16];
+          if (c >= vis_warp) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pw[e] = 0u;
+            tmem_st16u(s_addr + c / 2, pw);
+            continue;
+          }
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             const uint64_t x = ffma2(f2pack(sv[c + e], sv[c + e + 1]), scale2, negm2);
@@ -721,9 +780,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           f2unpack(fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3])), s0, s1);
           l_run += s0 + s1;
         }
+        if (t == 0) RDX_EV(2, 5, static_cast<int>(l_run != 12345.f));  // softmax: exp + P stores issued
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[h]);
+        if (t == 0) RDX_EV(2, 2, h * 16 + j);  // softmax: P_h(j) published
         if (RDX_STATS_ON) st_exp += clock64() - st_b;
       }
       // hand the row sum to the epilogue warps (slot u_cnt & 1: the epilogue of
@@ -732,6 +793,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       mbar_arrive(&l_full[2 * h + (u_cnt & 1)]);
       ++u_cnt;
     }
+    if (t == 0) RDX_EV_FLUSH();
     if (RDX_STATS_ON && t == 0) {
       atomicAdd(a.stats + ST_SM_SFULL, static_cast<unsigned long long>(st_s));
       atomicAdd(a.stats + ST_SM_RESCALE, static_cast<unsigned long long>(st_resc));
@@ -748,6 +810,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 }
 
 unsigned long long* g_stats = nullptr;  // debug counters (RDX_ATTN_STATS=1)
+uint32_t* g_trace = nullptr;            // debug event log of CTA 0 (RDX_ATTN_STATS=1)
 
 template <int HDP, int NQB, int NSLOT, uint32_t EMU>
 int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
@@ -820,6 +883,7 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
   a.use_tma = (head_dim % 64 == 0) && (reinterpret_cast<uintptr_t>(qkv_bf16) % 16 == 0) && qkv_rows > 0 &&
               qkv_rows < (int64_t(1) << 31) && ld_qkv < (int64_t(1) << 31);
   a.stats = nullptr;
+  a.trace = nullptr;
   if (const char* e = std::getenv("RDX_ATTN_STATS")) {
     if (e[0] == '1') {
       if (!g_stats) {
@@ -827,6 +891,9 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
         RDX_CUDA_TRY(cudaMemset(g_stats, 0, ST_N * sizeof(unsigned long long)));
       }
       a.stats = g_stats;
+      if (!g_trace) RDX_CUDA_TRY(cudaMalloc(&g_trace, (2 + 2 * 4096) * sizeof(uint32_t)));
+      RDX_CUDA_TRY(cudaMemsetAsync(g_trace, 0, 2 * sizeof(uint32_t), as_stream(stream)));
+      a.trace = g_trace;
     }
   }
   // short units (few key tiles): double-buffer Q; long units: deeper K/V ring
@@ -845,5 +912,15 @@ extern "C" int rdx_attention_debug_stats(unsigned long long* host, int n) {
   const int m = n < ST_N ? n : ST_N;
   RDX_CUDA_TRY(cudaMemcpy(host, g_stats, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   RDX_CUDA_TRY(cudaMemset(g_stats, 0, ST_N * sizeof(unsigned long long)));
+  return RDX_OK;
+}
+
+// Debug: copy the CTA-0 event log of the last launch (RDX_ATTN_STATS=1 builds
+// with RDX_ATTN_STATS_BUILD): [count, (clock, code) x min(count, 4096)].
+extern "C" int rdx_attention_debug_trace(uint32_t* host, int n_words) {
+  using namespace rdx::attn;
+  if (!g_trace || n_words < 2) return RDX_ERR_INVALID_ARGUMENT;
+  const int m = n_words < 2 + 2 * 4096 ? n_words : 2 + 2 * 4096;
+  RDX_CUDA_TRY(cudaMemcpy(host, g_trace, m * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   return RDX_OK;
 }

@@ -114,3 +114,21 @@ if os.environ.get("RDX_ATTN_STATS") == "1":
         print(label, "per-role clock fractions:",
               {n: round(x / max(den[n.split("_")[0]], 1), 3) for n, x in zip(names, v) if n != "sm_rescales"},
               "sm_rescales", v[10], flush=True)
+if os.environ.get("RDX_ATTN_TRACE") == "1":
+    import ctypes
+
+    ours()
+    torch.cuda.synchronize()
+    buf = (ctypes.c_uint32 * (2 + 2 * 4096))()
+    lib.rdx_attention_debug_trace(buf, len(buf))
+    n = min(buf[0], 4096)
+    ev = sorted((buf[2 + 2 * i], buf[3 + 2 * i]) for i in range(n))
+    t0 = ev[0][0] if ev else 0
+    roles = {0: "LOAD", 1: "MMA ", 2: "SOFT", 3: "EPI "}
+    names = {(0, 1): "K tile", (0, 2): "V tile", (1, 1): "issue S", (1, 2): "got P", (2, 1): "got S",
+             (2, 2): "pub P", (2, 3): "S in regs", (2, 4): "max done", (2, 5): "exp done", (3, 1): "O ready",
+             (3, 2): "O stored"}
+    for tt, code in ev[:int(os.environ.get("TRACE_N", "160"))]:
+        role, e, pl = code >> 12, (code >> 8) & 15, code & 255
+        print(f"{(tt - t0) & 0xffffffff:9d} {roles.get(role, role)} {names.get((role, e), e):9s} h={pl >> 4} j={pl & 15}"
+              + (f" [{'box' if pl & 0x80 else 'r16' if pl & 0x40 else 'g4'}]" if role == 0 else ""))
