@@ -17,6 +17,8 @@
  *   rdx_gather_rows       <- radix_compact.ops.gather_rows / scatter_rows
  *                            (pkg/src/radix_compact/ops.py:50-66) and the
  *                            bindings gather_rows / scatter_rows (…:72-89)
+ *   rdx_gather_rows_backward <- ops.gather_rows_backward / scatter_rows_backward
+ *                            (ops.py:69-107), deterministic ascending-j adds
  *   rdx_embed_rmsnorm     <- model.py:329,341 (token gather + embedding rows)
  *                            fused with the layer-0 rmsnorm (model.py:147-152,349)
  *   rdx_rmsnorm_rows      <- rmsnorm (model.py:147-152) at model.py:392,404
@@ -107,6 +109,22 @@ int rdx_gather_rows(const void* src, int64_t src_rows, int64_t ld_src_bytes,
                     const uint32_t* idx, int64_t n_idx, void* dst,
                     int64_t ld_dst_bytes, int64_t row_bytes, uint32_t* err_flag,
                     void* stream);
+
+/* ---------------------------------------------------------------------
+ * Adjoint of the row gather / scatter (ops.py:69-107, gather_rows_backward
+ * and scatter_rows_backward; used by loss_and_grads, model.py:456-500):
+ *   out = zeros(n_out, cols);  out[idx[j]] += grad[j]   for j = 0, 1, ...
+ * in ascending-j order per output row, i.e. bit-identical to the
+ * reference's np.add.at path.  dtype RDX_DTYPE_F32 or RDX_DTYPE_F64 (the
+ * reference's float dtypes).  Indices >= n_out set *err_flag (IndexOutOfRange)
+ * and are skipped.  scratch: rdx_gather_rows_backward_scratch_bytes(n_idx, n_out)
+ * bytes of device memory.
+ * --------------------------------------------------------------------- */
+enum { RDX_DTYPE_F32 = 0, RDX_DTYPE_F64 = 1 };
+size_t rdx_gather_rows_backward_scratch_bytes(int64_t n_idx, int64_t n_out);
+int rdx_gather_rows_backward(const void* grad, int64_t ld_grad_bytes, const uint32_t* idx, int64_t n_idx,
+                             int64_t n_out, void* out, int64_t ld_out_bytes, int64_t cols, int32_t dtype,
+                             uint32_t* err_flag, void* scratch, size_t scratch_bytes, void* stream);
 
 /* ---------------------------------------------------------------------
  * Compact embedding gather fused with RMSNorm:

@@ -29,6 +29,8 @@ EXPORTS = (
     "rdx_plan_scratch_bytes",
     "rdx_plan_build",
     "rdx_gather_rows",
+    "rdx_gather_rows_backward_scratch_bytes",
+    "rdx_gather_rows_backward",
     "rdx_embed_rmsnorm",
     "rdx_rmsnorm_rows",
     "rdx_rope_table",
@@ -41,6 +43,8 @@ EXPORTS = (
 )
 
 RDX_PLAN_ALLOW_EMPTY = 0x1
+RDX_DTYPE_F32 = 0
+RDX_DTYPE_F64 = 1
 
 EPI_STORE_BF16 = 0
 EPI_STORE_F32 = 1
@@ -91,6 +95,9 @@ _SIGNATURES = {
         [_vp, _vp, _vp, _i64, _i64, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp],
     ),
     "rdx_gather_rows": (ctypes.c_int, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _vp, _vp]),
+    "rdx_gather_rows_backward_scratch_bytes": (ctypes.c_size_t, [_i64, _i64]),
+    "rdx_gather_rows_backward": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _i64, _i64, _i32, _vp, _vp,
+                                                ctypes.c_size_t, _vp]),
     "rdx_embed_rmsnorm": (
         ctypes.c_int,
         [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _vp, _vp, _vp],

@@ -83,3 +83,72 @@ def gather_rows(x, gather_indices, num_threads: int | None = None):
 def scatter_rows(y, scatter_indices, num_threads: int | None = None):
     """out[i, :] = y[scatter_indices[i], :] (ops.py:64-66), on the GPU."""
     return gather_rows(y, scatter_indices, num_threads=num_threads)
+
+
+def gather_rows_backward_device(grad, idx, n: int, out=None, err=None, stream=None):
+    """Device adjoint of the row gather: out[n, cols] = 0; out[idx[j]] += grad[j] in
+    ascending j (ops.py:69-99).  grad fp32/fp64 [len(idx), cols], idx int32/u32."""
+    import torch
+
+    if grad.dim() != 2:
+        raise ShapeMismatch(f"expected a 2-D matrix, got shape {tuple(grad.shape)}")
+    if grad.dtype not in (torch.float32, torch.float64):
+        raise TypeError(f"gather_rows_backward: float32/float64 gradients only, got {grad.dtype}")
+    if idx.dim() != 1 or idx.shape[0] != grad.shape[0]:
+        raise ShapeMismatch(f"{idx.shape[0] if idx.dim() == 1 else tuple(idx.shape)} indices vs "
+                            f"{grad.shape[0]} gradient rows")
+    if grad.stride(1) != 1:
+        grad = grad.contiguous()
+    cols = int(grad.shape[1])
+    if out is None:
+        out = torch.empty((int(n), cols), dtype=grad.dtype, device=grad.device)
+    lib = _native.lib()
+    from .plan import _WORKSPACE
+
+    nbytes = int(lib.rdx_gather_rows_backward_scratch_bytes(int(idx.shape[0]), int(n)))
+    scratch = _WORKSPACE.get(grad.device, nbytes)
+    esz = grad.element_size()
+    dtype = _native.RDX_DTYPE_F32 if grad.dtype == torch.float32 else _native.RDX_DTYPE_F64
+    code = lib.rdx_gather_rows_backward(
+        grad.data_ptr(), grad.stride(0) * esz, idx.data_ptr(), int(idx.shape[0]), int(n), out.data_ptr(),
+        out.stride(0) * esz, cols, dtype, None if err is None else err.data_ptr(), scratch.data_ptr(),
+        scratch.numel(), _native.stream_handle(stream))
+    _native.check(code, "rdx_gather_rows_backward")
+    return out
+
+
+def gather_rows_backward(grad_out, gather_indices, n: int, num_threads: int | None = None):
+    """Adjoint of gather_rows (ops.py:69-99): zero-init scatter-add into n rows with
+    ascending-j accumulation (bit-identical to the reference's np.add.at path)."""
+    del num_threads
+    import torch
+
+    if isinstance(grad_out, torch.Tensor):
+        idx = gather_indices
+        if not isinstance(idx, torch.Tensor):
+            idx = torch.from_numpy(_check_host_indices(idx, n).astype(np.int32))
+        idx = idx.to(device=grad_out.device, dtype=torch.int32)
+        err = torch.zeros(1, dtype=torch.int32, device=grad_out.device)
+        out = gather_rows_backward_device(grad_out, idx, n, err=err)
+        if int(err.item()):
+            raise IndexOutOfRange(f"index outside [0, {n})")
+        return out
+    g = np.asarray(grad_out)
+    if g.ndim != 2:
+        raise ShapeMismatch(f"expected a 2-D matrix, got shape {g.shape}")
+    idx = _check_host_indices(gather_indices, n)
+    if idx.size != g.shape[0]:
+        raise ShapeMismatch(f"{idx.size} indices vs {g.shape[0]} gradient rows")
+    if g.dtype not in (np.float32, np.float64):
+        raise TypeError(f"gather_rows_backward: float32/float64 gradients only, got {g.dtype}")
+    if n == 0 or g.shape[1] == 0:
+        return np.zeros((n, g.shape[1]), dtype=g.dtype)
+    gd = torch.from_numpy(np.ascontiguousarray(g)).cuda()
+    idd = torch.from_numpy(idx.astype(np.int32)).cuda()
+    return gather_rows_backward_device(gd, idd, n).cpu().numpy()
+
+
+def scatter_rows_backward(grad_out, scatter_indices, n_compact: int, num_threads: int | None = None):
+    """Adjoint of scatter_rows (ops.py:102-107): duplicated originals summed into their
+    compact representative, ascending-i accumulation."""
+    return gather_rows_backward(grad_out, scatter_indices, n_compact, num_threads=num_threads)
