@@ -486,7 +486,8 @@ def run_ours(args):
     config, model_name, global_batch, label = build_config(args.config, world)
     shards = partition_by_subtree(global_batch, world)
     mine = shards[rank]
-    model = RadixQwen3(config, DeviceWeights.random(config, seed=0), use_graphs=not args.no_graphs)
+    model = RadixQwen3(config, DeviceWeights.random(config, seed=0), use_graphs=not args.no_graphs,
+                       fused_norm=True if args.fused_norm else None)
     db = DeviceBatch.from_batch(mine.batch)
     rr = RadixReranker(model, dedup=True)
     rr_base = RadixReranker(model, dedup=False)
@@ -593,6 +594,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--profile", action="store_true", help="radix steps only, for ncu")
     ap.add_argument("--no-graphs", action="store_true", help="eager launches instead of CUDA-graph replay")
+    ap.add_argument("--fused-norm", action="store_true", help="RMSNorm fused into the GEMMs (RDX_EPI_RESID_NORM A/B)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -138,6 +138,14 @@ int rdx_embed_rmsnorm(const uint32_t* tok, const uint32_t* gather, int64_t n_row
                       const float* norm_w, float eps, float* h_out, void* hn_bf16_out,
                       uint32_t* err_flag, void* stream);
 
+/* Compact embedding gather for the fused-norm layer stack (RDX_EPI_RESID_NORM
+ * / row_ss): h[j] = embed[t] (fp32), hb[j] = bf16 copy, ss[j, g] = sum of
+ * h[j, 64g:64g+64]^2 (d % 64 == 0).  The layer-0 ln1 is then applied by the
+ * QKV GEMM (row_ss + ln1 folded into its weight). */
+int rdx_embed_rows(const uint32_t* tok, const uint32_t* gather, int64_t n_rows, const void* embed_bf16,
+                   int64_t vocab, int64_t d, float* h_out, void* hb_out, float* ss_out, uint32_t* err_flag,
+                   void* stream);
+
 /* RMSNorm of selected fp32 rows: out[j] = bf16(x[rows[j]] / rms * w)
  * (rows == NULL selects row j). */
 int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t n_rows,
@@ -163,9 +171,15 @@ typedef enum rdx_epilogue {
   RDX_EPI_RESID_F32 = 2,  /* resid_f32[m, n] += acc                                  */
   RDX_EPI_SWIGLU = 3,     /* B rows interleaved per tile: [gate(BN/2) | up(BN/2)];
                              out_bf16[m, n/2] = bf16(silu(g) * u)                    */
-  RDX_EPI_QKV = 4         /* per-head RMSNorm of q/k heads (q_norm/k_norm weights)
+  RDX_EPI_QKV = 4,        /* per-head RMSNorm of q/k heads (q_norm/k_norm weights)
                              + rotate-half RoPE from rope_table, v passthrough,
                              bf16 store (model.py:356-366)                           */
+  RDX_EPI_RESID_NORM = 5  /* residual add + the next RMSNorm's statistics:
+                             h = out_f32[m, n] += acc; out_bf16[m, n] = bf16(h);
+                             ss_out[m, n/64] = sum of h^2 per 64 columns (n % 64 == 0).
+                             Replaces the residual add and the rmsnorm pass of
+                             model.py:387-392 / 397-404 (the weight half of the norm
+                             is folded into the next GEMM's B, see row_ss)          */
 } rdx_epilogue;
 
 typedef struct rdx_gemm_args {
@@ -183,6 +197,18 @@ typedef struct rdx_gemm_args {
   const float* rope_table; /* [M, head_dim/2, 2] (cos, sin) */
   int32_t head_dim, q_heads, kv_heads;
   float eps;
+  /* Optional RMSNorm of the A rows fused into any epilogue: when row_ss != NULL
+   * accumulator row m is scaled by rsqrt(sum_{t<ss_parts} row_ss[m*ss_parts+t]
+   * / norm_dim + norm_eps) first (A = bf16 of the unnormalised rows, B = W with
+   * the norm weight folded in: B[n, k] = W[n, k] * w[k]). */
+  const float* row_ss;
+  int32_t ss_parts;
+  int32_t norm_dim;
+  float norm_eps;
+  /* RDX_EPI_RESID_NORM outputs (out = fp32 residual, read-modify-write) */
+  void* out_bf16;
+  int64_t ldo_bf16;
+  float* ss_out;
 } rdx_gemm_args;
 
 int rdx_gemm(const rdx_gemm_args* args, void* stream);

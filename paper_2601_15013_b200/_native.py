@@ -32,6 +32,7 @@ EXPORTS = (
     "rdx_gather_rows_backward_scratch_bytes",
     "rdx_gather_rows_backward",
     "rdx_embed_rmsnorm",
+    "rdx_embed_rows",
     "rdx_rmsnorm_rows",
     "rdx_rope_table",
     "rdx_gemm",
@@ -51,6 +52,7 @@ EPI_STORE_F32 = 1
 EPI_RESID_F32 = 2
 EPI_SWIGLU = 3
 EPI_QKV = 4
+EPI_RESID_NORM = 5
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -82,6 +84,13 @@ class GemmArgs(ctypes.Structure):
         ("q_heads", _i32),
         ("kv_heads", _i32),
         ("eps", _f32),
+        ("row_ss", _vp),
+        ("ss_parts", _i32),
+        ("norm_dim", _i32),
+        ("norm_eps", _f32),
+        ("out_bf16", _vp),
+        ("ldo_bf16", _i64),
+        ("ss_out", _vp),
     ]
 
 
@@ -102,6 +111,7 @@ _SIGNATURES = {
         ctypes.c_int,
         [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _vp, _vp, _vp],
     ),
+    "rdx_embed_rows": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "rdx_rmsnorm_rows": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _i64, _vp]),
     "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmArgs), _vp]),

@@ -20,6 +20,7 @@
 // give bit-identical rows (the reference's _mm rule, model.py:124-144).
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -40,19 +41,43 @@ struct EpiParams {
   const float2* rope;
   int hd, q_dim, kv_dim;
   float eps;
+  // fused RMSNorm of the A rows: acc row m *= rsqrt(sum_t row_ss[m*ss_parts+t] / norm_dim + norm_eps)
+  const float* row_ss;
+  int ss_parts;
+  float inv_norm_dim, norm_eps;
+  // RDX_EPI_RESID_NORM: h (fp32, in/out), hb = bf16(h_new), ss_out = per-64-column partial sum of h_new^2
+  float* h;
+  int64_t ldh;
+  __nv_bfloat16* hb;
+  int64_t ldhb;
+  float* ss_out;
+  int ss_out_parts;
 };
 
-template <int BN, int CG>
+constexpr int kNormGroup = 64;  // columns per partial sum of squares (RDX_EPI_RESID_NORM)
+
+// rsqrt(mean of squares + eps) of row r from its partial sums (fixed order: deterministic).
+__device__ __forceinline__ float row_rstd(const EpiParams& ep, int64_t r) {
+  const float* p = ep.row_ss + r * ep.ss_parts;
+  float s = 0.f;
+  for (int t = 0; t < ep.ss_parts; ++t) s += __ldg(p + t);
+  return rsqrtf(s * ep.inv_norm_dim + ep.norm_eps);
+}
+
+template <int BN, int CG, int EPI>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_ROWS = BN / CG;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * 2 * kEpiBoxBytes;
+  // RESID_NORM warps stage two fp32 boxes (h in/out) and two bf16 boxes (hb out)
+  static constexpr int EPI_WARP_BYTES = EPI == RDX_EPI_RESID_NORM ? 2 * kEpiBoxBytes + 2 * 2048 : 2 * kEpiBoxBytes;
+  static constexpr int EPI_BYTES = kEpiWarps * EPI_WARP_BYTES;
   static constexpr int AUX_BYTES = 1024;
-  static constexpr int BUDGET = 227 * 1024 - 1024 - 256 - EPI_BYTES - AUX_BYTES;
+  static constexpr int BAR_BYTES = 512;
+  static constexpr int BUDGET = 227 * 1024 - 1024 - BAR_BYTES - EPI_BYTES - AUX_BYTES;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + AUX_BYTES + 256;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + AUX_BYTES + BAR_BYTES;
   static constexpr uint32_t IDESC = umma_idesc_bf16(BM * CG, BN);
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static_assert(STAGES >= 3, "pipeline too shallow");
@@ -69,7 +94,9 @@ struct EpiWarp {
   uint8_t* base;
   int cur;
   int lane;
-  int32_t row0;  // first global row of this warp's 32-row slab
+  int32_t row0;     // first global row of this warp's 32-row slab
+  uint64_t* lbar;   // RESID_NORM: two TMA-load barriers (one per fp32 box)
+  uint32_t lphase;  // their phase bits
 };
 
 template <int NB>
@@ -139,7 +166,7 @@ __device__ __forceinline__ void rope_pair32(float* x1, float* x2, const float* w
 template <int HD, int NB>
 __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t n0, int c_lo, int c_hi, int64_t N,
                                          const EpiParams& ep, const float* s_qn, const float* s_kn,
-                                         const float2* rope_row, const CUtensorMap* map) {
+                                         const float2* rope_row, const CUtensorMap* map, float rs) {
   if constexpr (HD >= 64) {
     constexpr int H = HD / 2;
 #pragma unroll 1
@@ -153,6 +180,8 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
           float v[32];
           tmem_ld32p(taddr + h0 + c, v);
           tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= rs;
           emit_bf16x32(e, v, map, static_cast<int32_t>(col0 + c));
         }
         continue;
@@ -165,9 +194,12 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
         tmem_ld32p(taddr + h0 + c, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) ss += v[j] * v[j];
+        for (int j = 0; j < 32; ++j) {
+          v[j] *= rs;
+          ss += v[j] * v[j];
+        }
       }
-      const float inv = rsqrtf(ss / static_cast<float>(HD) + ep.eps);
+      const float inv = rsqrtf(ss / static_cast<float>(HD) + ep.eps) * rs;  // x1/x2 below are unscaled
 #pragma unroll 1
       for (int c = 0; c < H; c += 32) {
         float x1[32], x2[32];
@@ -188,6 +220,8 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
       float x[32];
       tmem_ld32p(taddr + c0, x);
       tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] *= rs;
 #pragma unroll
       for (int h = 0; h < 32; h += HD) {
         const int64_t col0 = colc + h;
@@ -220,7 +254,8 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
 template <int BN, int EPI, int NB>
 __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, int ch, int64_t gm_lane, int64_t M,
                                               int64_t n_blk, int64_t N, const EpiParams& ep, const float* s_qn,
-                                              const float* s_kn, const CUtensorMap* map) {
+                                              const float* s_kn, const CUtensorMap* map, const CUtensorMap* map_hb,
+                                              float rs) {
   constexpr int HALF = BN / 2;
   const int64_t n0 = n_blk * BN;
   const int c_lo = ch * HALF;
@@ -239,8 +274,64 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
 #pragma unroll
     for (int c = 0; c < HALF; c += 32) tmem_ld32p(taddr + c_lo + c, v + c);
   }
+  const int64_t r_clamped = gm_lane < M ? gm_lane : (M > 0 ? M - 1 : 0);
   if constexpr (EPI != RDX_EPI_QKV) tmem_wait_ld();
-  if constexpr (EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
+  if constexpr (EPI == RDX_EPI_RESID_NORM) {
+    // h tile (32 rows x 32 fp32 columns per chunk) comes in by TMA into an fp32 box,
+    // each lane adds its accumulator row, writes h_new back into the box and
+    // bf16(h_new) into a bf16 box, and both go out by TMA store; the partial sum
+    // of h_new^2 per 64 columns goes to ss_out.  Loads run one chunk ahead.
+    constexpr int CHUNKS = HALF / 32;
+    auto fbox = [&](int i) { return e.base + (i & 1) * kEpiBoxBytes; };
+    auto bbox = [&](int i) { return e.base + 2 * kEpiBoxBytes + (i & 1) * 2048; };
+    auto load = [&](int i) {
+      if (e.lane == 0) {
+        bulk_wait_read<0>();  // the stores that last read these boxes are done with them
+        mbar_arrive_expect_tx(&e.lbar[i & 1], kEpiBoxBytes);
+        tma_load_2d(map, fbox(i), &e.lbar[i & 1], static_cast<int32_t>(n0 + c_lo + 32 * i), e.row0);
+      }
+    };
+    load(0);
+    float ssp = 0.f;
+#pragma unroll
+    for (int i = 0; i < CHUNKS; ++i) {
+      const int64_t col = n0 + c_lo + 32 * i;
+      if (i + 1 < CHUNKS && col + 32 < N) load(i + 1);
+      if (col >= N) break;
+      mbar_wait(&e.lbar[i & 1], (e.lphase >> (i & 1)) & 1);
+      e.lphase ^= 1u << (i & 1);
+      const uint32_t fb = smem_u32(fbox(i)) + e.lane * 128;
+      const uint32_t bb = smem_u32(bbox(i)) + e.lane * 64;
+      uint32_t w[16];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t addr = fb + ((j ^ (e.lane & 7)) << 4);
+        float4 hv = ld_shared_f4(addr);
+        hv.x += v[32 * i + 4 * j];
+        hv.y += v[32 * i + 4 * j + 1];
+        hv.z += v[32 * i + 4 * j + 2];
+        hv.w += v[32 * i + 4 * j + 3];
+        ssp += hv.x * hv.x + hv.y * hv.y + hv.z * hv.z + hv.w * hv.w;
+        st_shared_v4(addr, __float_as_uint(hv.x), __float_as_uint(hv.y), __float_as_uint(hv.z), __float_as_uint(hv.w));
+        w[2 * j] = pack_bf16x2(hv.x, hv.y);
+        w[2 * j + 1] = pack_bf16x2(hv.z, hv.w);
+      }
+      const int sw = (e.lane >> 1) & 3;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st_shared_v4(bb + ((j ^ sw) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (e.lane == 0) {
+        tma_store_2d(map, fbox(i), static_cast<int32_t>(col), e.row0);
+        tma_store_2d(map_hb, bbox(i), static_cast<int32_t>(col), e.row0);
+        bulk_commit();
+      }
+      if ((i & 1) == 1) {  // end of a 64-column group
+        if (gm_lane < M) ep.ss_out[gm_lane * ep.ss_out_parts + col / kNormGroup] = ssp;
+        ssp = 0.f;
+      }
+    }
+  } else if constexpr (EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
 #pragma unroll
     for (int c = 0; c < HALF; c += 32) {
       if (n0 + c_lo + c < N) {
@@ -257,20 +348,22 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
         float* g = v + q;
         const float* u = v + HALF / 2 + q;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) g[j] = __fdividef(g[j], 1.f + __expf(-g[j])) * u[j];
+        for (int j = 0; j < 32; ++j) {
+          const float gj = g[j] * rs;
+          g[j] = __fdividef(gj, 1.f + __expf(-gj)) * (u[j] * rs);
+        }
         emit_bf16x32(e, g, map, static_cast<int32_t>(ocol));
       }
     }
   } else if constexpr (EPI == RDX_EPI_QKV) {
     // chunked: TMEM loads interleaved with the norm / RoPE math and the stores
-    const int64_t r = gm_lane < M ? gm_lane : (M > 0 ? M - 1 : 0);
-    const float2* rope_row = ep.rope + r * (ep.hd >> 1);
+    const float2* rope_row = ep.rope + r_clamped * (ep.hd >> 1);
     const int c_hi = c_lo + HALF;
     switch (ep.hd) {
-      case 128: qkv_cols<128>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
-      case 64: qkv_cols<64>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
-      case 32: qkv_cols<32>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
-      default: qkv_cols<16>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map); break;
+      case 128: qkv_cols<128>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
+      case 64: qkv_cols<64>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
+      case 32: qkv_cols<32>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
+      default: qkv_cols<16>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
     }
   }
 }
@@ -279,8 +372,9 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
 template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-            const __grid_constant__ CUtensorMap tmC, int64_t M, int64_t N, int64_t K, EpiParams ep) {
-  using C = Cfg<BN, CG>;
+            const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int64_t M, int64_t N,
+            int64_t K, EpiParams ep) {
+  using C = Cfg<BN, CG, EPI>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -291,7 +385,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* eload = tempty + 2;  // [kEpiWarps][2] epilogue TMA-load barriers (RESID_NORM)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(eload + 2 * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -315,6 +410,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps * CG);
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&eload[i], 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -405,9 +501,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int ch = ew >> 2;  // column half of the tile
-    constexpr int NB = (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) ? 2 : 4;
+    constexpr int NB = (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32 || EPI == RDX_EPI_RESID_NORM) ? 2 : 4;
     EpiWarp<NB> e;
-    e.base = epi_smem + ew * kEpiWarpBytes;
+    e.base = epi_smem + ew * C::EPI_WARP_BYTES;
+    e.lbar = eload + 2 * ew;
+    e.lphase = 0;
     e.cur = 0;
     e.lane = lane;
     const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
@@ -416,11 +514,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
       const int64_t m_blk = tile % m_tiles;
       const int64_t n_blk = tile / m_tiles;
+      e.row0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM + q * 32);
+      // row scale of the fused RMSNorm: its loads overlap the wait for the accumulator
+      const int64_t gm = e.row0 + lane;
+      const float rs = ep.row_ss ? row_rstd(ep, gm < M ? gm : (M > 0 ? M - 1 : 0)) : 1.f;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      e.row0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM + q * 32);
-      epilogue_tile<BN, EPI, NB>(e, taddr, ch, e.row0 + lane, M, n_blk, N, ep, s_norm, s_norm + 128, &tmC);
+      epilogue_tile<BN, EPI, NB>(e, taddr, ch, gm, M, n_blk, N, ep, s_norm, s_norm + 128, &tmC, &tmD, rs);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -478,7 +579,7 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* pt
 
 template <int BN, int EPI, int CG>
 int launch(const rdx_gemm_args& a, cudaStream_t stream) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPI>;
   auto kern = gemm_kernel<BN, EPI, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -486,12 +587,13 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
     if (CG == 2) RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     attr_set = true;
   }
-  CUtensorMap ma, mb, mc;
+  CUtensorMap ma, mb, mc, md;
+  std::memset(&md, 0, sizeof(md));
   int st = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.a, a.k, a.m, a.lda, BK, BM);
   if (st) return st;
   st = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, C::B_ROWS);
   if (st) return st;
-  if (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
+  if (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32 || EPI == RDX_EPI_RESID_NORM) {
     st = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.out, a.n, a.m, a.ldo, 32, 32);
   } else {
     const int64_t ncols = EPI == RDX_EPI_SWIGLU ? a.n / 2 : a.n;
@@ -499,6 +601,11 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
                   CU_TENSOR_MAP_SWIZZLE_64B);
   }
   if (st) return st;
+  if (EPI == RDX_EPI_RESID_NORM) {
+    st = make_map(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.out_bf16, a.n, a.m, a.ldo_bf16, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_64B);
+    if (st) return st;
+  }
   EpiParams ep;
   ep.qn = a.q_norm_w;
   ep.kn = a.k_norm_w;
@@ -507,6 +614,16 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   ep.q_dim = a.q_heads * a.head_dim;
   ep.kv_dim = a.kv_heads * a.head_dim;
   ep.eps = a.eps;
+  ep.row_ss = a.row_ss;
+  ep.ss_parts = a.ss_parts;
+  ep.inv_norm_dim = a.norm_dim > 0 ? 1.f / static_cast<float>(a.norm_dim) : 0.f;
+  ep.norm_eps = a.norm_eps;
+  ep.h = static_cast<float*>(a.out);
+  ep.ldh = a.ldo;
+  ep.hb = static_cast<__nv_bfloat16*>(a.out_bf16);
+  ep.ldhb = a.ldo_bf16;
+  ep.ss_out = a.ss_out;
+  ep.ss_out_parts = static_cast<int>(a.n / kNormGroup);
   const int64_t tiles = ((a.m + BM * CG - 1) / (BM * CG)) * ((a.n + BN - 1) / BN);
   const int64_t units_max = num_sms() / CG;
   const int64_t units = tiles < units_max ? tiles : units_max;
@@ -522,14 +639,18 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, a.m, a.n, a.k, ep));
+  RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, md, a.m, a.n, a.k, ep));
   return RDX_OK;
 }
 
 template <int EPI>
 int dispatch(const rdx_gemm_args& a, int bn, int cg, cudaStream_t s) {
   if (cg == 2) return bn == 256 ? launch<256, EPI, 2>(a, s) : launch<128, EPI, 2>(a, s);
-  return bn == 256 ? launch<256, EPI, 1>(a, s) : launch<128, EPI, 1>(a, s);
+  if constexpr (EPI == RDX_EPI_RESID_NORM) {
+    return launch<128, EPI, 1>(a, s);  // the 1-CTA 256-wide tile leaves too few stages next to its staging boxes
+  } else {
+    return bn == 256 ? launch<256, EPI, 1>(a, s) : launch<128, EPI, 1>(a, s);
+  }
 }
 
 // Pick (CG, BN): fewest tile rounds x tile width, preferring the CTA pair.
@@ -597,6 +718,7 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
   int bn = 256, cg = 1;
   if (a.epi == RDX_EPI_QKV && (a.head_dim <= 0 || a.head_dim % 16 || a.head_dim > 128))
     return RDX_ERR_SHAPE_MISMATCH;
+  if (a.row_ss && (a.ss_parts <= 0 || a.norm_dim <= 0)) return RDX_ERR_INVALID_ARGUMENT;
   choose_shape(a, &bn, &cg);
   cudaStream_t s = as_stream(stream);
   switch (a.epi) {
@@ -609,6 +731,10 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
     case RDX_EPI_RESID_F32:
       if (a.ldo % 4 || a.ldo < a.n) return RDX_ERR_SHAPE_MISMATCH;
       return dispatch<RDX_EPI_RESID_F32>(a, bn, cg, s);
+    case RDX_EPI_RESID_NORM:
+      if (a.n % kNormGroup || a.ldo % 4 || a.ldo < a.n || a.ldo_bf16 % 8 || a.ldo_bf16 < a.n) return RDX_ERR_SHAPE_MISMATCH;
+      if (!a.out_bf16 || !a.ss_out || (reinterpret_cast<uintptr_t>(a.out_bf16) & 15)) return RDX_ERR_INVALID_ARGUMENT;
+      return dispatch<RDX_EPI_RESID_NORM>(a, bn, cg, s);
     case RDX_EPI_SWIGLU:
       if (a.n % (2 * kSwigluUnit) || a.ldo % 8 || a.ldo < a.n / 2) return RDX_ERR_SHAPE_MISMATCH;
       return dispatch<RDX_EPI_SWIGLU>(a, bn, cg, s);

@@ -104,6 +104,44 @@ embed_rmsnorm_kernel(const uint32_t* __restrict__ tok, const uint32_t* __restric
   }
 }
 
+// Compact embedding gather for the fused-norm layer stack: h (fp32), hb = bf16(h)
+// (= the bf16 embedding row, exactly) and one partial sum of h^2 per 64 columns
+// (8 lanes x 8 columns, fixed xor-tree order).  One warp per row; d % 64 == 0.
+__global__ void __launch_bounds__(256)
+embed_rows_kernel(const uint32_t* __restrict__ tok, const uint32_t* __restrict__ gather, int64_t n_rows,
+                  const __nv_bfloat16* __restrict__ embed, int64_t vocab, int64_t d, float* __restrict__ h,
+                  __nv_bfloat16* __restrict__ hb, float* __restrict__ ss_out, uint32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t parts = d / 64;
+  for (int64_t j = warp0; j < n_rows; j += nwarps) {
+    const uint32_t src = gather ? __ldg(gather + j) : static_cast<uint32_t>(j);
+    const uint32_t t = __ldg(tok + src);
+    const bool bad = static_cast<int64_t>(t) >= vocab;
+    if (bad && lane == 0) report(err, RDX_ERR_INDEX_OUT_OF_RANGE);
+    float* hrow = h + j * d;
+    int4* brow = reinterpret_cast<int4*>(hb + j * d);
+    const int4* erow = reinterpret_cast<const int4*>(embed + static_cast<int64_t>(bad ? 0 : t) * d);
+    for (int64_t c = lane; c < d / 8; c += 32) {  // d/8 is a multiple of 8: groups never straddle the loop
+      const int4 raw = bad ? make_int4(0, 0, 0, 0) : __ldg(erow + c);
+      float f[8];
+      bf16x8_to_f32(raw, f);
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += f[i] * f[i];
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if ((lane & 7) == 0) ss_out[j * parts + c / 8] = s;
+      float4* hp = reinterpret_cast<float4*>(hrow + c * 8);
+      hp[0] = make_float4(f[0], f[1], f[2], f[3]);
+      hp[1] = make_float4(f[4], f[5], f[6], f[7]);
+      brow[c] = raw;
+    }
+  }
+}
+
 // One warp per selected row; d % 8 == 0.
 __global__ void __launch_bounds__(256)
 rmsnorm_rows_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_t* __restrict__ rows,
@@ -242,6 +280,20 @@ extern "C" int rdx_embed_rmsnorm(const uint32_t* tok, const uint32_t* gather, in
   embed_rmsnorm_kernel<<<grid_for_rows(n_rows, 8), 256, 0, as_stream(stream)>>>(
       tok, gather, n_rows, static_cast<const __nv_bfloat16*>(embed_bf16), vocab, d, norm_w, eps, h_out,
       static_cast<__nv_bfloat16*>(hn_bf16_out), err_flag);
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}
+
+extern "C" int rdx_embed_rows(const uint32_t* tok, const uint32_t* gather, int64_t n_rows, const void* embed_bf16,
+                              int64_t vocab, int64_t d, float* h_out, void* hb_out, float* ss_out, uint32_t* err_flag,
+                              void* stream) {
+  using namespace rdx;
+  if (n_rows < 0 || d <= 0 || (d % 64) != 0) return RDX_ERR_SHAPE_MISMATCH;
+  if (n_rows == 0) return RDX_OK;
+  if (!tok || !embed_bf16 || !h_out || !hb_out || !ss_out) return RDX_ERR_INVALID_ARGUMENT;
+  embed_rows_kernel<<<grid_for_rows(n_rows, 8), 256, 0, as_stream(stream)>>>(
+      tok, gather, n_rows, static_cast<const __nv_bfloat16*>(embed_bf16), vocab, d, h_out,
+      static_cast<__nv_bfloat16*>(hb_out), ss_out, err_flag);
   RDX_LAUNCH_CHECK();
   return RDX_OK;
 }

@@ -234,6 +234,22 @@ class DeviceWeights:
                 t[pre + nm] = dev(pre + nm, f32)
         return cls(config, t)
 
+    def fold_norms(self) -> None:
+        """w_qkv_n = w_qkv * ln1, w_gu_n = w_gu * ln2 (per input column), bf16; idempotent.
+
+        RMSNorm(x) W^T = rstd(x) * (x (W diag(w))^T): the weight half of the norm
+        moves into the GEMM operand, the row scale into the GEMM epilogue.
+        """
+        import torch
+
+        for i in range(self.config.num_layers):
+            pre = f"layers.{i}."
+            for wname, nname in (("w_qkv", "ln1"), ("w_gu", "ln2")):
+                key = pre + wname + "_n"
+                if key not in self.t:
+                    w = self.t[pre + wname].float() * self.t[pre + nname].float()[None, :]
+                    self.t[key] = w.to(torch.bfloat16).contiguous()
+
     @classmethod
     def from_params(cls, config: ModelConfig, params: dict, device="cuda"):
         import torch
@@ -327,12 +343,22 @@ class RadixQwen3:
     plans to a bucket (``pad_plan``) to bound the number of distinct keys.
     """
 
-    def __init__(self, config: ModelConfig, weights: DeviceWeights, use_graphs: bool = False):
+    def __init__(self, config: ModelConfig, weights: DeviceWeights, use_graphs: bool = False,
+                 fused_norm: bool | None = None):
         _check_kernel_shapes(config)
         self.config = config
         self.w = weights
         self.di_pad = padded_intermediate(config)
         self.use_graphs = use_graphs
+        # fused_norm: ln1/ln2 folded into the QKV / gate-up weights, row statistics from the
+        # residual GEMM epilogue (RDX_EPI_RESID_NORM) -> no standalone rmsnorm passes.
+        # Off by default: measured on B200 it does not beat the TMA reduce-add epilogue +
+        # rmsnorm pass (C2 7.48-7.58 vs 7.66-7.68 ms, C4 551 vs 556 ms; DESIGN.md).
+        self.fused_norm = False if fused_norm is None else fused_norm
+        if self.fused_norm:
+            if config.hidden_size % 64:
+                raise ShapeMismatch("fused_norm needs hidden_size % 64 == 0")
+            weights.fold_norms()
         self.op_hook = None  # optional callable(name, launch_fn, flops) (bench.py per-op CUDA events)
         self._graphs: dict = {}
 
@@ -342,7 +368,8 @@ class RadixQwen3:
             return self.op_hook(name, fn, flops)
         return fn()
 
-    def _gemm(self, name, a, w, epi, out, *, m, stream, qkv=False, rope=None, layer=None):
+    def _gemm(self, name, a, w, epi, out, *, m, stream, qkv=False, rope=None, layer=None, row_ss=None,
+              hb=None, ss_out=None):
         cfg = self.config
         args = _native.GemmArgs()
         args.a = a.data_ptr()
@@ -364,6 +391,15 @@ class RadixQwen3:
             args.q_heads = cfg.num_heads
             args.kv_heads = cfg.num_kv_heads
             args.eps = cfg.norm_eps
+        if row_ss is not None:  # RMSNorm of the A rows fused in (weight folded into w)
+            args.row_ss = row_ss.data_ptr()
+            args.ss_parts = row_ss.shape[1]
+            args.norm_dim = cfg.hidden_size
+            args.norm_eps = cfg.norm_eps
+        if hb is not None:  # RDX_EPI_RESID_NORM outputs
+            args.out_bf16 = hb.data_ptr()
+            args.ldo_bf16 = hb.stride(0)
+            args.ss_out = ss_out.data_ptr()
         lib = _native.lib()
 
         def launch():
@@ -542,16 +578,26 @@ class RadixQwen3:
         qd, kvd = cfg.q_dim, cfg.kv_dim
         bf = torch.bfloat16
         h = torch.empty(m, d, dtype=torch.float32, device=dev)
-        hn = torch.empty(m, d, dtype=bf, device=dev)
+        hn = torch.empty(m, d, dtype=bf, device=dev)  # fused_norm: bf16(h), unnormalised
         err = torch.zeros(1, dtype=torch.int32, device=dev)
+        fused = self.fused_norm
+        ss = torch.empty(m, d // 64, dtype=torch.float32, device=dev) if fused else None
 
         def embed():
+            if fused:
+                code = lib.rdx_embed_rows(tok.data_ptr(), None if gather is None else gather.data_ptr(), m,
+                                          T["embed"].data_ptr(), cfg.vocab_size, d, h.data_ptr(), hn.data_ptr(),
+                                          ss.data_ptr(), err.data_ptr(), st)
+                _native.check(code, "rdx_embed_rows")
+                return
             code = lib.rdx_embed_rmsnorm(tok.data_ptr(), None if gather is None else gather.data_ptr(), m,
                                          T["embed"].data_ptr(), cfg.vocab_size, d, T["layers.0.ln1"].data_ptr(),
                                          cfg.norm_eps, h.data_ptr(), hn.data_ptr(), err.data_ptr(), st)
             _native.check(code, "rdx_embed_rmsnorm")
 
         self._op("embed_rmsnorm", embed)
+        resid_epi = _native.EPI_RESID_NORM if fused else _native.EPI_RESID_F32
+        sfx = "_n" if fused else ""
         rope = torch.empty(m, hd // 2, 2, dtype=torch.float32, device=dev)
 
         def rope_fn():
@@ -572,8 +618,8 @@ class RadixQwen3:
 
         for i in range(cfg.num_layers):
             pre = f"layers.{i}."
-            self._gemm("qkv", hn, T[pre + "w_qkv"], _native.EPI_QKV, qkv, m=m, stream=st, qkv=True, rope=rope,
-                       layer=pre)
+            self._gemm("qkv", hn, T[pre + "w_qkv" + sfx], _native.EPI_QKV, qkv, m=m, stream=st, qkv=True,
+                       rope=rope, layer=pre, row_ss=ss)
             if mode == "plain":
                 a = self._attn(qkv, None, cu32, cu32, b, max_k, max_k, attn_out, att_flops, st)
             elif mode == "suffix":
@@ -584,11 +630,14 @@ class RadixQwen3:
                 self._attn(qkv_full, None, cu32, cu32, b, max_k, max_k, a_full, att_flops, st)
                 a = self._gather("gather_attn", a_full, gather, stream)
             a = a.reshape(m, qd)
-            self._gemm("o_proj", a, T[pre + "wo"], _native.EPI_RESID_F32, h, m=m, stream=st)
-            self._rmsnorm(h, T[pre + "ln2"], hn, stream=st)
-            self._gemm("gate_up", hn, T[pre + "w_gu"], _native.EPI_SWIGLU, act, m=m, stream=st)
-            self._gemm("down", act, T[pre + "w_down"], _native.EPI_RESID_F32, h, m=m, stream=st)
-            if i + 1 < cfg.num_layers:
+            self._gemm("o_proj", a, T[pre + "wo"], resid_epi, h, m=m, stream=st, hb=hn if fused else None,
+                       ss_out=ss)
+            if not fused:
+                self._rmsnorm(h, T[pre + "ln2"], hn, stream=st)
+            self._gemm("gate_up", hn, T[pre + "w_gu" + sfx], _native.EPI_SWIGLU, act, m=m, stream=st, row_ss=ss)
+            self._gemm("down", act, T[pre + "w_down"], resid_epi, h, m=m, stream=st, hb=hn if fused else None,
+                       ss_out=ss)
+            if not fused and i + 1 < cfg.num_layers:
                 self._rmsnorm(h, T[f"layers.{i + 1}.ln1"], hn, stream=st)
 
         vocab = cfg.vocab_size

@@ -153,3 +153,66 @@ def test_gemm_error_codes():
     with pytest.raises(ShapeMismatch):
         _gemm(a, w, _native.EPI_STORE_BF16, out)
     np.testing.assert_equal(1, 1)
+
+
+def _gemm_norm(a, w, epi, out, block_n=0, row_ss=None, norm_dim=0, eps=1e-6, hb=None, ss_out=None):
+    from paper_2601_15013_b200 import _native
+
+    args = _native.GemmArgs()
+    args.a, args.b = a.data_ptr(), w.data_ptr()
+    args.m, args.n, args.k = a.shape[0], w.shape[0], w.shape[1]
+    args.lda, args.ldb = a.stride(0), w.stride(0)
+    args.epi, args.block_n = epi, block_n
+    args.out, args.ldo = out.data_ptr(), out.stride(0)
+    if row_ss is not None:
+        args.row_ss, args.ss_parts, args.norm_dim, args.norm_eps = row_ss.data_ptr(), row_ss.shape[1], norm_dim, eps
+    if hb is not None:
+        args.out_bf16, args.ldo_bf16, args.ss_out = hb.data_ptr(), hb.stride(0), ss_out.data_ptr()
+    _native.check(_native.lib().rdx_gemm(args, _native.stream_handle()), "rdx_gemm")
+
+
+@pytest.mark.parametrize("m,n,k", [(300, 1024, 2048), (7024, 1024, 3072), (129, 64, 128), (1000, 2560, 512)])
+@pytest.mark.parametrize("block_n", [128, 256])
+def test_resid_norm_epilogue(m, n, k, block_n):
+    """RDX_EPI_RESID_NORM: h += acc, hb = bf16(h), ss = per-64-column sums of h^2 (model.py:387-392 fused)."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    a, w = _rand(m, k, 11), _rand(n, k, 12, 0.05)
+    h0 = torch.randn(m, n, device="cuda")
+    h = h0.clone()
+    hb = torch.full((m, n), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ss = torch.full((m, n // 64), float("nan"), device="cuda")
+    _gemm_norm(a, w, _native.EPI_RESID_NORM, h, block_n, hb=hb, ss_out=ss)
+    torch.cuda.synchronize()
+    ref = h0 + a.float() @ w.float().T
+    assert (h - ref).abs().max().item() <= 1e-3 * ref.abs().max().item()
+    assert torch.equal(hb, h.to(torch.bfloat16))  # exactly the bf16 of the stored residual
+    ref_ss = (h * h).view(m, n // 64, 64).sum(-1)
+    assert torch.allclose(ss, ref_ss, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("block_n", [128, 256])
+def test_row_norm_fused_swiglu_and_qkv(block_n):
+    """row_ss scaling == RMSNorm of the A rows with the weight folded into B."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    m, d, di = 517, 1024, 1536
+    x = torch.randn(m, d, device="cuda") * 3
+    ln = torch.rand(d, device="cuda") + 0.5
+    ss = (x * x).view(m, d // 64, 64).sum(-1)
+    xb = x.to(torch.bfloat16)
+    # SwiGLU: gate/up interleaved in 64-column units (csrc/gemm.cu)
+    wg, wu = _rand(di, d, 21, 0.05), _rand(di, d, 22, 0.05)
+    w_gu = torch.cat([wg.view(di // 64, 1, 64, d), wu.view(di // 64, 1, 64, d)], 1).reshape(2 * di, d)
+    w_fold = (w_gu.float() * ln[None, :]).to(torch.bfloat16)
+    out = torch.full((m, di), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _gemm_norm(xb, w_fold, _native.EPI_SWIGLU, out, block_n, row_ss=ss, norm_dim=d, eps=1e-6)
+    torch.cuda.synchronize()
+    xn = x / torch.sqrt((x * x).mean(1, keepdim=True) + 1e-6) * ln
+    g, u = xn @ wg.float().T, xn @ wu.float().T
+    ref = torch.nn.functional.silu(g) * u
+    assert (out.float() - ref).abs().max().item() <= 3e-2 * ref.abs().max().item()

@@ -141,3 +141,22 @@ def test_causality():
         diff = np.abs(a - p).max(axis=1)
         assert np.all(diff[:4] == 0.0)
         assert np.all(diff[4:] > 0.0)
+
+
+def test_fused_norm_path_matches_reference():
+    """RMSNorm folded into the GEMMs (RDX_EPI_RESID_NORM + row_ss) gives the reference's logits."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2601_15013_b200 import TINY_C1, DeviceWeights, RadixQwen3, build_plan, init_params
+    from paper_2601_15013_b200.model import DeviceBatch
+    from paper_2601_15013_b200.workloads import SyntheticSpec, make_synthetic_batch
+
+    batch = make_synthetic_batch(SyntheticSpec(B=8, prefix_len=32, suffix_len=16, vocab=1024, seed=0))
+    params = init_params(TINY_C1, seed=0)
+    model = RadixQwen3(TINY_C1, DeviceWeights.from_params(TINY_C1, params), fused_norm=True)
+    out = model.prefill(DeviceBatch.from_batch(batch), build_plan(batch)).float().cpu().numpy()
+    ref = orc.forward_oracle(TINY_C1, params, batch.token_ids, batch.position_ids, batch.cu_seqlens)
+    err = float(np.abs(out - ref).max() / np.abs(ref).max())
+    assert err <= 2e-2, err
+    torch.cuda.synchronize()
