@@ -38,7 +38,8 @@ namespace {
 constexpr int kPlanThreads = 512;
 constexpr int kPlanWarps = kPlanThreads / 32;
 constexpr int kMaxAttempts = 4;
-constexpr int kTokensPerBlockTarget = 2048;
+constexpr int kTokensPerBlockTarget = 512;
+constexpr int64_t kSingleCtaTokens = 1024;  // up to here one CTA beats a cooperative grid (launch + grid barriers)
 
 __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
   k ^= k >> 33;
@@ -128,9 +129,17 @@ __device__ uint64_t block_sum_u64(uint64_t v, uint64_t* warp_tot) {
   return total;
 }
 
+// SINGLE = one CTA (small batches): phases are separated by __syncthreads
+// instead of cooperative grid barriers, and the launch is an ordinary one.
+template <bool SINGLE>
 __global__ void __launch_bounds__(kPlanThreads)
 plan_build_kernel(PlanArgs a, PlanScratch s) {
-  cg::grid_group grid = cg::this_grid();
+  struct Sync {
+    __device__ void sync() {
+      if constexpr (SINGLE) __syncthreads();
+      else cg::this_grid().sync();
+    }
+  } grid;
   __shared__ uint64_t warp_tot[kPlanWarps];
 
   const int64_t n = a.n;
@@ -316,7 +325,7 @@ int max_coop_blocks() {
   static int cached = 0;
   if (cached == 0) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_build_kernel, kPlanThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_build_kernel<false>, kPlanThreads, 0) !=
         cudaSuccess)
       return 0;
     cached = per_sm * num_sms();
@@ -382,7 +391,12 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
   if (want < 1) want = 1;
   const int grid = static_cast<int>(want < mg ? want : mg);
   void* params[] = {&a, &s};
-  RDX_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_build_kernel), dim3(grid),
+  if (n_tokens <= kSingleCtaTokens) {  // small batch: one CTA, no grid-wide barriers
+    plan_build_kernel<true><<<1, kPlanThreads, 0, as_stream(stream)>>>(a, s);
+    RDX_LAUNCH_CHECK();
+    return RDX_OK;
+  }
+  RDX_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_build_kernel<false>), dim3(grid),
                                            dim3(kPlanThreads), params, 0, as_stream(stream)));
   return RDX_OK;
 }
