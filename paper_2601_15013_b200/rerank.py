@@ -52,13 +52,14 @@ class RadixReranker:
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
-    def upload(self, batch: RaggedBatch) -> DeviceBatch:
+    def upload(self, batch: RaggedBatch, slot: int = 0) -> DeviceBatch:
+        """Pinned staging (slot = double-buffer index for pipelined streams) -> HBM, async."""
         import torch
 
         n, b = batch.num_tokens, batch.num_sequences
-        tok = self._pinned.get("tok", n, torch.int32)
-        pos = self._pinned.get("pos", n, torch.int32)
-        cu = self._pinned.get("cu", b + 1, torch.int64)
+        tok = self._pinned.get(f"tok{slot}", n, torch.int32)
+        pos = self._pinned.get(f"pos{slot}", n, torch.int32)
+        cu = self._pinned.get(f"cu{slot}", b + 1, torch.int64)
         tok.numpy()[:] = batch.token_ids.view(np.int32)
         pos.numpy()[:] = batch.position_ids.view(np.int32)
         cu.numpy()[:] = batch.cu_seqlens
@@ -68,11 +69,17 @@ class RadixReranker:
         self.h2d_bytes = tok.numel() * 4 + pos.numel() * 4 + cu.numel() * 8
         return DeviceBatch(dt, dp, dc, dc.to(torch.int32), cu_host, n, b, int(lens.max()) if lens.size else 0)
 
-    def score_device(self, db: DeviceBatch):
-        """Device-resident batch -> device scores [B] (float32)."""
+    def plan(self, db: DeviceBatch):
+        """GPU plan of a device batch (None when dedup is off)."""
+        return build_plan_device(db.tok, db.pos, db.cu) if self.dedup else None
+
+    def score_device(self, db: DeviceBatch, plan="build"):
+        """Device-resident batch -> device scores [B] (float32).  ``plan``: "build" (GPU
+        planner now), or a plan prepared earlier (pipelined streams)."""
         import torch
 
-        plan = build_plan_device(db.tok, db.pos, db.cu) if self.dedup else None
+        if isinstance(plan, str) and plan == "build":
+            plan = self.plan(db)
         self.last_plan = plan
         logits = self.model.prefill(db, plan, attention=self.attention, logits="last")
         scores = torch.empty(db.b, dtype=torch.float32, device=logits.device)
@@ -88,4 +95,15 @@ class RadixReranker:
         out = scores.cpu().numpy()
         # D2H: the plan's (N', status, cu_q) read (dedup only) and the scores
         self.d2h_bytes = out.nbytes + ((4 + batch.num_sequences + 1) * 4 if self.dedup else 0)
+        return out
+
+    def score_many(self, batches) -> list:
+        """Scores of a stream of host batches; batch t+1's upload and plan build overlap
+        batch t's prefill (pipeline.score_stream).  Same results as ``score`` per batch."""
+        from .pipeline import score_stream
+
+        out = score_stream(self, batches)
+        if out:
+            last = batches[-1]
+            self.d2h_bytes = out[-1].nbytes + ((4 + last.num_sequences + 1) * 4 if self.dedup else 0)
         return out
