@@ -39,6 +39,7 @@ from .ops import (gather_rows, gather_rows_backward, gather_rows_backward_device
                   scatter_rows_backward)
 from .pipeline import PipelineReport, pipelined_run, score_stream
 from .primitives import apply_rope, attention_ragged, rmsnorm, swiglu_mlp
+from .training import loss_and_grads
 from .plan import (
     CompactionPlan,
     DevicePlan,
@@ -68,7 +69,7 @@ __all__ = [
     "OverflowId", "PlanBatchMismatch", "QWEN3_PRESETS", "Qwen3Config", "RadixCompactError", "RadixQwen3",
     "RaggedBatch", "ShapeMismatch", "TINY_C1", "batch_from_json", "batch_to_json", "build_plan",
     "build_plan_auto", "build_plan_device", "build_plan_fast_paths", "default_positions", "forward",
-    "forward_scores", "apply_rope", "attention_ragged", "rmsnorm", "swiglu_mlp", "pipelined_run", "PipelineReport", "score_stream", "gather_rows", "gather_rows_backward", "gather_rows_backward_device", "gather_rows_device", "init_params", "load_plan", "pad_plan",
+    "forward_scores", "loss_and_grads", "apply_rope", "attention_ragged", "rmsnorm", "swiglu_mlp", "pipelined_run", "PipelineReport", "score_stream", "gather_rows", "gather_rows_backward", "gather_rows_backward_device", "gather_rows_device", "init_params", "load_plan", "pad_plan",
     "plan_from_bytes", "plan_from_json", "plan_to_bytes", "plan_to_json", "save_plan", "scatter_rows", "scatter_rows_backward",
     "should_enable", "validate_batch",
 ]

@@ -16,6 +16,8 @@ Outputs (committed, small):
                  (seed 7), C1 (2L, d=64, 4 heads, 8x(32+16)), and a 1-layer
                  Qwen3-0.6B-dimension slice (q_dim != hidden via a subclass
                  that overrides only __post_init__, SURVEY finding 3).
+  grads.npz      reference loss_and_grads() on C1: loss + every parameter gradient
+                 (fp32) with the plan, loss without it.
   plan_toy.rdxp / plan_toy.json  reference serialisation of the toy plan.
 """
 
@@ -163,6 +165,25 @@ def forward():
     np.savez_compressed(os.path.join(OUT, "forward.npz"), **out)
 
 
+def grads():
+    """Reference loss_and_grads (model.py:419-531) on C1 with seeded targets: loss and
+    every gradient with the plan, loss without it."""
+    out = {}
+    c1 = rc.ModelConfig(num_layers=2, hidden_size=64, intermediate_size=192, num_heads=4, num_kv_heads=2,
+                        head_dim=16, vocab_size=1024)
+    p1 = rc.init_params(c1, seed=0)
+    b1 = make_synthetic_batch(SyntheticSpec(B=8, prefix_len=32, suffix_len=16, vocab=1024, seed=0))
+    t1 = np.random.default_rng(11).integers(0, c1.vocab_size, size=b1.num_tokens)
+    out["c1_targets"] = t1
+    loss, g = rc.loss_and_grads(c1, p1, b1, trie.build_plan(b1), t1)
+    out["c1_radix_loss"] = np.array(loss)
+    for name, val in g.items():  # fp32 storage: 6e-8 relative, far inside the 1e-6 check
+        out[f"c1_radix_grad:{name}"] = val.astype(np.float32)
+    loss_base, _ = rc.loss_and_grads(c1, p1, b1, None, t1)
+    out["c1_base_loss"] = np.array(loss_base)
+    np.savez_compressed(os.path.join(OUT, "grads.npz"), **out)
+
+
 def serial():
     plan = trie.build_plan(make([1, 2, 3, 1, 2, 4], [0, 3, 6]))
     trie.save_plan(plan, os.path.join(OUT, "plan_toy.rdxp"), binary=True)
@@ -173,6 +194,7 @@ if __name__ == "__main__":
     plans()
     synthetic()
     forward()
+    grads()
     serial()
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
