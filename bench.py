@@ -521,10 +521,15 @@ def run_ours(args):
     launches_per_step = _native.LAUNCHES.launches - c0
     model.use_graphs = graphs_on
 
-    if args.profile:  # short run for ncu: warm-ups + a few radix steps, no JSON
-        for _ in range(args.warmup + args.steps):
+    if args.profile:  # short run for ncu: warm-ups, then the profiled radix steps (cudaProfilerStart/Stop
+        for _ in range(args.warmup):  # bracket them, for `ncu --profile-from-start off`), no JSON
             step_radix()
         torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        for _ in range(args.steps):
+            step_radix()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         return
     sampler = ClockSampler(local) if rank == 0 else None
     ms_radix, per_radix, clocks = time_steps(step_radix, args.steps, args.warmup, world, flush, sampler)

@@ -110,8 +110,9 @@ def score_stream(reranker, batches):
     if not batches:
         return []
     main = torch.cuda.current_stream()
-    side = torch.cuda.Stream()
-    out_pinned = [None, None]
+    side = getattr(reranker, "_side_stream", None)
+    if side is None:
+        side = reranker._side_stream = torch.cuda.Stream()
 
     def prepare(batch, slot):
         validate_batch(batch)
@@ -134,15 +135,12 @@ def score_stream(reranker, batches):
                 x.record_stream(main)
         scores = reranker.score_device(db, plan=plan)
         b = scores.shape[0]
-        buf = out_pinned[t & 1]
-        if buf is None or buf.numel() < b:
-            buf = torch.empty(max(b, 1), dtype=torch.float32, pin_memory=True)
-            out_pinned[t & 1] = buf
-        buf[:b].copy_(scores, non_blocking=True)
+        buf = reranker._pinned.get(f"scores{t & 1}", b, torch.float32)  # grow-only, reused across calls
+        buf.copy_(scores, non_blocking=True)
         done = torch.cuda.Event()
         done.record(main)
         if t + 1 < len(batches):
             nxt = prepare(batches[t + 1], (t + 1) & 1)  # overlaps the prefill of batch t
         done.synchronize()
-        results.append(np.array(buf[:b].numpy(), copy=True))
+        results.append(np.array(buf.numpy(), copy=True))
     return results
