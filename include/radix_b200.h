@@ -213,6 +213,11 @@ typedef struct rdx_gemm_args {
 
 int rdx_gemm(const rdx_gemm_args* args, void* stream);
 
+/* Debug: the GEMM splits the tiles of a last partial round into 2 or 4
+ * narrower tiles (same per-element K reduction, same bits); 0 turns that off
+ * for A/B runs, 1 back on.  Returns the previous setting. */
+int rdx_gemm_debug_tail_split(int on);
+
 /* ---------------------------------------------------------------------
  * Causal GQA prefill attention on tcgen05/TMEM with the RadixMLP attention
  * boundary fused into its loads (replaces model.py:368-383 + 228-265):

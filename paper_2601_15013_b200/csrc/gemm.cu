@@ -79,6 +79,8 @@ struct Cfg {
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + AUX_BYTES + BAR_BYTES;
   static constexpr uint32_t IDESC = umma_idesc_bf16(BM * CG, BN);
+  static constexpr uint32_t IDESC_HALF = umma_idesc_bf16(BM * CG, BN / 2);
+  static constexpr uint32_t IDESC_QUARTER = umma_idesc_bf16(BM * CG, BN / 4);
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static_assert(STAGES >= 3, "pipeline too shallow");
 };
@@ -252,27 +254,31 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
 // All of the warp's accumulator columns are read from TMEM with one wait,
 // then transformed in registers and emitted box by box.
 template <int BN, int EPI, int NB>
-__device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, int ch, int64_t gm_lane, int64_t M,
-                                              int64_t n_blk, int64_t N, const EpiParams& ep, const float* s_qn,
-                                              const float* s_kn, const CUtensorMap* map, const CUtensorMap* map_hb,
-                                              float rs) {
+// hw = columns per warp of this tile (BN/2, or BN/4 for a split tail tile),
+// n0 = the tile's first output-space column.
+__device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, int ch, int hw, int64_t gm_lane,
+                                              int64_t M, int64_t n0, int64_t N, const EpiParams& ep,
+                                              const float* s_qn, const float* s_kn, const CUtensorMap* map,
+                                              const CUtensorMap* map_hb, float rs) {
   constexpr int HALF = BN / 2;
-  const int64_t n0 = n_blk * BN;
-  const int c_lo = ch * HALF;
+  const int c_lo = ch * hw;
   float v[HALF];
   if constexpr (EPI == RDX_EPI_SWIGLU) {
-    // warp ch owns outputs [ch*BN/4, (ch+1)*BN/4) of the tile's BN/2: output o of
+    // warp ch owns outputs [ch*hw/2, (ch+1)*hw/2) of the tile's width/2: output o of
     // pair p = o/64 reads gate column p*128 + o%64 and up column +64
 #pragma unroll
     for (int q = 0; q < HALF / 2; q += 32) {
-      const int o = ch * (HALF / 2) + q;
-      const int gcol = (o / kSwigluUnit) * 2 * kSwigluUnit + o % kSwigluUnit;
-      tmem_ld32p(taddr + gcol, v + q);
-      tmem_ld32p(taddr + gcol + kSwigluUnit, v + HALF / 2 + q);
+      if (q < hw / 2) {
+        const int o = ch * (hw / 2) + q;
+        const int gcol = (o / kSwigluUnit) * 2 * kSwigluUnit + o % kSwigluUnit;
+        tmem_ld32p(taddr + gcol, v + q);
+        tmem_ld32p(taddr + gcol + kSwigluUnit, v + HALF / 2 + q);
+      }
     }
   } else if constexpr (EPI != RDX_EPI_QKV) {
 #pragma unroll
-    for (int c = 0; c < HALF; c += 32) tmem_ld32p(taddr + c_lo + c, v + c);
+    for (int c = 0; c < HALF; c += 32)
+      if (c < hw) tmem_ld32p(taddr + c_lo + c, v + c);
   }
   const int64_t r_clamped = gm_lane < M ? gm_lane : (M > 0 ? M - 1 : 0);
   if constexpr (EPI != RDX_EPI_QKV) tmem_wait_ld();
@@ -281,7 +287,7 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
     // each lane adds its accumulator row, writes h_new back into the box and
     // bf16(h_new) into a bf16 box, and both go out by TMA store; the partial sum
     // of h_new^2 per 64 columns goes to ss_out.  Loads run one chunk ahead.
-    constexpr int CHUNKS = HALF / 32;
+    const int CHUNKS = hw / 32;
     auto fbox = [&](int i) { return e.base + (i & 1) * kEpiBoxBytes; };
     auto bbox = [&](int i) { return e.base + 2 * kEpiBoxBytes + (i & 1) * 2048; };
     auto load = [&](int i) {
@@ -294,7 +300,8 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
     load(0);
     float ssp = 0.f;
 #pragma unroll
-    for (int i = 0; i < CHUNKS; ++i) {
+    for (int i = 0; i < HALF / 32; ++i) {
+      if (i >= CHUNKS) break;
       const int64_t col = n0 + c_lo + 32 * i;
       if (i + 1 < CHUNKS && col + 32 < N) load(i + 1);
       if (col >= N) break;
@@ -334,7 +341,7 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
   } else if constexpr (EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
 #pragma unroll
     for (int c = 0; c < HALF; c += 32) {
-      if (n0 + c_lo + c < N) {
+      if (c < hw && n0 + c_lo + c < N) {
         if constexpr (EPI == RDX_EPI_STORE_BF16) emit_bf16x32(e, v + c, map, static_cast<int32_t>(n0 + c_lo + c));
         else emit_f32x32(e, v + c, map, static_cast<int32_t>(n0 + c_lo + c), EPI == RDX_EPI_RESID_F32);
       }
@@ -343,8 +350,8 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
     const int64_t nout = N / 2;
 #pragma unroll
     for (int q = 0; q < HALF / 2; q += 32) {
-      const int64_t ocol = n_blk * (BN / 2) + ch * (HALF / 2) + q;
-      if (ocol < nout) {
+      const int64_t ocol = n0 / 2 + ch * (hw / 2) + q;
+      if (q < hw / 2 && ocol < nout) {
         float* g = v + q;
         const float* u = v + HALF / 2 + q;
 #pragma unroll
@@ -358,7 +365,7 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
   } else if constexpr (EPI == RDX_EPI_QKV) {
     // chunked: TMEM loads interleaved with the norm / RoPE math and the stores
     const float2* rope_row = ep.rope + r_clamped * (ep.hd >> 1);
-    const int c_hi = c_lo + HALF;
+    const int c_hi = c_lo + hw;
     switch (ep.hd) {
       case 128: qkv_cols<128>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
       case 64: qkv_cols<64>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
@@ -372,8 +379,9 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
 template <int BN, int EPI, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmB4,
             const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int64_t M, int64_t N,
-            int64_t K, EpiParams ep) {
+            int64_t K, int64_t tail_start, int split, EpiParams ep) {
   using C = Cfg<BN, CG, EPI>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -395,12 +403,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const int64_t n_units = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
   const int64_t m_tiles = (M + BM * CG - 1) / (BM * CG);
   const int64_t n_tiles = (N + BN - 1) / BN;
-  const int64_t num_tiles = m_tiles * n_tiles;
+  const int64_t full_tiles = m_tiles * n_tiles;
+  // Tail split: the tiles of the last partial round (from tail_start on) run as
+  // `split` narrower tiles each (width BN/split), so r leftover tiles occupy
+  // ceil(split*r/units)/split of a round instead of a whole one.  No split-K:
+  // every output element is still one CTA's full K reduction -> same bits.
+  const int64_t num_tiles = tail_start + split * (full_tiles - tail_start);
+  auto decode = [&](int64_t t, int64_t& m_blk, int64_t& n0, int& width) {
+    int64_t f = t;
+    int part = 0;
+    width = BN;
+    if (t >= tail_start) {
+      f = tail_start + (t - tail_start) / split;
+      part = static_cast<int>((t - tail_start) % split);
+      width = BN / split;
+    }
+    m_blk = f % m_tiles;
+    n0 = (f / m_tiles) * BN + part * width;
+  };
   const int kblocks = static_cast<int>((K + BK - 1) / BK);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmB2);
+    tma_prefetch_desc(&tmB4);
     tma_prefetch_desc(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -439,21 +466,27 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
-        const int32_t m0 = static_cast<int32_t>((tile % m_tiles) * (BM * CG) + rank * BM);
-        const int32_t nb0 = static_cast<int32_t>((tile / m_tiles) * BN + rank * C::B_ROWS);
+        int64_t m_blk, n0;
+        int width;
+        decode(tile, m_blk, n0, width);
+        const int div = BN / width;  // 1, 2 or 4
+        const int32_t m0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM);
+        const int32_t nb0 = static_cast<int32_t>(n0 + rank * (C::B_ROWS / div));
+        const uint32_t bytes = C::A_BYTES + C::B_BYTES / div;
+        const CUtensorMap* mapb = div == 1 ? &tmB : (div == 2 ? &tmB2 : &tmB4);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
           if constexpr (CG == 2) {
             const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
-            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
             tma_load_2d_cg2(&tmA, sa, bar, kb * BK, m0);
-            tma_load_2d_cg2(&tmB, sb, bar, kb * BK, nb0);
+            tma_load_2d_cg2(mapb, sb, bar, kb * BK, nb0);
           } else {
-            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], bytes);
             tma_load_2d(&tmA, sa, &full[stage], kb * BK, m0);
-            tma_load_2d(&tmB, sb, &full[stage], kb * BK, nb0);
+            tma_load_2d(mapb, sb, &full[stage], kb * BK, nb0);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -469,6 +502,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
+        int64_t m_blk, n0;
+        int width;
+        decode(tile, m_blk, n0, width);
+        const uint32_t idesc = width == BN ? C::IDESC : (width == BN / 2 ? C::IDESC_HALF : C::IDESC_QUARTER);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -481,8 +518,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // +32 B per K=16 step inside the 128 B swizzle atom (encoded >> 4)
-            if constexpr (CG == 2) umma_bf16_cg2_elect(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
-            else umma_bf16_elect(d_tmem, da + 2 * k, db + 2 * k, C::IDESC, (kb | k) != 0);
+            if constexpr (CG == 2) umma_bf16_cg2_elect(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+            else umma_bf16_elect(d_tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
           }
           if constexpr (CG == 2) umma_commit_cg2_mc_elect(&empty[stage], 0x3);
           else umma_commit_elect(&empty[stage]);
@@ -512,8 +549,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
-      const int64_t m_blk = tile % m_tiles;
-      const int64_t n_blk = tile / m_tiles;
+      int64_t m_blk, n0;
+      int width;
+      decode(tile, m_blk, n0, width);
       e.row0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM + q * 32);
       // row scale of the fused RMSNorm: its loads overlap the wait for the accumulator
       const int64_t gm = e.row0 + lane;
@@ -521,7 +559,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      epilogue_tile<BN, EPI, NB>(e, taddr, ch, gm, M, n_blk, N, ep, s_norm, s_norm + 128, &tmC, &tmD, rs);
+      epilogue_tile<BN, EPI, NB>(e, taddr, ch, width / 2, gm, M, n0, N, ep, s_norm, s_norm + 128, &tmC, &tmD, rs);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -577,6 +615,16 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* pt
   return r == CUDA_SUCCESS ? RDX_OK : RDX_ERR_INVALID_ARGUMENT;
 }
 
+// RDX_GEMM_TAIL_SPLIT=0 (env) or rdx_gemm_debug_tail_split(0) disables the tail split (A/B runs).
+int g_tail_split = -1;
+bool tail_split_enabled() {
+  if (g_tail_split < 0) {
+    const char* e = getenv("RDX_GEMM_TAIL_SPLIT");
+    g_tail_split = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_tail_split == 1;
+}
+
 template <int BN, int EPI, int CG>
 int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   using C = Cfg<BN, CG, EPI>;
@@ -587,11 +635,15 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
     if (CG == 2) RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     attr_set = true;
   }
-  CUtensorMap ma, mb, mc, md;
+  CUtensorMap ma, mb, mb2, mb4, mc, md;
   std::memset(&md, 0, sizeof(md));
   int st = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.a, a.k, a.m, a.lda, BK, BM);
   if (st) return st;
   st = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, C::B_ROWS);
+  if (st) return st;
+  st = make_map(&mb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, C::B_ROWS / 2);
+  if (st) return st;
+  st = make_map(&mb4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, C::B_ROWS / 4);
   if (st) return st;
   if (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32 || EPI == RDX_EPI_RESID_NORM) {
     st = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.out, a.n, a.m, a.ldo, 32, 32);
@@ -627,6 +679,28 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   const int64_t tiles = ((a.m + BM * CG - 1) / (BM * CG)) * ((a.n + BN - 1) / BN);
   const int64_t units_max = num_sms() / CG;
   const int64_t units = tiles < units_max ? tiles : units_max;
+  // tail split (see gemm_kernel): pick the factor s in {1, 2} that minimises the
+  // last round's length ceil(s*rem/units)/s, subject to each narrow tile keeping
+  // whole epilogue units per warp (64-column SwiGLU pairs, whole heads, 64-column
+  // norm groups, 32-column boxes)
+  const int64_t rem = tiles % units;
+  int split = 1;
+  if (BN == 256 && rem > 0 && tail_split_enabled()) {
+    double best = 1.0;
+    for (int sf : {2}) {  // quarters measured slower: a narrow tile still streams the full A tile
+      const int w = BN / sf;
+      bool ok = (w / 2) % 32 == 0;
+      if (EPI == RDX_EPI_SWIGLU) ok = ok && w % (2 * kSwigluUnit) == 0;
+      if (EPI == RDX_EPI_QKV) ok = ok && a.head_dim > 0 && (w / 2) % a.head_dim == 0;
+      if (EPI == RDX_EPI_RESID_NORM) ok = ok && (w / 2) % kNormGroup == 0;
+      const double len = static_cast<double>((sf * rem + units - 1) / units) / sf;
+      if (ok && len < best - 1e-9) {
+        best = len;
+        split = sf;
+      }
+    }
+  }
+  const int64_t tail_start = split > 1 ? tiles - rem : tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(units * CG));
   cfg.blockDim = dim3(kThreads);
@@ -639,7 +713,7 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, md, a.m, a.n, a.k, ep));
+  RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mb2, mb4, mc, md, a.m, a.n, a.k, tail_start, split, ep));
   return RDX_OK;
 }
 
@@ -748,4 +822,11 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
     default:
       return RDX_ERR_INVALID_ARGUMENT;
   }
+}
+
+// Debug: switch the GEMM tail split on (1) / off (0); returns the previous setting.
+extern "C" int rdx_gemm_debug_tail_split(int on) {
+  const int prev = rdx::gemm::tail_split_enabled() ? 1 : 0;
+  rdx::gemm::g_tail_split = on ? 1 : 0;
+  return prev;
 }

@@ -216,3 +216,39 @@ def test_row_norm_fused_swiglu_and_qkv(block_n):
     g, u = xn @ wg.float().T, xn @ wu.float().T
     ref = torch.nn.functional.silu(g) * u
     assert (out.float() - ref).abs().max().item() <= 3e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("epi_name,m,n,k", [("EPI_RESID_F32", 7024, 1536, 2048), ("EPI_SWIGLU", 7024, 6144, 1024),
+                                            ("EPI_STORE_BF16", 7024, 2560, 3072), ("EPI_STORE_F32", 5000, 2048, 512)])
+def test_tail_split_bit_identical(epi_name, m, n, k):
+    """The last partial round runs as half-width tiles (e.g. the C2 gate-up shape): every
+    element is still one CTA's full K reduction -> identical bits."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    lib = _native.lib()
+    epi = getattr(_native, epi_name)
+    a, w = _rand(m, k, 31), _rand(n, k, 32, 0.05)
+    if epi == _native.EPI_SWIGLU:
+        shape, dt = (m, n // 2), torch.bfloat16
+    elif epi == _native.EPI_STORE_BF16:
+        shape, dt = (m, n), torch.bfloat16
+    else:
+        shape, dt = (m, n), torch.float32
+    base = torch.randn(shape, device="cuda").to(dt) if epi == _native.EPI_RESID_F32 else torch.zeros(shape, dtype=dt,
+                                                                                                      device="cuda")
+    outs = []
+    for on in (1, 0):
+        prev = lib.rdx_gemm_debug_tail_split(on)
+        try:
+            o = base.clone()
+            _gemm(a, w, epi, o)
+            torch.cuda.synchronize()
+        finally:
+            lib.rdx_gemm_debug_tail_split(prev)
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
+    if epi == _native.EPI_STORE_F32:
+        ref = a.float() @ w.float().T
+        assert (outs[0] - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
