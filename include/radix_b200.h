@@ -218,6 +218,12 @@ int rdx_gemm(const rdx_gemm_args* args, void* stream);
  * for A/B runs, 1 back on.  Returns the previous setting. */
 int rdx_gemm_debug_tail_split(int on);
 
+/* Debug: programmatic dependent launch (PDL) of the layer-stack kernels on (1)
+ * or off (0) for launches / CUDA-graph captures made after the call (default
+ * off -- measured neutral; RDX_PDL=1 in the environment turns it on).  Returns
+ * the previous setting. */
+int rdx_debug_pdl(int on);
+
 /* ---------------------------------------------------------------------
  * Causal GQA prefill attention on tcgen05/TMEM with the RadixMLP attention
  * boundary fused into its loads (replaces model.py:368-383 + 228-265):

@@ -381,6 +381,9 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  // barrier init + TMEM alloc overlapped the previous kernel's tail (PDL); inputs from here on
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp >= 8) {
     setmaxnreg_dec<80>();
@@ -841,9 +844,8 @@ int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
     if (e) return e;
   }
   const int ctas = a.n_units < num_sms() ? a.n_units : num_sms();
-  kern<<<static_cast<unsigned>(ctas), kThreads, T::SMEM, st>>>(map_kv, map_q, map_g4, map_r16, a);
-  RDX_LAUNCH_CHECK();
-  return RDX_OK;
+  return launch_pdl(kern, dim3(static_cast<unsigned>(ctas)), dim3(kThreads), T::SMEM, st, map_kv, map_q, map_g4,
+                    map_r16, a);
 }
 
 }  // namespace attn

@@ -1,5 +1,6 @@
 // capi.cu — status plumbing and device queries shared by every entry point.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -25,6 +26,15 @@ int num_sms() {
     cached = n;
   }
   return cached;
+}
+
+int g_pdl = -1;
+bool pdl_enabled() {
+  if (g_pdl < 0) {
+    const char* e = std::getenv("RDX_PDL");  // off by default: measured neutral on the C2 graph step
+    g_pdl = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_pdl == 1;
 }
 
 }  // namespace rdx
@@ -55,3 +65,11 @@ extern "C" const char* rdx_status_name(int status) {
 extern "C" const char* rdx_last_cuda_error(void) { return rdx::g_last_error; }
 
 extern "C" int rdx_num_sms(void) { return rdx::num_sms(); }
+
+// Debug: programmatic dependent launch of the layer-stack kernels on (1) / off (0)
+// for launches made (or CUDA graphs captured) after the call; returns the previous setting.
+extern "C" int rdx_debug_pdl(int on) {
+  const int prev = rdx::pdl_enabled() ? 1 : 0;
+  rdx::g_pdl = on ? 1 : 0;
+  return prev;
+}

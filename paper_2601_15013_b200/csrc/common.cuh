@@ -26,6 +26,38 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int num_sms();
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of the layer stack are launched with the PDL attribute: a kernel's CTAs
+// may start (barrier init, TMEM alloc, descriptor prefetch) while its predecessor
+// drains, and block in pdl_wait() until the predecessor grid has completed and
+// its writes are visible.  No-ops for ordinary launches.  Off by default (RDX_PDL=1
+// or rdx_debug_pdl(1) turns it on): A/B on the C2 CUDA-graph step measured it
+// neutral (7.59 vs 7.58 ms), the graph already hides launch latency.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  return e == cudaSuccess ? 0 : set_cuda_error(e);
+}
+#define RDX_LAUNCH_PDL(kern, grid, block, smem, st, ...)                                   \
+  do {                                                                                       \
+    const int _rc = ::rdx::launch_pdl(kern, dim3(grid), dim3(block), smem, st, __VA_ARGS__); \
+    if (_rc) return _rc;                                                                     \
+  } while (0)
+
 namespace gemm {
 // 2-D row-major TMA map (defined in gemm.cu): inner = columns, outer = rows, box = box_inner x box_outer.
 int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* ptr, int64_t inner, int64_t outer,

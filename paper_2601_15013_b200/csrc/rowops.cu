@@ -20,6 +20,7 @@ __global__ void __launch_bounds__(256)
 gather_rows_kernel(const char* __restrict__ src, int64_t src_rows, int64_t ld_src,
                    const uint32_t* __restrict__ idx, int64_t n_idx, char* __restrict__ dst,
                    int64_t ld_dst, int64_t row_vecs, uint32_t* err) {
+  pdl_wait();  // no early trigger: a waiting dependent CTA would crowd out this grid's own blocks
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -62,6 +63,7 @@ embed_rmsnorm_kernel(const uint32_t* __restrict__ tok, const uint32_t* __restric
                      int64_t n_rows, const __nv_bfloat16* __restrict__ embed, int64_t vocab,
                      int64_t d, const float* __restrict__ w, float eps, float* __restrict__ h,
                      __nv_bfloat16* __restrict__ hn, uint32_t* err) {
+  pdl_wait();  // no early trigger: a waiting dependent CTA would crowd out this grid's own blocks
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(256)
 embed_rows_kernel(const uint32_t* __restrict__ tok, const uint32_t* __restrict__ gather, int64_t n_rows,
                   const __nv_bfloat16* __restrict__ embed, int64_t vocab, int64_t d, float* __restrict__ h,
                   __nv_bfloat16* __restrict__ hb, float* __restrict__ ss_out, uint32_t* err) {
+  pdl_wait();  // no early trigger: a waiting dependent CTA would crowd out this grid's own blocks
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -147,6 +150,7 @@ __global__ void __launch_bounds__(256)
 rmsnorm_rows_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_t* __restrict__ rows,
                     int64_t n_rows, int64_t d, const float* __restrict__ w, float eps,
                     __nv_bfloat16* __restrict__ out, int64_t ld_out) {
+  pdl_wait();  // no early trigger: a waiting dependent CTA would crowd out this grid's own blocks
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -180,6 +184,7 @@ __global__ void __launch_bounds__(256)
 rmsnorm_rows_reg_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_t* __restrict__ rows,
                         int64_t n_rows, const float* __restrict__ w, float eps, __nv_bfloat16* __restrict__ out,
                         int64_t ld_out) {
+  pdl_wait();  // no early trigger: a waiting dependent CTA would crowd out this grid's own blocks
   constexpr int D = 128 * V;
   const int lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -208,6 +213,7 @@ rmsnorm_rows_reg_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_
 
 __global__ void rope_table_kernel(const uint32_t* __restrict__ pos, int64_t n_rows, int half,
                                   double theta, int head_dim, float2* __restrict__ table) {
+  pdl_wait();  // no early trigger: a waiting dependent CTA would crowd out this grid's own blocks
   const int64_t total = n_rows * half;
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -223,6 +229,7 @@ __global__ void rope_table_kernel(const uint32_t* __restrict__ pos, int64_t n_ro
 
 __global__ void rerank_kernel(const float* __restrict__ logits, int64_t n, int64_t ld, int64_t yes,
                               int64_t no, float* __restrict__ out) {
+  pdl_wait();  // no early trigger: a waiting dependent CTA would crowd out this grid's own blocks
   const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b < n) {
     const float z = logits[b * ld + yes] - logits[b * ld + no];
@@ -254,15 +261,15 @@ extern "C" int rdx_gather_rows(const void* src, int64_t src_rows, int64_t ld_src
                           static_cast<uintptr_t>(row_bytes);
   cudaStream_t st = as_stream(stream);
   if ((align & 15) == 0) {
-    gather_rows_kernel<int4, 4><<<grid, 256, 0, st>>>(
+    RDX_LAUNCH_PDL((gather_rows_kernel<int4, 4>), grid, 256, 0, st, 
         static_cast<const char*>(src), src_rows, ld_src_bytes, idx, n_idx, static_cast<char*>(dst),
         ld_dst_bytes, row_bytes / 16, err_flag);
   } else if ((align & 3) == 0) {
-    gather_rows_kernel<uint32_t, 8><<<grid, 256, 0, st>>>(
+    RDX_LAUNCH_PDL((gather_rows_kernel<uint32_t, 8>), grid, 256, 0, st, 
         static_cast<const char*>(src), src_rows, ld_src_bytes, idx, n_idx, static_cast<char*>(dst),
         ld_dst_bytes, row_bytes / 4, err_flag);
   } else {
-    gather_rows_kernel<uint8_t, 8><<<grid, 256, 0, st>>>(
+    RDX_LAUNCH_PDL((gather_rows_kernel<uint8_t, 8>), grid, 256, 0, st, 
         static_cast<const char*>(src), src_rows, ld_src_bytes, idx, n_idx, static_cast<char*>(dst),
         ld_dst_bytes, row_bytes, err_flag);
   }
@@ -277,7 +284,7 @@ extern "C" int rdx_embed_rmsnorm(const uint32_t* tok, const uint32_t* gather, in
   using namespace rdx;
   if (n_rows < 0 || d <= 0 || (d % 8) != 0) return RDX_ERR_SHAPE_MISMATCH;
   if (n_rows == 0) return RDX_OK;
-  embed_rmsnorm_kernel<<<grid_for_rows(n_rows, 8), 256, 0, as_stream(stream)>>>(
+  RDX_LAUNCH_PDL(embed_rmsnorm_kernel, grid_for_rows(n_rows, 8), 256, 0, as_stream(stream), 
       tok, gather, n_rows, static_cast<const __nv_bfloat16*>(embed_bf16), vocab, d, norm_w, eps, h_out,
       static_cast<__nv_bfloat16*>(hn_bf16_out), err_flag);
   RDX_LAUNCH_CHECK();
@@ -291,7 +298,7 @@ extern "C" int rdx_embed_rows(const uint32_t* tok, const uint32_t* gather, int64
   if (n_rows < 0 || d <= 0 || (d % 64) != 0) return RDX_ERR_SHAPE_MISMATCH;
   if (n_rows == 0) return RDX_OK;
   if (!tok || !embed_bf16 || !h_out || !hb_out || !ss_out) return RDX_ERR_INVALID_ARGUMENT;
-  embed_rows_kernel<<<grid_for_rows(n_rows, 8), 256, 0, as_stream(stream)>>>(
+  RDX_LAUNCH_PDL(embed_rows_kernel, grid_for_rows(n_rows, 8), 256, 0, as_stream(stream), 
       tok, gather, n_rows, static_cast<const __nv_bfloat16*>(embed_bf16), vocab, d, h_out,
       static_cast<__nv_bfloat16*>(hb_out), ss_out, err_flag);
   RDX_LAUNCH_CHECK();
@@ -310,14 +317,14 @@ extern "C" int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* ro
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out_bf16);
   const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) == 0;
   switch (aligned ? d : 0) {
-    case 1024: rmsnorm_rows_reg_kernel<8><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
-    case 2048: rmsnorm_rows_reg_kernel<16><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
-    case 2560: rmsnorm_rows_reg_kernel<20><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
-    case 4096: rmsnorm_rows_reg_kernel<32><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
-    case 512: rmsnorm_rows_reg_kernel<4><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
-    case 256: rmsnorm_rows_reg_kernel<2><<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 1024: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<8>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 2048: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<16>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 2560: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<20>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 4096: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<32>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 512: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<4>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 256: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<2>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
     default:
-      rmsnorm_rows_kernel<<<grid, 256, 0, st>>>(x, ld_x, rows, n_rows, d, w, eps, o, ld_out);
+      RDX_LAUNCH_PDL(rmsnorm_rows_kernel, grid, 256, 0, st, x, ld_x, rows, n_rows, d, w, eps, o, ld_out);
   }
   RDX_LAUNCH_CHECK();
   return RDX_OK;
@@ -333,7 +340,7 @@ extern "C" int rdx_rope_table(const uint32_t* pos, int64_t n_rows, int32_t head_
   int64_t total = n_rows * half;
   int64_t g = (total + 255) / 256;
   if (g > num_sms() * 8) g = num_sms() * 8;
-  rope_table_kernel<<<static_cast<int>(g), 256, 0, as_stream(stream)>>>(
+  RDX_LAUNCH_PDL(rope_table_kernel, static_cast<int>(g), 256, 0, as_stream(stream), 
       pos, n_rows, half, theta, head_dim, reinterpret_cast<float2*>(table_out));
   RDX_LAUNCH_CHECK();
   return RDX_OK;
@@ -344,7 +351,7 @@ extern "C" int rdx_rerank_scores(const float* logits, int64_t n_rows, int64_t ld
   using namespace rdx;
   if (n_rows <= 0) return RDX_OK;
   if (yes_id < 0 || no_id < 0 || yes_id >= ld || no_id >= ld) return RDX_ERR_INDEX_OUT_OF_RANGE;
-  rerank_kernel<<<static_cast<int>((n_rows + 127) / 128), 128, 0, as_stream(stream)>>>(
+  RDX_LAUNCH_PDL(rerank_kernel, static_cast<int>((n_rows + 127) / 128), 128, 0, as_stream(stream), 
       logits, n_rows, ld, yes_id, no_id, scores_out);
   RDX_LAUNCH_CHECK();
   return RDX_OK;

@@ -1,0 +1,40 @@
+"""A/B of a library switch on the C2 CUDA-graph step: two models captured with the switch on / off,
+replays interleaved (same box, same clocks).  python scripts/ab_graph.py [pdl|tail]"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2601_15013_b200 import DeviceBatch, DeviceWeights, RadixQwen3, _native  # noqa: E402
+from paper_2601_15013_b200.rerank import RadixReranker  # noqa: E402
+
+what = sys.argv[1] if len(sys.argv) > 1 else "pdl"
+cfg_name = sys.argv[2] if len(sys.argv) > 2 else "c2"
+lib = _native.lib()
+setter = lib.rdx_debug_pdl if what == "pdl" else lib.rdx_gemm_debug_tail_split
+config, _, batch, _ = bench.build_config(cfg_name, 1)
+w = DeviceWeights.random(config, seed=0)
+db = DeviceBatch.from_batch(batch)
+arms = {}
+for on in (1, 0):
+    setter(on)
+    rr = RadixReranker(RadixQwen3(config, w, use_graphs=True))
+    for _ in range(3):
+        rr.score_device(db)  # captures this arm's graph with the switch in this state
+    torch.cuda.synchronize()
+    arms[on] = rr
+flush = bench.L2Flusher()
+res = {1: [], 0: []}
+for it in range(int(os.environ.get("AB_ITERS", "20"))):
+    for on in (1, 0):
+        flush()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        arms[on].score_device(db)
+        e.record()
+        e.synchronize()
+        res[on].append(s.elapsed_time(e))
+med = {k: sorted(v)[len(v) // 2] for k, v in res.items()}
+print(f"{what} on: median {med[1]:.4f} ms   off: median {med[0]:.4f} ms   ({(med[0] / med[1] - 1) * 100:+.1f}% from on)")
