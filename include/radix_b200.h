@@ -157,6 +157,16 @@ int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t
 int rdx_rope_table(const uint32_t* pos, int64_t n_rows, int32_t head_dim, double theta,
                    float* table_out, void* stream);
 
+/* The same values in the QKV epilogue's lane-blocked layout (rdx_gemm_args.
+ * rope_blocked = 1): rows in blocks of 32, column pairs outermost within a
+ * block, so the 32 lanes of a GEMM epilogue warp (32 consecutive rows) read one
+ * contiguous 512 B run per column pair.  (cos, sin) of (row j, column i) sits at
+ * float2 index 2 * (((j / 32) * (hd / 4) + i / 2) * 32 + j % 32) + i % 2;
+ * table_out holds ceil(n_rows / 32) * 32 * hd / 2 float2 (16-byte aligned,
+ * head_dim % 4 == 0). */
+int rdx_rope_table_blocked(const uint32_t* pos, int64_t n_rows, int32_t head_dim, double theta,
+                           float* table_out, void* stream);
+
 /* ---------------------------------------------------------------------
  * tcgen05/TMEM GEMM on sm_100a: acc[m, n] = sum_k A[m, k] * B[n, k]
  * (A [M, K] bf16 row-major = activations, B [N, K] bf16 row-major = weight
@@ -194,7 +204,7 @@ typedef struct rdx_gemm_args {
   /* RDX_EPI_QKV */
   const float* q_norm_w;   /* [head_dim] */
   const float* k_norm_w;   /* [head_dim] */
-  const float* rope_table; /* [M, head_dim/2, 2] (cos, sin) */
+  const float* rope_table; /* [M, head_dim/2, 2] (cos, sin), or the blocked layout */
   int32_t head_dim, q_heads, kv_heads;
   float eps;
   /* Optional RMSNorm of the A rows fused into any epilogue: when row_ss != NULL
@@ -209,6 +219,13 @@ typedef struct rdx_gemm_args {
   void* out_bf16;
   int64_t ldo_bf16;
   float* ss_out;
+  /* RDX_EPI_QKV: 1 = rope_table is in rdx_rope_table_blocked's layout */
+  int32_t rope_blocked;
+  /* RDX_EPI_QKV, head_dim 64 or 128: when rope_pos != NULL the epilogue computes
+   * (cos, sin)(rope_pos[m] * rope_theta^(-2i/head_dim)) itself (fp64 inverse
+   * frequencies, |error| < 1e-6 for positions < 2^20) and rope_table is unused. */
+  const uint32_t* rope_pos;
+  double rope_theta;
 } rdx_gemm_args;
 
 int rdx_gemm(const rdx_gemm_args* args, void* stream);
@@ -217,6 +234,11 @@ int rdx_gemm(const rdx_gemm_args* args, void* stream);
  * narrower tiles (same per-element K reduction, same bits); 0 turns that off
  * for A/B runs, 1 back on.  Returns the previous setting. */
 int rdx_gemm_debug_tail_split(int on);
+
+/* Debug: clock64 role counters of builds made with -DRDX_GEMM_STATS_BUILD (MMA
+ * waits / epilogue waits and busy cycles, see gemm.cu); RDX_ERR_UNSUPPORTED
+ * otherwise.  out8 may be NULL; reset != 0 zeroes the counters. */
+int rdx_gemm_debug_stats(unsigned long long* out8, int reset);
 
 /* Debug: programmatic dependent launch (PDL) of the layer-stack kernels on (1)
  * or off (0) for launches / CUDA-graph captures made after the call (default

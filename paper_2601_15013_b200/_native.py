@@ -35,8 +35,10 @@ EXPORTS = (
     "rdx_embed_rows",
     "rdx_rmsnorm_rows",
     "rdx_rope_table",
+    "rdx_rope_table_blocked",
     "rdx_gemm",
     "rdx_gemm_debug_tail_split",
+    "rdx_gemm_debug_stats",
     "rdx_debug_pdl",
     "rdx_attention",
     "rdx_attention_debug_stats",
@@ -93,6 +95,9 @@ class GemmArgs(ctypes.Structure):
         ("out_bf16", _vp),
         ("ldo_bf16", _i64),
         ("ss_out", _vp),
+        ("rope_blocked", _i32),
+        ("rope_pos", _vp),
+        ("rope_theta", _f64),
     ]
 
 
@@ -116,8 +121,10 @@ _SIGNATURES = {
     "rdx_embed_rows": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "rdx_rmsnorm_rows": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _i64, _vp]),
     "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
+    "rdx_rope_table_blocked": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmArgs), _vp]),
     "rdx_gemm_debug_tail_split": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_gemm_debug_stats": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rdx_debug_pdl": (ctypes.c_int, [ctypes.c_int]),
     "rdx_rerank_scores": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "rdx_attention": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i64,

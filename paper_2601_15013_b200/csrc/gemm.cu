@@ -32,6 +32,23 @@ constexpr int BM = 128;  // rows per CTA
 constexpr int BK = 64;   // 64 bf16 = 128 B = one SWIZZLE_128B atom row
 constexpr int kEpiWarps = 8;   // 2 per TMEM lane quarter, each owning half of the tile's columns
 constexpr int kThreads = 64 + 32 * kEpiWarps;
+
+// Debug build (-DRDX_GEMM_STATS_BUILD): clock64 wait / busy counters per role,
+// read with rdx_gemm_debug_stats.  [0] MMA waits on tempty, [1] MMA waits on
+// full stages, [2] MMA loop total, [3] epilogue waits on tfull (sum over warps),
+// [4] epilogue busy (tfull seen -> accumulator released), [5] epilogue tiles.
+#ifdef RDX_GEMM_STATS_BUILD
+__device__ unsigned long long g_gemm_stats[8];
+#define GST_WAIT(slot, ...)                 \
+  do {                                      \
+    const long long _t = clock64();         \
+    __VA_ARGS__;                            \
+    slot += clock64() - _t;                 \
+  } while (0)
+#else
+#define GST_WAIT(slot, ...) __VA_ARGS__
+#endif
+
 constexpr int kSwigluUnit = 64;     // gate/up interleave unit (columns)
 constexpr int kEpiBoxBytes = 4096;  // staging box: 32 rows x 32 cols (bf16: 64 B rows, f32: 128 B rows)
 
@@ -39,6 +56,9 @@ struct EpiParams {
   const float* qn;
   const float* kn;
   const float2* rope;
+  int rope_ps;  // float2 stride between column pairs: 1 = row-major [M][hd/2], 32 = lane-blocked
+  const uint32_t* rope_pos;  // non-null: (cos, sin) computed in the epilogue from positions
+  double rope_theta;
   int hd, q_dim, kv_dim;
   float eps;
   // fused RMSNorm of the A rows: acc row m *= rsqrt(sum_t row_ss[m*ss_parts+t] / norm_dim + norm_eps)
@@ -73,7 +93,8 @@ struct Cfg {
   // RESID_NORM warps stage two fp32 boxes (h in/out) and two bf16 boxes (hb out)
   static constexpr int EPI_WARP_BYTES = EPI == RDX_EPI_RESID_NORM ? 2 * kEpiBoxBytes + 2 * 2048 : 2 * kEpiBoxBytes;
   static constexpr int EPI_BYTES = kEpiWarps * EPI_WARP_BYTES;
-  static constexpr int AUX_BYTES = 1024;
+  // q/k-norm weights (2 x 128 fp32); QKV adds the RoPE inverse frequencies (64 x (hi, lo) fp32)
+  static constexpr int AUX_BYTES = EPI == RDX_EPI_QKV ? 1536 : 1024;
   static constexpr int BAR_BYTES = 512;
   static constexpr int BUDGET = 227 * 1024 - 1024 - BAR_BYTES - EPI_BYTES - AUX_BYTES;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
@@ -146,13 +167,27 @@ __device__ __forceinline__ void emit_f32x32(EpiWarp<NB>& e, const float* v, cons
   epi_issue(e, map, c0, reduce_add);
 }
 
+// (cos, sin) of pos * inv_freq for one column.  g = inv_freq / (2*pi) in fp64,
+// kept as an fp32 (hi, lo) pair; the angle in turns is pos*g_hi (exact FMA
+// residual) + pos*g_lo, its integer part drops out exactly, and MUFU sin/cos run
+// on the remaining [-1/2, 1/2] turn.  |error| < 1e-6 rad against the fp64 angle
+// for positions < 2^20, far below the bf16 output rounding.
+__device__ __forceinline__ void rope_cs(float pos, float ghi, float glo, float& c, float& s) {
+  const float t = pos * ghi;
+  float e = fmaf(pos, ghi, -t);
+  e = fmaf(pos, glo, e);
+  const float r = (t - rintf(t)) + e;  // t - rint(t) is exact
+  __sincosf(r * 6.283185307179586f, &s, &c);
+}
+
 // RoPE on a (first-half, second-half) pair of 32-column slices of a normalised head:
 // x1 = cols [c, c+32), x2 = cols [c+H, c+H+32) of a head of width 2H (model.py:363-365).
+// cs = this lane's (cos, sin) of column c; column c + j sits at cs + j * ps (j even).
 __device__ __forceinline__ void rope_pair32(float* x1, float* x2, const float* w1, const float* w2, float inv,
-                                            const float2* __restrict__ cs) {
+                                            const float2* __restrict__ cs, int ps) {
 #pragma unroll
   for (int j = 0; j < 32; j += 2) {
-    const float4 t = __ldg(reinterpret_cast<const float4*>(cs + j));
+    const float4 t = __ldg(reinterpret_cast<const float4*>(cs + j * ps));
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const float c = u ? t.z : t.x, s = u ? t.w : t.y;
@@ -168,7 +203,7 @@ __device__ __forceinline__ void rope_pair32(float* x1, float* x2, const float* w
 template <int HD, int NB>
 __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t n0, int c_lo, int c_hi, int64_t N,
                                          const EpiParams& ep, const float* s_qn, const float* s_kn,
-                                         const float2* rope_row, const CUtensorMap* map, float rs) {
+                                         const float2* rope_row, const CUtensorMap* map, float rs, float pos) {
   if constexpr (HD >= 64) {
     constexpr int H = HD / 2;
 #pragma unroll 1
@@ -207,8 +242,34 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
         float x1[32], x2[32];
         tmem_ld32p(taddr + h0 + c, x1);
         tmem_ld32p(taddr + h0 + H + c, x2);
-        tmem_wait_ld();
-        rope_pair32(x1, x2, w + c, w + H + c, inv, rope_row + c);
+        if (ep.rope_pos) {  // (cos, sin) from the position; the math overlaps the TMEM loads
+          float cs[32], sn[32];
+          const uint32_t fq = smem_u32(s_qn + 256);
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float4 f = ld_shared_f4(fq + 8 * (c + j));
+            rope_cs(pos, f.x, f.y, cs[j], sn[j]);
+            rope_cs(pos, f.z, f.w, cs[j + 1], sn[j + 1]);
+          }
+          tmem_wait_ld();
+          const uint32_t ws = smem_u32(w);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 w1 = ld_shared_f4(ws + 4 * (c + j));
+            const float4 w2 = ld_shared_f4(ws + 4 * (H + c + j));
+            const float wa[4] = {w1.x, w1.y, w1.z, w1.w}, wb[4] = {w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float a = x1[j + u] * inv * wa[u];
+              const float b = x2[j + u] * inv * wb[u];
+              x1[j + u] = a * cs[j + u] - b * sn[j + u];
+              x2[j + u] = b * cs[j + u] + a * sn[j + u];
+            }
+          }
+        } else {
+          tmem_wait_ld();
+          rope_pair32(x1, x2, w + c, w + H + c, inv, rope_row + c * ep.rope_ps, ep.rope_ps);
+        }
         emit_bf16x32(e, x1, map, static_cast<int32_t>(col0 + c));
         emit_bf16x32(e, x2, map, static_cast<int32_t>(col0 + H + c));
       }
@@ -237,7 +298,7 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
           constexpr int H = HD / 2;
 #pragma unroll
           for (int j = 0; j < H; ++j) {
-            const float2 cs = __ldg(rope_row + j);
+            const float2 cs = __ldg(rope_row + (j & ~1) * ep.rope_ps + (j & 1));
             const float a = x[h + j] * inv * w[j];
             const float b = x[h + j + H] * inv * w[j + H];
             x[h + j] = a * cs.x - b * cs.y;
@@ -364,13 +425,16 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
     }
   } else if constexpr (EPI == RDX_EPI_QKV) {
     // chunked: TMEM loads interleaved with the norm / RoPE math and the stores
-    const float2* rope_row = ep.rope + r_clamped * (ep.hd >> 1);
+    // row-major: row r at r * hd/2; blocked: ((r/32) * hd/4 * 32 + r%32) float4s
+    const float2* rope_row = ep.rope_ps == 1 ? ep.rope + r_clamped * (ep.hd >> 1)
+                                             : ep.rope + 2 * ((r_clamped >> 5) * (ep.hd >> 2) * 32 + (r_clamped & 31));
     const int c_hi = c_lo + hw;
+    const float pos = ep.rope_pos ? static_cast<float>(__ldg(ep.rope_pos + r_clamped)) : 0.f;
     switch (ep.hd) {
-      case 128: qkv_cols<128>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
-      case 64: qkv_cols<64>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
-      case 32: qkv_cols<32>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
-      default: qkv_cols<16>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs); break;
+      case 128: qkv_cols<128>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
+      case 64: qkv_cols<64>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
+      case 32: qkv_cols<32>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
+      default: qkv_cols<16>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
     }
   }
 }
@@ -454,6 +518,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       s_norm[i] = ep.qn[i];
       s_norm[128 + i] = ep.kn[i];
     }
+    if (ep.rope_pos) {
+      // inv_freq_i = theta^(-2i/hd) in fp64 (model.py:165-172), in turns (/ 2 pi), as an fp32 (hi, lo) pair
+      for (int i = threadIdx.x; i < ep.hd / 2; i += blockDim.x) {
+        const double f = pow(ep.rope_theta, -2.0 * i / static_cast<double>(ep.hd)) * 0.15915494309189533577;
+        const float hi = static_cast<float>(f);
+        s_norm[256 + 2 * i] = hi;
+        s_norm[256 + 2 * i + 1] = static_cast<float>(f - static_cast<double>(hi));
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -504,16 +577,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      long long st_te = 0, st_fu = 0;
+      const long long st_t0 = clock64();
       for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
         int64_t m_blk, n0;
         int width;
         decode(tile, m_blk, n0, width);
         const uint32_t idesc = width == BN ? C::IDESC : (width == BN / 2 ? C::IDESC_HALF : C::IDESC_QUARTER);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        GST_WAIT(st_te, mbar_wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
+          GST_WAIT(st_fu, mbar_wait(&full[stage], phase));
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint64_t da = umma_sdesc_sw128(sa);
@@ -536,6 +611,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+#ifdef RDX_GEMM_STATS_BUILD
+      if (lane == 0) {
+        atomicAdd(&g_gemm_stats[0], static_cast<unsigned long long>(st_te));
+        atomicAdd(&g_gemm_stats[1], static_cast<unsigned long long>(st_fu));
+        atomicAdd(&g_gemm_stats[2], static_cast<unsigned long long>(clock64() - st_t0));
+      }
+#endif
+      (void)st_te;
+      (void)st_fu;
+      (void)st_t0;
     }
   } else {
     const int ew = warp - 2;
@@ -551,6 +636,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     int acc = 0;
     uint32_t acc_phase = 0;
+    long long st_w = 0, st_b = 0, n_t = 0;
     for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
       int64_t m_blk, n0;
       int width;
@@ -559,7 +645,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       // row scale of the fused RMSNorm: its loads overlap the wait for the accumulator
       const int64_t gm = e.row0 + lane;
       const float rs = ep.row_ss ? row_rstd(ep, gm < M ? gm : (M > 0 ? M - 1 : 0)) : 1.f;
-      mbar_wait(&tfull[acc], acc_phase);
+      GST_WAIT(st_w, mbar_wait(&tfull[acc], acc_phase));
+      const long long st_tb = clock64();
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       epilogue_tile<BN, EPI, NB>(e, taddr, ch, width / 2, gm, M, n0, N, ep, s_norm, s_norm + 128, &tmC, &tmD, rs);
@@ -571,8 +658,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      st_b += clock64() - st_tb;
+      ++n_t;
     }
     if (lane == 0) bulk_wait_all();
+#ifdef RDX_GEMM_STATS_BUILD
+    if (lane == 0) {
+      atomicAdd(&g_gemm_stats[3], static_cast<unsigned long long>(st_w));
+      atomicAdd(&g_gemm_stats[4], static_cast<unsigned long long>(st_b));
+      atomicAdd(&g_gemm_stats[5], static_cast<unsigned long long>(n_t));
+    }
+#endif
+    (void)st_w;
+    (void)st_b;
+    (void)n_t;
   }
 
   tc_fence_before();
@@ -665,6 +764,9 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   ep.qn = a.q_norm_w;
   ep.kn = a.k_norm_w;
   ep.rope = reinterpret_cast<const float2*>(a.rope_table);
+  ep.rope_ps = a.rope_blocked ? 32 : 1;
+  ep.rope_pos = a.rope_pos;
+  ep.rope_theta = a.rope_theta;
   ep.hd = a.head_dim;
   ep.q_dim = a.q_heads * a.head_dim;
   ep.kv_dim = a.kv_heads * a.head_dim;
@@ -732,7 +834,6 @@ int dispatch(const rdx_gemm_args& a, int bn, int cg, cudaStream_t s) {
   }
 }
 
-// Pick (CG, BN): fewest tile rounds x tile width, preferring the CTA pair.
 // Pick (CG, BN) minimising tile rounds x per-tile cost.  A 1-CTA tile streams
 // a third more operand bytes per FLOP than the pair tile, hence the penalty.
 // RDX_GEMM_SHAPE="cg,bn" (env) pins the choice for experiments.
@@ -757,8 +858,12 @@ void choose_shape(const rdx_gemm_args& a, int* bn_out, int* cg_out) {
       if (a.epi == RDX_EPI_QKV && ((bn / 2) % a.head_dim) && a.head_dim > 32) continue;
       const int64_t tiles = ((a.m + BM * cg - 1) / (BM * cg)) * ((a.n + bn - 1) / bn);
       const int64_t units = num_sms() / cg;
-      const int64_t rounds = (tiles + units - 1) / units;
-      const double cost = static_cast<double>(rounds) * (bn + 64) * (cg == 1 ? 1.15 : 1.0);
+      // a partial last round costs about a quarter of a full one per missing tile
+      // (measured: the few busy SMs clock up under the power cap), so rounds are
+      // counted fractionally plus a 0.25 penalty on the idle share
+      const double frac = static_cast<double>(tiles) / static_cast<double>(units);
+      const double rounds = frac + 0.25 * (static_cast<double>((tiles + units - 1) / units) - frac);
+      const double cost = rounds * (bn + 64) * (cg == 1 ? 1.15 : 1.0);
       if (cost < best_cost) {
         best_cost = cost;
         best_bn = bn;
@@ -820,7 +925,12 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
     case RDX_EPI_QKV: {
       if (a.head_dim > 32 && (bn / 2) % a.head_dim) return RDX_ERR_SHAPE_MISMATCH;
       if (a.n != static_cast<int64_t>(a.q_heads + 2 * a.kv_heads) * a.head_dim) return RDX_ERR_SHAPE_MISMATCH;
-      if (!a.q_norm_w || !a.k_norm_w || !a.rope_table) return RDX_ERR_INVALID_ARGUMENT;
+      if (!a.q_norm_w || !a.k_norm_w) return RDX_ERR_INVALID_ARGUMENT;
+      if (a.rope_pos) {
+        if ((a.head_dim != 64 && a.head_dim != 128) || !(a.rope_theta > 0.0)) return RDX_ERR_INVALID_ARGUMENT;
+      } else if (!a.rope_table) {
+        return RDX_ERR_INVALID_ARGUMENT;
+      }
       if (a.ldo % 8 || a.ldo < a.n) return RDX_ERR_SHAPE_MISMATCH;
       return dispatch<RDX_EPI_QKV>(a, bn, cg, s);
     }
@@ -830,6 +940,22 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
 }
 
 // Debug: switch the GEMM tail split on (1) / off (0); returns the previous setting.
+extern "C" int rdx_gemm_debug_stats(unsigned long long* out8, int reset) {
+#ifdef RDX_GEMM_STATS_BUILD
+  if (out8 && cudaMemcpyFromSymbol(out8, rdx::gemm::g_gemm_stats, sizeof(unsigned long long) * 8) != cudaSuccess)
+    return RDX_ERR_CUDA;
+  if (reset) {
+    const unsigned long long z[8] = {};
+    if (cudaMemcpyToSymbol(rdx::gemm::g_gemm_stats, z, sizeof(z)) != cudaSuccess) return RDX_ERR_CUDA;
+  }
+  return RDX_OK;
+#else
+  (void)out8;
+  (void)reset;
+  return RDX_ERR_UNSUPPORTED;
+#endif
+}
+
 extern "C" int rdx_gemm_debug_tail_split(int on) {
   const int prev = rdx::gemm::tail_split_enabled() ? 1 : 0;
   rdx::gemm::g_tail_split = on ? 1 : 0;

@@ -211,8 +211,10 @@ rmsnorm_rows_reg_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_
   }
 }
 
+// blocked = 0: table[j][i]; blocked = 1: the QKV epilogue's lane-coalesced layout
+// (see rdx_rope_table_blocked): float2 (j, i) at 2*(((j/32)*(half/2) + i/2)*32 + j%32) + i%2.
 __global__ void rope_table_kernel(const uint32_t* __restrict__ pos, int64_t n_rows, int half,
-                                  double theta, int head_dim, float2* __restrict__ table) {
+                                  double theta, int head_dim, int blocked, float2* __restrict__ table) {
   pdl_wait();  // no early trigger: a waiting dependent CTA would crowd out this grid's own blocks
   const int64_t total = n_rows * half;
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
@@ -223,7 +225,8 @@ __global__ void rope_table_kernel(const uint32_t* __restrict__ pos, int64_t n_ro
     const double ang = static_cast<double>(pos[j]) * inv_freq;
     double sn, cs;
     sincos(ang, &sn, &cs);
-    table[t] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
+    const int64_t o = blocked ? 2 * (((j >> 5) * (half >> 1) + (i >> 1)) * 32 + (j & 31)) + (i & 1) : t;
+    table[o] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
   }
 }
 
@@ -330,20 +333,40 @@ extern "C" int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* ro
   return RDX_OK;
 }
 
+namespace rdx {
+namespace {
+int rope_table_launch(const uint32_t* pos, int64_t n_rows, int32_t head_dim, double theta, int blocked,
+                      float* table_out, void* stream) {
+  const int half = head_dim / 2;
+  int64_t total = n_rows * half;
+  int64_t g = (total + 255) / 256;
+  if (g > num_sms() * 8) g = num_sms() * 8;
+  RDX_LAUNCH_PDL(rope_table_kernel, static_cast<int>(g), 256, 0, as_stream(stream), 
+      pos, n_rows, half, theta, head_dim, blocked, reinterpret_cast<float2*>(table_out));
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}
+}  // namespace
+}  // namespace rdx
+
 extern "C" int rdx_rope_table(const uint32_t* pos, int64_t n_rows, int32_t head_dim, double theta,
                               float* table_out, void* stream) {
   using namespace rdx;
   if (head_dim <= 0) return RDX_ERR_SHAPE_MISMATCH;
   if (head_dim % 2) return RDX_ERR_ODD_HEAD_DIM;
   if (n_rows <= 0) return RDX_OK;
-  const int half = head_dim / 2;
-  int64_t total = n_rows * half;
-  int64_t g = (total + 255) / 256;
-  if (g > num_sms() * 8) g = num_sms() * 8;
-  RDX_LAUNCH_PDL(rope_table_kernel, static_cast<int>(g), 256, 0, as_stream(stream), 
-      pos, n_rows, half, theta, head_dim, reinterpret_cast<float2*>(table_out));
-  RDX_LAUNCH_CHECK();
-  return RDX_OK;
+  return rope_table_launch(pos, n_rows, head_dim, theta, 0, table_out, stream);
+}
+
+extern "C" int rdx_rope_table_blocked(const uint32_t* pos, int64_t n_rows, int32_t head_dim, double theta,
+                                      float* table_out, void* stream) {
+  using namespace rdx;
+  if (head_dim <= 0) return RDX_ERR_SHAPE_MISMATCH;
+  if (head_dim % 2) return RDX_ERR_ODD_HEAD_DIM;
+  if (head_dim % 4) return RDX_ERR_SHAPE_MISMATCH;
+  if (n_rows <= 0) return RDX_OK;
+  if (reinterpret_cast<uintptr_t>(table_out) & 15) return RDX_ERR_INVALID_ARGUMENT;
+  return rope_table_launch(pos, n_rows, head_dim, theta, 1, table_out, stream);
 }
 
 extern "C" int rdx_rerank_scores(const float* logits, int64_t n_rows, int64_t ld, int64_t yes_id,

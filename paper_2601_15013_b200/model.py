@@ -386,7 +386,12 @@ class RadixQwen3:
         if qkv:
             args.q_norm_w = self.w.t[layer + "q_norm"].data_ptr()
             args.k_norm_w = self.w.t[layer + "k_norm"].data_ptr()
-            args.rope_table = rope.data_ptr()
+            if rope[0] == "pos":  # (cos, sin) computed in the epilogue from the row positions
+                args.rope_pos = rope[1].data_ptr()
+                args.rope_theta = float(cfg.rope_theta)
+            else:  # lane-blocked fp64-derived table
+                args.rope_table = rope[1].data_ptr()
+                args.rope_blocked = 1
             args.head_dim = cfg.head_dim
             args.q_heads = cfg.num_heads
             args.kv_heads = cfg.num_kv_heads
@@ -598,13 +603,18 @@ class RadixQwen3:
         self._op("embed_rmsnorm", embed)
         resid_epi = _native.EPI_RESID_NORM if fused else _native.EPI_RESID_F32
         sfx = "_n" if fused else ""
-        rope = torch.empty(m, hd // 2, 2, dtype=torch.float32, device=dev)
+        if hd in (64, 128):
+            rope = ("pos", positions)  # the QKV epilogue computes (cos, sin) itself: no table pass
+        else:
+            # lane-blocked (cos, sin) table: the QKV epilogue's 32 lanes read contiguous runs
+            table = torch.empty(-(-m // 32) * 32 * (hd // 2) * 2, dtype=torch.float32, device=dev)
+            rope = ("table", table)
 
-        def rope_fn():
-            _native.check(lib.rdx_rope_table(positions.data_ptr(), m, hd, float(cfg.rope_theta), rope.data_ptr(),
-                                             st), "rdx_rope_table")
+            def rope_fn():
+                _native.check(lib.rdx_rope_table_blocked(positions.data_ptr(), m, hd, float(cfg.rope_theta),
+                                                         table.data_ptr(), st), "rdx_rope_table_blocked")
 
-        self._op("rope_table", rope_fn)
+            self._op("rope_table", rope_fn)
         qkv = torch.empty(m, qd + 2 * kvd, dtype=bf, device=dev)
         act = torch.empty(m, self.di_pad, dtype=bf, device=dev)
         attn_out = torch.empty(m, qd, dtype=bf, device=dev)

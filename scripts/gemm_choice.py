@@ -1,0 +1,54 @@
+"""Time every C2/C3/C4 GEMM (compact M) under the current RDX_GEMM_SHAPE (unset = auto choice)."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2601_15013_b200 import _native  # noqa: E402
+from paper_2601_15013_b200.model import SWIGLU_UNIT  # noqa: E402
+from scripts.gemm_epi_bench_lib import gemm  # noqa: E402
+
+CONFIGS = {"c2": (7024, 1024, 3072, 16, 8), "c2nd": (11056, 1024, 3072, 16, 8), "c3": (28168, 2560, 9728, 32, 8),
+           "c4": (34816, 4096, 12288, 32, 8)}
+bf = torch.bfloat16
+hd = 128
+
+
+def t(fn, it=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(it):
+        fn()
+    e.record()
+    e.synchronize()
+    return s.elapsed_time(e) / it * 1e3
+
+
+out = []
+for name, (M, d, di, H, KV) in CONFIGS.items():
+    di_pad = -(-di // SWIGLU_UNIT) * SWIGLU_UNIT
+    a = torch.randn(M, max(d, di_pad, H * hd), device="cuda").to(bf)
+    wqkv = (torch.randn((H + 2 * KV) * hd, d, device="cuda") * 0.05).to(bf)
+    qkv = torch.empty(M, (H + 2 * KV) * hd, dtype=bf, device="cuda")
+    qn = torch.ones(hd, device="cuda")
+    pos = torch.randint(0, 2048, (M,), device="cuda", dtype=torch.int32)
+    wgu = (torch.randn(2 * di_pad, d, device="cuda") * 0.05).to(bf)
+    act = torch.empty(M, di_pad, dtype=bf, device="cuda")
+    wo = (torch.randn(d, H * hd, device="cuda") * 0.05).to(bf)
+    wd = (torch.randn(d, di_pad, device="cuda") * 0.05).to(bf)
+    h = torch.zeros(M, d, device="cuda")
+    ad, ah, ai = a[:, :d], a[:, :H * hd], a[:, :di_pad]
+    res = {
+        "qkv": t(gemm(ad, wqkv, _native.EPI_QKV, qkv, q_norm_w=qn.data_ptr(), k_norm_w=qn.data_ptr(),
+                      rope_pos=pos.data_ptr(), rope_theta=1e6, head_dim=hd, q_heads=H, kv_heads=KV, eps=1e-6)),
+        "gate_up": t(gemm(ad, wgu, _native.EPI_SWIGLU, act)),
+        "o_proj": t(gemm(ah, wo, _native.EPI_RESID_F32, h)),
+        "down": t(gemm(ai, wd, _native.EPI_RESID_F32, h)),
+    }
+    out.append(f"{name}: " + "  ".join(f"{k} {v:7.1f}" for k, v in res.items()) + f"  sum {sum(res.values()):7.1f}")
+print(f"[{os.environ.get('RDX_GEMM_SHAPE', 'auto')}]")
+print("\n".join(out), flush=True)

@@ -6,22 +6,9 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_15013_b200 import _native  # noqa: E402
+from scripts.gemm_epi_bench_lib import gemm  # noqa: E402
 
 M = int(os.environ.get("M", "7024"))
-
-
-def gemm(a, w, epi, out, bn=0, **kw):
-    args = _native.GemmArgs()
-    args.a, args.b = a.data_ptr(), w.data_ptr()
-    args.m, args.n, args.k = a.shape[0], w.shape[0], w.shape[1]
-    args.lda, args.ldb = a.stride(0), w.stride(0)
-    args.epi, args.block_n = epi, bn
-    args.out, args.ldo = out.data_ptr(), out.stride(0)
-    for k, v in kw.items():
-        setattr(args, k, v)
-    lib = _native.lib()
-    st = _native.stream_handle()
-    return lambda: _native.check(lib.rdx_gemm(args, st), "rdx_gemm")
 
 
 def t(fn, it=50):
@@ -49,8 +36,16 @@ for bn in (0,):
     us_store = t(gemm(a, wqkv, _native.EPI_STORE_BF16, qkv, bn))
     us_qkv = t(gemm(a, wqkv, _native.EPI_QKV, qkv, bn, q_norm_w=qn.data_ptr(), k_norm_w=qn.data_ptr(),
                     rope_table=rope.data_ptr(), head_dim=hd, q_heads=H, kv_heads=KV, eps=1e-6))
+    rope_bl = torch.randn(-(-M // 32) * 32 * hd, device="cuda")
+    us_bl = t(gemm(a, wqkv, _native.EPI_QKV, qkv, bn, q_norm_w=qn.data_ptr(), k_norm_w=qn.data_ptr(),
+                   rope_table=rope_bl.data_ptr(), rope_blocked=1, head_dim=hd, q_heads=H, kv_heads=KV, eps=1e-6))
+    posd = torch.randint(0, 2048, (M,), device="cuda", dtype=torch.int32)
+    us_pos = t(gemm(a, wqkv, _native.EPI_QKV, qkv, bn, q_norm_w=qn.data_ptr(), k_norm_w=qn.data_ptr(),
+                    rope_pos=posd.data_ptr(), rope_theta=1e6, head_dim=hd, q_heads=H, kv_heads=KV, eps=1e-6))
+    print(f"  rope from positions {us_pos:.1f} us ({fl / us_pos / 1e6:.0f} TF/s)", flush=True)
     print(f"qkv shape M={M}: store_bf16 {us_store:.1f} us ({fl / us_store / 1e6:.0f} TF/s)  "
-          f"EPI_QKV {us_qkv:.1f} us ({fl / us_qkv / 1e6:.0f} TF/s)", flush=True)
+          f"EPI_QKV {us_qkv:.1f} us ({fl / us_qkv / 1e6:.0f} TF/s)  "
+          f"blocked rope {us_bl:.1f} us ({fl / us_bl / 1e6:.0f} TF/s)", flush=True)
 wgu = (torch.randn(2 * di, d, device="cuda") * 0.05).to(bf)
 act = torch.empty(M, di, dtype=bf, device="cuda")
 gu = torch.empty(M, 2 * di, dtype=bf, device="cuda")

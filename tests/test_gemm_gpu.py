@@ -26,6 +26,9 @@ def _gemm(a, w, epi, out, block_n=0, **qkv):
         args.q_norm_w = qkv["qn"].data_ptr()
         args.k_norm_w = qkv["kn"].data_ptr()
         args.rope_table = qkv["rope"].data_ptr()
+        args.rope_blocked = int(qkv.get("blocked", 0))
+        if qkv.get("pos") is not None:
+            args.rope_pos, args.rope_theta = qkv["pos"].data_ptr(), qkv.get("theta", 1e6)
         args.head_dim, args.q_heads, args.kv_heads = qkv["hd"], qkv["H"], qkv["KV"]
         args.eps = qkv["eps"]
     _native.check(_native.lib().rdx_gemm(args, _native.stream_handle()), "rdx_gemm")
@@ -140,6 +143,98 @@ def test_qkv_norm_rope(hd, H, KV):
     ref = torch.cat([q, k, v], 1)
     err = (out.float() - ref).abs().max().item()
     assert err <= 2e-2 * ref.abs().max().item(), err
+
+
+def _blocked_rope(pos, hd, theta=1e6):
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    m = pos.shape[0]
+    t = torch.full((-(-m // 32) * 32 * (hd // 2) * 2,), float("nan"), device="cuda")
+    _native.check(_native.lib().rdx_rope_table_blocked(pos.data_ptr(), m, hd, theta, t.data_ptr(),
+                                                       _native.stream_handle()), "rope_blocked")
+    return t
+
+
+@pytest.mark.parametrize("m,hd", [(1, 16), (45, 64), (300, 128), (4097, 128)])
+def test_rope_table_blocked_layout(m, hd):
+    """rdx_rope_table_blocked holds rdx_rope_table's values at the documented indices."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    pos = torch.randint(0, 40000, (m,), device="cuda", dtype=torch.int32)
+    rm = torch.empty(m, hd // 2, 2, device="cuda")
+    _native.check(_native.lib().rdx_rope_table(pos.data_ptr(), m, hd, 1e6, rm.data_ptr(),
+                                               _native.stream_handle()), "rope")
+    bl = _blocked_rope(pos, hd).view(-1, 2)
+    j = torch.arange(m, device="cuda")[:, None]
+    i = torch.arange(hd // 2, device="cuda")[None, :]
+    idx = 2 * (((j // 32) * (hd // 4) + i // 2) * 32 + j % 32) + i % 2
+    assert torch.equal(bl[idx.reshape(-1)].view(m, hd // 2, 2), rm)
+
+
+@pytest.mark.parametrize("m,hd,H,KV", [(300, 128, 16, 8), (7024, 128, 16, 8), (77, 16, 4, 2), (129, 64, 4, 2),
+                                       (1000, 32, 6, 2)])
+def test_qkv_blocked_rope_bit_identical(m, hd, H, KV):
+    """The lane-blocked RoPE table gives the same bits as the row-major one."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    d = 256
+    a = _rand(m, d, 12)
+    n = (H + 2 * KV) * hd
+    w = _rand(n, d, 13, 0.2)
+    qn = torch.rand(hd, device="cuda") + 0.5
+    kn = torch.rand(hd, device="cuda") + 0.5
+    pos = torch.randint(0, 4000, (m,), device="cuda", dtype=torch.int32)
+    rope = torch.empty(m, hd // 2, 2, device="cuda")
+    _native.check(_native.lib().rdx_rope_table(pos.data_ptr(), m, hd, 1e6, rope.data_ptr(),
+                                               _native.stream_handle()), "rope")
+    out_rm = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    out_bl = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    kw = dict(qn=qn, kn=kn, hd=hd, H=H, KV=KV, eps=1e-6)
+    _gemm(a, w, _native.EPI_QKV, out_rm, 0, rope=rope, **kw)
+    _gemm(a, w, _native.EPI_QKV, out_bl, 0, rope=_blocked_rope(pos, hd), blocked=1, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(out_rm, out_bl)
+
+
+@pytest.mark.parametrize("m,hd,H,KV,maxpos", [(300, 128, 16, 8, 4000), (7024, 128, 16, 8, 40000),
+                                              (129, 64, 4, 2, 1 << 20), (1000, 64, 6, 2, 300)])
+def test_qkv_rope_from_positions(m, hd, H, KV, maxpos):
+    """(cos, sin) computed in the epilogue from positions: same result as the fp64-derived
+    table within the bf16 output rounding (|angle error| < 1e-6 by construction)."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    d = 256
+    a = _rand(m, d, 14)
+    n = (H + 2 * KV) * hd
+    w = _rand(n, d, 15, 0.2)
+    qn = torch.rand(hd, device="cuda") + 0.5
+    kn = torch.rand(hd, device="cuda") + 0.5
+    pos = torch.randint(0, maxpos, (m,), device="cuda", dtype=torch.int32)
+    pos[0] = maxpos - 1
+    rope = torch.empty(m, hd // 2, 2, device="cuda")
+    _native.check(_native.lib().rdx_rope_table(pos.data_ptr(), m, hd, 1e6, rope.data_ptr(),
+                                               _native.stream_handle()), "rope")
+    kw = dict(qn=qn, kn=kn, hd=hd, H=H, KV=KV, eps=1e-6)
+    out_t = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    out_p = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    _gemm(a, w, _native.EPI_QKV, out_t, 0, rope=rope, **kw)
+    _gemm(a, w, _native.EPI_QKV, out_p, 0, rope=rope, pos=pos, theta=1e6, **kw)
+    torch.cuda.synchronize()
+    t, p = out_t.float(), out_p.float()
+    # v columns never see RoPE: bit-identical
+    assert torch.equal(out_t[:, (H + KV) * hd:], out_p[:, (H + KV) * hd:])
+    # q/k: at most one bf16 rounding step apart (2^-8 relative), almost always equal
+    diff = (t - p).abs()
+    assert (diff <= t.abs() * 2.0 ** -7 + 1e-6).all(), diff.max().item()
+    assert (diff == 0).float().mean().item() > 0.95
 
 
 def test_gemm_error_codes():
