@@ -311,6 +311,17 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
   }
 }
 
+// RDX_EPI_RESID_NORM: TMA loads of the warp's first two 32-column h chunks, issued
+// before the accumulator wait so their latency overlaps the mainloop.
+template <int NB>
+__device__ __forceinline__ void resid_norm_prefetch(EpiWarp<NB>& e, const CUtensorMap* map, int64_t c0, int64_t N) {
+  if (e.lane == 0 && c0 < N) {
+    bulk_wait_read<0>();  // the previous tile's stores are done reading the boxes
+    mbar_arrive_expect_tx(&e.lbar[0], 2 * kEpiBoxBytes);
+    tma_load_3d(map, e.base, &e.lbar[0], 0, e.row0, static_cast<int32_t>(c0 / 32));
+  }
+}
+
 // This warp: 32 rows (lane quarter) x columns [ch*BN/2, (ch+1)*BN/2) of the tile.
 // All of the warp's accumulator columns are read from TMEM with one wait,
 // then transformed in registers and emitted box by box.
@@ -344,60 +355,58 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
   const int64_t r_clamped = gm_lane < M ? gm_lane : (M > 0 ? M - 1 : 0);
   if constexpr (EPI != RDX_EPI_QKV) tmem_wait_ld();
   if constexpr (EPI == RDX_EPI_RESID_NORM) {
-    // h tile (32 rows x 32 fp32 columns per chunk) comes in by TMA into an fp32 box,
-    // each lane adds its accumulator row, writes h_new back into the box and
-    // bf16(h_new) into a bf16 box, and both go out by TMA store; the partial sum
-    // of h_new^2 per 64 columns goes to ss_out.  Loads run one chunk ahead.
-    const int CHUNKS = hw / 32;
-    auto fbox = [&](int i) { return e.base + (i & 1) * kEpiBoxBytes; };
-    auto bbox = [&](int i) { return e.base + 2 * kEpiBoxBytes + (i & 1) * 2048; };
-    auto load = [&](int i) {
-      if (e.lane == 0) {
-        bulk_wait_read<0>();  // the stores that last read these boxes are done with them
-        mbar_arrive_expect_tx(&e.lbar[i & 1], kEpiBoxBytes);
-        tma_load_2d(map, fbox(i), &e.lbar[i & 1], static_cast<int32_t>(n0 + c_lo + 32 * i), e.row0);
+    // 64-column steps: one 8 KB TMA load of h (two stacked 32x32 fp32 swizzled boxes,
+    // 3-D map), each lane adds its accumulator row, writes h_new back into the box and
+    // bf16(h_new) into a 4 KB 32x64 bf16 box, and both go out as one TMA store each;
+    // the sum of h_new^2 over the 64 columns goes to ss_out.  Step 0's load was issued
+    // before the accumulator wait (resid_norm_prefetch); later steps reuse the boxes
+    // once the previous step's stores have read them.
+    uint8_t* fb8 = e.base;
+    uint8_t* bb8 = e.base + 2 * kEpiBoxBytes;
+#pragma unroll
+    for (int g = 0; g < HALF / 64; ++g) {
+      const int64_t col = n0 + c_lo + 64 * g;
+      if (64 * g >= hw || col >= N) break;
+      if (g > 0 && e.lane == 0) {
+        bulk_wait_read<0>();
+        mbar_arrive_expect_tx(&e.lbar[0], 2 * kEpiBoxBytes);
+        tma_load_3d(map, fb8, &e.lbar[0], 0, e.row0, static_cast<int32_t>(col / 32));
       }
-    };
-    load(0);
-    float ssp = 0.f;
+      mbar_wait(&e.lbar[0], e.lphase & 1);
+      e.lphase ^= 1u;
+      float ssp = 0.f;
+      const uint32_t bb = smem_u32(bb8) + e.lane * 128;
 #pragma unroll
-    for (int i = 0; i < HALF / 32; ++i) {
-      if (i >= CHUNKS) break;
-      const int64_t col = n0 + c_lo + 32 * i;
-      if (i + 1 < CHUNKS && col + 32 < N) load(i + 1);
-      if (col >= N) break;
-      mbar_wait(&e.lbar[i & 1], (e.lphase >> (i & 1)) & 1);
-      e.lphase ^= 1u << (i & 1);
-      const uint32_t fb = smem_u32(fbox(i)) + e.lane * 128;
-      const uint32_t bb = smem_u32(bbox(i)) + e.lane * 64;
-      uint32_t w[16];
+      for (int c = 0; c < 2; ++c) {
+        const uint32_t fb = smem_u32(fb8) + c * kEpiBoxBytes + e.lane * 128;
+        uint32_t w[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t addr = fb + ((j ^ (e.lane & 7)) << 4);
-        float4 hv = ld_shared_f4(addr);
-        hv.x += v[32 * i + 4 * j];
-        hv.y += v[32 * i + 4 * j + 1];
-        hv.z += v[32 * i + 4 * j + 2];
-        hv.w += v[32 * i + 4 * j + 3];
-        ssp += hv.x * hv.x + hv.y * hv.y + hv.z * hv.z + hv.w * hv.w;
-        st_shared_v4(addr, __float_as_uint(hv.x), __float_as_uint(hv.y), __float_as_uint(hv.z), __float_as_uint(hv.w));
-        w[2 * j] = pack_bf16x2(hv.x, hv.y);
-        w[2 * j + 1] = pack_bf16x2(hv.z, hv.w);
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t addr = fb + ((j ^ (e.lane & 7)) << 4);
+          float4 hv = ld_shared_f4(addr);
+          const float* a = v + 64 * g + 32 * c + 4 * j;
+          hv.x += a[0];
+          hv.y += a[1];
+          hv.z += a[2];
+          hv.w += a[3];
+          ssp += hv.x * hv.x + hv.y * hv.y + hv.z * hv.z + hv.w * hv.w;
+          st_shared_v4(addr, __float_as_uint(hv.x), __float_as_uint(hv.y), __float_as_uint(hv.z), __float_as_uint(hv.w));
+          w[2 * j] = pack_bf16x2(hv.x, hv.y);
+          w[2 * j + 1] = pack_bf16x2(hv.z, hv.w);
+        }
+        // bf16 row of 128 B = 8 chunks of 16 B; this c fills chunks 4c .. 4c+3
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          st_shared_v4(bb + (((4 * c + j) ^ (e.lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
       }
-      const int sw = (e.lane >> 1) & 3;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) st_shared_v4(bb + ((j ^ sw) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
       fence_proxy_async_smem();
       __syncwarp();
       if (e.lane == 0) {
-        tma_store_2d(map, fbox(i), static_cast<int32_t>(col), e.row0);
-        tma_store_2d(map_hb, bbox(i), static_cast<int32_t>(col), e.row0);
+        tma_store_3d(map, fb8, 0, e.row0, static_cast<int32_t>(col / 32));
+        tma_store_2d(map_hb, bb8, static_cast<int32_t>(col), e.row0);
         bulk_commit();
       }
-      if ((i & 1) == 1) {  // end of a 64-column group
-        if (gm_lane < M) ep.ss_out[gm_lane * ep.ss_out_parts + col / kNormGroup] = ssp;
-        ssp = 0.f;
-      }
+      if (gm_lane < M) ep.ss_out[gm_lane * ep.ss_out_parts + col / kNormGroup] = ssp;
     }
   } else if constexpr (EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
 #pragma unroll
@@ -645,6 +654,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       // row scale of the fused RMSNorm: its loads overlap the wait for the accumulator
       const int64_t gm = e.row0 + lane;
       const float rs = ep.row_ss ? row_rstd(ep, gm < M ? gm : (M > 0 ? M - 1 : 0)) : 1.f;
+      if constexpr (EPI == RDX_EPI_RESID_NORM) resid_norm_prefetch(e, &tmC, n0 + ch * (width / 2), N);
       GST_WAIT(st_w, mbar_wait(&tfull[acc], acc_phase));
       const long long st_tb = clock64();
       tc_fence_after();
@@ -717,6 +727,25 @@ int make_map(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* pt
   return r == CUDA_SUCCESS ? RDX_OK : RDX_ERR_INVALID_ARGUMENT;
 }
 
+// 3-D view [blocks][outer][inner] of a row-major matrix whose column blocks of
+// `inner` elements are stacked: dims {inner, outer, blocks}, strides {ld, inner}
+// (bytes), 128B swizzle; a {inner, box_outer, box_blocks} box lands in smem as
+// box_blocks consecutive [box_outer][inner] swizzled boxes.
+int make_map_3d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* ptr, int64_t inner, int64_t outer,
+                int64_t blocks, int64_t ld_elems, int box_inner, int box_outer, int box_blocks) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return RDX_ERR_UNSUPPORTED;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer),
+                        static_cast<cuuint64_t>(blocks)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld_elems) * esize, static_cast<cuuint64_t>(inner) * esize};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer),
+                       static_cast<cuuint32_t>(box_blocks)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, dt, 3, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? RDX_OK : RDX_ERR_INVALID_ARGUMENT;
+}
+
 // RDX_GEMM_TAIL_SPLIT=0 (env) or rdx_gemm_debug_tail_split(0) disables the tail split (A/B runs).
 int g_tail_split = -1;
 bool tail_split_enabled() {
@@ -747,7 +776,10 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   if (st) return st;
   st = make_map(&mb4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, C::B_ROWS / 4);
   if (st) return st;
-  if (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32 || EPI == RDX_EPI_RESID_NORM) {
+  if (EPI == RDX_EPI_RESID_NORM) {
+    // [col blocks of 32][rows][32 cols] view: a box of {32, 32, 2} = two stacked swizzled 32x32 boxes
+    st = make_map_3d(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.out, 32, a.m, a.n / 32, a.ldo, 32, 32, 2);
+  } else if (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32) {
     st = make_map(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.out, a.n, a.m, a.ldo, 32, 32);
   } else {
     const int64_t ncols = EPI == RDX_EPI_SWIGLU ? a.n / 2 : a.n;
@@ -756,8 +788,7 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   }
   if (st) return st;
   if (EPI == RDX_EPI_RESID_NORM) {
-    st = make_map(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.out_bf16, a.n, a.m, a.ldo_bf16, 32, 32,
-                  CU_TENSOR_MAP_SWIZZLE_64B);
+    st = make_map(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.out_bf16, a.n, a.m, a.ldo_bf16, 64, 32);
     if (st) return st;
   }
   EpiParams ep;

@@ -196,7 +196,11 @@ rmsnorm_rows_reg_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
+#ifdef RDX_RMS_LDG
+      v[i] = __ldg(xr + lane + 32 * i);
+#else
       v[i] = __ldcs(xr + lane + 32 * i);
+#endif
       ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
     }
     ss = warp_sum(ss);

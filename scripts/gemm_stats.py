@@ -18,16 +18,34 @@ out = torch.empty(M, (H + 2 * KV) * hd, dtype=bf, device="cuda")
 qn = torch.ones(hd, device="cuda")
 pos = torch.randint(0, 2048, (M,), device="cuda", dtype=torch.int32)
 V = os.environ.get("VARIANT", "pos")
-fn = gemm(a, w, _native.EPI_STORE_BF16, out) if V == "store" else gemm(a, w, _native.EPI_QKV, out, q_norm_w=qn.data_ptr(), k_norm_w=qn.data_ptr(), rope_pos=pos.data_ptr(),
+if V in ("resid", "residnorm"):  # o_proj shape: K = H * hd, N = d
+    ao = torch.randn(M, H * hd, device="cuda").to(bf)
+    wo = (torch.randn(d, H * hd, device="cuda") * 0.05).to(bf)
+    hres = torch.zeros(M, d, device="cuda")
+    hb = torch.empty(M, d, dtype=bf, device="cuda")
+    ss = torch.empty(M, d // 64, device="cuda")
+    if V == "resid":
+        fn = gemm(ao, wo, _native.EPI_RESID_F32, hres)
+    else:
+        fn = gemm(ao, wo, _native.EPI_RESID_NORM, hres, out_bf16=hb.data_ptr(), ldo_bf16=hb.stride(0),
+                  ss_out=ss.data_ptr())
+elif V == "store":
+    fn = gemm(a, w, _native.EPI_STORE_BF16, out)
+else:
+    fn = gemm(a, w, _native.EPI_QKV, out, q_norm_w=qn.data_ptr(), k_norm_w=qn.data_ptr(), rope_pos=pos.data_ptr(),
           rope_theta=1e6, head_dim=hd, q_heads=H, kv_heads=KV, eps=1e-6)
 lib = _native.lib()
 fn()
 torch.cuda.synchronize()
 lib.rdx_gemm_debug_stats(None, 1)
 it = 20
+s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s_ev.record()
 for _ in range(it):
     fn()
+e_ev.record()
 torch.cuda.synchronize()
+print(f"{V}: {s_ev.elapsed_time(e_ev) / it * 1e3:.1f} us per launch")
 st = (ctypes.c_ulonglong * 8)()
 _native.check(lib.rdx_gemm_debug_stats(st, 0), "stats")
 st = list(st)
