@@ -196,11 +196,7 @@ rmsnorm_rows_reg_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-#ifdef RDX_RMS_LDG
-      v[i] = __ldg(xr + lane + 32 * i);
-#else
       v[i] = __ldcs(xr + lane + 32 * i);
-#endif
       ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
     }
     ss = warp_sum(ss);
@@ -211,6 +207,51 @@ rmsnorm_rows_reg_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_
       const float4 g = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * i);
       orow[lane + 32 * i] = make_uint2(pack_bf16x2(v[i].x * inv * g.x, v[i].y * inv * g.y),
                                        pack_bf16x2(v[i].z * inv * g.z, v[i].w * inv * g.w));
+    }
+  }
+}
+
+// Same math with a two-row software pipeline: the grid is exactly resident (one
+// wave) and each warp loads row j + stride while it reduces and writes row j, so
+// a row's HBM latency overlaps the previous row's work instead of forming a
+// second wave (d <= 2048).
+template <int V>
+__global__ void __launch_bounds__(256)
+rmsnorm_rows_pipe_kernel(const float* __restrict__ x, int64_t ld_x, const uint32_t* __restrict__ rows,
+                         int64_t n_rows, const float* __restrict__ w, float eps, __nv_bfloat16* __restrict__ out,
+                         int64_t ld_out) {
+  pdl_wait();
+  constexpr int D = 128 * V;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  auto load = [&](int64_t j, float4 (&v)[V]) {
+    const int64_t r = rows ? static_cast<int64_t>(__ldg(rows + j)) : j;
+    const float4* xr = reinterpret_cast<const float4*>(x + r * ld_x);
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = __ldcs(xr + lane + 32 * i);
+  };
+  float4 cur[V], nxt[V];
+  int64_t j = warp0;
+  if (j < n_rows) load(j, cur);
+  for (; j < n_rows; j += nwarps) {
+    const bool more = j + nwarps < n_rows;
+    if (more) load(j + nwarps, nxt);
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) ss += cur[i].x * cur[i].x + cur[i].y * cur[i].y + cur[i].z * cur[i].z + cur[i].w * cur[i].w;
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / static_cast<float>(D) + eps);
+    uint2* orow = reinterpret_cast<uint2*>(out + j * ld_out);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * i);
+      orow[lane + 32 * i] = make_uint2(pack_bf16x2(cur[i].x * inv * g.x, cur[i].y * inv * g.y),
+                                       pack_bf16x2(cur[i].z * inv * g.z, cur[i].w * inv * g.w));
+    }
+    if (more) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) cur[i] = nxt[i];
     }
   }
 }
@@ -320,12 +361,19 @@ extern "C" int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* ro
     return RDX_ERR_SHAPE_MISMATCH;
   if (n_rows == 0) return RDX_OK;
   const int grid = grid_for_rows(n_rows, 8);
+  // pipelined kernels: exactly the resident blocks (one wave), never more than the rows need
+  auto pgrid = [&](auto kern) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) != cudaSuccess || per_sm < 1) per_sm = 1;
+    const int64_t g = static_cast<int64_t>(per_sm) * num_sms();
+    return static_cast<int>(g < grid ? g : grid);
+  };
   cudaStream_t st = as_stream(stream);
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out_bf16);
   const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) == 0;
   switch (aligned ? d : 0) {
-    case 1024: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<8>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
-    case 2048: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<16>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 1024: RDX_LAUNCH_PDL(rmsnorm_rows_pipe_kernel<8>, pgrid(rmsnorm_rows_pipe_kernel<8>), 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
+    case 2048: RDX_LAUNCH_PDL(rmsnorm_rows_pipe_kernel<16>, pgrid(rmsnorm_rows_pipe_kernel<16>), 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
     case 2560: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<20>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
     case 4096: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<32>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
     case 512: RDX_LAUNCH_PDL(rmsnorm_rows_reg_kernel<4>, grid, 256, 0, st, x, ld_x, rows, n_rows, w, eps, o, ld_out); break;
