@@ -11,3 +11,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"gemm_kernel<.int.256, .int.3" -s 28 -c 1 -o gpurun_out/prof_gemm_gateup python bench.py --profile --steps 1 --warmup 1 --no-cpu --no-graphs > gpurun_out/ncu_gemm_gateup.log 2>&1; echo ncu_gemm=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attention_kernel -s 28 -c 1 -o gpurun_out/prof_attn_c2step python bench.py --profile --steps 1 --warmup 1 --no-cpu --no-graphs > gpurun_out/ncu_attn_c2step.log 2>&1; echo ncu_attn=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gather_rows_kernel -s 3 -c 1 -o gpurun_out/prof_gather python scripts/gather_probe.py > gpurun_out/ncu_gather.log 2>&1; echo ncu_gather=$?
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"gemm_kernel<.int.256, .int.4" -s 28 -c 1 -o gpurun_out/prof_gemm_qkv python bench.py --profile --steps 1 --warmup 1 --no-cpu --no-graphs > gpurun_out/ncu_gemm_qkv.log 2>&1; echo ncu_qkv=$?
