@@ -246,6 +246,23 @@ def op_breakdown(model, step, steps, peak_tflops):
     return roof, ms / steps, breakdown
 
 
+def ncu_traffic(path):
+    """dram read + write bytes of one launch from a committed ncu --set full summary
+    (scripts/ncu_summary.py output under profiles/), or None."""
+    scale = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9}
+    try:
+        tot, kernel = 0.0, None
+        for line in open(path):
+            parts = line.split()
+            if line.startswith("kernel:"):
+                kernel = line.split(":", 1)[1].strip()[:60]
+            if len(parts) >= 4 and parts[0] == "dram" and parts[1] in ("read", "write"):
+                tot += float(parts[2]) * scale[parts[3].lower()]
+        return (round(tot), kernel) if tot else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 # ------------------------------------------------------------------ gather GB/s
 def gather_microbench(peak_gbs):
     import torch
@@ -570,6 +587,11 @@ def run_ours(args):
                                                      peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
     roof["peak_source"] = f"{peaks_src} bf16_tflops_sustained (kernels inside a long step)"
     roof["gemm_share_of_step"] = round(gemm_ms_per_step / (ms_radix / args.steps), 3)
+    tr = ncu_traffic(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                  f"r1_ncu_gemm_gateup_{args.config}.txt"))
+    if tr is not None:  # DRAM bytes of one gate_up launch (the largest GEMM) from the committed ncu capture
+        roof["traffic"] = tr[0]
+        roof["traffic_source"] = f"profiles/r1_ncu_gemm_gateup_{args.config}.txt ({tr[1]}; dram read+write, 1 launch)"
     _, _, breakdown_base = op_breakdown(model, step_base, 3, 1.0)
 
     gather = gather_microbench(peaks["hbm_gbs"]) if rank == 0 else None
