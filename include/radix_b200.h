@@ -235,6 +235,11 @@ int rdx_gemm(const rdx_gemm_args* args, void* stream);
  * for A/B runs, 1 back on.  Returns the previous setting. */
 int rdx_gemm_debug_tail_split(int on);
 
+/* Debug: pin the GEMM tile shape (cg = 1 or 2 CTAs, block_n = 128 or 256) for
+ * later launches, or cg = 0 for the automatic choice (A/B experiments; the
+ * RDX_GEMM_SHAPE="cg,bn" environment variable sets the same override). */
+int rdx_gemm_debug_shape(int cg, int block_n);
+
 /* Debug: clock64 role counters of builds made with -DRDX_GEMM_STATS_BUILD (MMA
  * waits / epilogue waits and busy cycles, see gemm.cu); RDX_ERR_UNSUPPORTED
  * otherwise.  out8 may be NULL; reset != 0 zeroes the counters. */

@@ -868,8 +868,11 @@ int dispatch(const rdx_gemm_args& a, int bn, int cg, cudaStream_t s) {
 // Pick (CG, BN) minimising tile rounds x per-tile cost.  A 1-CTA tile streams
 // a third more operand bytes per FLOP than the pair tile, hence the penalty.
 // RDX_GEMM_SHAPE="cg,bn" (env) pins the choice for experiments.
+int g_forced_cg = -1, g_forced_bn = -1;  // RDX_GEMM_SHAPE / rdx_gemm_debug_shape
+
 void choose_shape(const rdx_gemm_args& a, int* bn_out, int* cg_out) {
-  static int forced_cg = -1, forced_bn = -1;
+  int& forced_cg = g_forced_cg;
+  int& forced_bn = g_forced_bn;
   if (forced_cg < 0) {
     forced_cg = 0;
     if (const char* e = getenv("RDX_GEMM_SHAPE")) {
@@ -985,6 +988,18 @@ extern "C" int rdx_gemm_debug_stats(unsigned long long* out8, int reset) {
   (void)reset;
   return RDX_ERR_UNSUPPORTED;
 #endif
+}
+
+extern "C" int rdx_gemm_debug_shape(int cg, int block_n) {
+  using namespace rdx::gemm;
+  if (cg == 0) {
+    g_forced_cg = 0;  // automatic choice
+    return RDX_OK;
+  }
+  if ((cg != 1 && cg != 2) || (block_n != 128 && block_n != 256)) return RDX_ERR_INVALID_ARGUMENT;
+  g_forced_cg = cg;
+  g_forced_bn = block_n;
+  return RDX_OK;
 }
 
 extern "C" int rdx_gemm_debug_tail_split(int on) {
