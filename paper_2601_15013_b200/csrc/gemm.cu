@@ -437,13 +437,17 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
     // row-major: row r at r * hd/2; blocked: ((r/32) * hd/4 * 32 + r%32) float4s
     const float2* rope_row = ep.rope_ps == 1 ? ep.rope + r_clamped * (ep.hd >> 1)
                                              : ep.rope + 2 * ((r_clamped >> 5) * (ep.hd >> 2) * 32 + (r_clamped & 31));
-    const int c_hi = c_lo + hw;
+    // a split tail tile narrower than two heads (hw < hd, hd >= 64): the ch = 0 warp
+    // takes its whole width (whole heads), the ch = 1 warp has nothing to do
+    const bool whole = hw % ep.hd != 0 && ep.hd > 32;
+    const int lo = whole ? (ch ? 2 * hw : 0) : c_lo;
+    const int c_hi = whole ? 2 * hw : c_lo + hw;
     const float pos = ep.rope_pos ? static_cast<float>(__ldg(ep.rope_pos + r_clamped)) : 0.f;
     switch (ep.hd) {
-      case 128: qkv_cols<128>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
-      case 64: qkv_cols<64>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
-      case 32: qkv_cols<32>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
-      default: qkv_cols<16>(e, taddr, n0, c_lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
+      case 128: qkv_cols<128>(e, taddr, n0, lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
+      case 64: qkv_cols<64>(e, taddr, n0, lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
+      case 32: qkv_cols<32>(e, taddr, n0, lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
+      default: qkv_cols<16>(e, taddr, n0, lo, c_hi, N, ep, s_qn, s_kn, rope_row, map, rs, pos); break;
     }
   }
 }
@@ -827,7 +831,8 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
       const int w = BN / sf;
       bool ok = (w / 2) % 32 == 0;
       if (EPI == RDX_EPI_SWIGLU) ok = ok && w % (2 * kSwigluUnit) == 0;
-      if (EPI == RDX_EPI_QKV) ok = ok && a.head_dim > 0 && (w / 2) % a.head_dim == 0;
+      // QKV: each warp needs whole heads; a tile of one head width goes to the ch = 0 warps
+      if (EPI == RDX_EPI_QKV) ok = ok && a.head_dim > 0 && ((w / 2) % a.head_dim == 0 || (a.head_dim > 32 && w % a.head_dim == 0));
       if (EPI == RDX_EPI_RESID_NORM) ok = ok && (w / 2) % kNormGroup == 0;
       const double len = static_cast<double>((sf * rem + units - 1) / units) / sf;
       if (ok && len < best - 1e-9) {

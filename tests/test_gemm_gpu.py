@@ -347,3 +347,32 @@ def test_tail_split_bit_identical(epi_name, m, n, k):
     if epi == _native.EPI_STORE_F32:
         ref = a.float() @ w.float().T
         assert (outs[0] - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("m,hd,H,KV", [(7024, 128, 16, 8), (34816, 128, 32, 8), (7024, 64, 16, 8)])
+def test_qkv_tail_split_bit_identical(m, hd, H, KV):
+    """QKV tail tiles one head wide go to one warp per lane quarter: same bits as unsplit."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    lib = _native.lib()
+    d = 1024
+    a = _rand(m, d, 41)
+    n = (H + 2 * KV) * hd
+    w = _rand(n, d, 42, 0.05)
+    qn = torch.rand(hd, device="cuda") + 0.5
+    kn = torch.rand(hd, device="cuda") + 0.5
+    pos = torch.randint(0, 4096, (m,), device="cuda", dtype=torch.int32)
+    outs = []
+    for on in (1, 0):
+        prev = lib.rdx_gemm_debug_tail_split(on)
+        try:
+            o = torch.full((m, n), float("nan"), dtype=torch.bfloat16, device="cuda")
+            _gemm(a, w, _native.EPI_QKV, o, 0, qn=qn, kn=kn, rope=pos, pos=pos, hd=hd, H=H, KV=KV, eps=1e-6)
+            torch.cuda.synchronize()
+        finally:
+            lib.rdx_gemm_debug_tail_split(prev)
+        outs.append(o)
+    assert not torch.isnan(outs[0].float()).any()
+    assert torch.equal(outs[0], outs[1])
