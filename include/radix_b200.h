@@ -152,6 +152,16 @@ int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t
                      int64_t d, const float* w, float eps, void* out_bf16, int64_t ld_out,
                      void* stream);
 
+/* rdx_rmsnorm_rows on rows 0..n_rows-1 that may still be in flight from a
+ * preceding rdx_gemm (RDX_EPI_RESID_F32 with done_ctr) on the same stream: the
+ * kernel is launched as a programmatic dependent of that GEMM (it can start on
+ * SMs the GEMM's last round leaves idle) and processes row r once
+ * done_ctr[r / 32] >= target.  d must be 128 * V for V in {2, 4, 8, 16, 20, 32}
+ * (else RDX_ERR_UNSUPPORTED: use rdx_rmsnorm_rows after a stream-ordered GEMM). */
+int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_rows, int64_t d, const float* w, float eps,
+                           void* out_bf16, int64_t ld_out, const uint32_t* done_ctr, uint32_t target,
+                           void* stream);
+
 /* RoPE table for compact rows: table[j][i] = (cos, sin)(pos[j] * theta^(-2i/hd))
  * for i < hd/2, computed in fp64 and rounded to fp32 (model.py:165-172). */
 int rdx_rope_table(const uint32_t* pos, int64_t n_rows, int32_t head_dim, double theta,
@@ -226,6 +236,11 @@ typedef struct rdx_gemm_args {
    * frequencies, |error| < 1e-6 for positions < 2^20) and rope_table is unused. */
   const uint32_t* rope_pos;
   double rope_theta;
+  /* RDX_EPI_RESID_F32: when done_ctr != NULL, tiles run in row-block-major order and,
+   * once a warp's reduce-adds have completed, done_ctr[row / 32] is incremented by
+   * the number of columns it wrote for those 32 rows (a 32-row slab is complete
+   * when its counter has grown by N).  Feeds rdx_rmsnorm_rows_after. */
+  uint32_t* done_ctr;
 } rdx_gemm_args;
 
 int rdx_gemm(const rdx_gemm_args* args, void* stream);

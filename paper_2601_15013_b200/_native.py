@@ -34,6 +34,7 @@ EXPORTS = (
     "rdx_embed_rmsnorm",
     "rdx_embed_rows",
     "rdx_rmsnorm_rows",
+    "rdx_rmsnorm_rows_after",
     "rdx_rope_table",
     "rdx_rope_table_blocked",
     "rdx_gemm",
@@ -99,6 +100,7 @@ class GemmArgs(ctypes.Structure):
         ("rope_blocked", _i32),
         ("rope_pos", _vp),
         ("rope_theta", _f64),
+        ("done_ctr", _vp),
     ]
 
 
@@ -121,6 +123,7 @@ _SIGNATURES = {
     ),
     "rdx_embed_rows": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "rdx_rmsnorm_rows": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _i64, _vp]),
+    "rdx_rmsnorm_rows_after": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _f32, _vp, _i64, _vp, _u32, _vp]),
     "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_rope_table_blocked": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmArgs), _vp]),

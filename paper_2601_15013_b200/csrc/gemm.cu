@@ -72,6 +72,9 @@ struct EpiParams {
   int64_t ldhb;
   float* ss_out;
   int ss_out_parts;
+  // RDX_EPI_RESID_F32 with a completion counter: tiles in row-block-major order, and
+  // per 32-row slab the number of columns whose stores have completed
+  uint32_t* done_ctr;
 };
 
 constexpr int kNormGroup = 64;  // columns per partial sum of squares (RDX_EPI_RESID_NORM)
@@ -495,8 +498,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       part = static_cast<int>((t - tail_start) % split);
       width = BN / split;
     }
-    m_blk = f % m_tiles;
-    n0 = (f / m_tiles) * BN + part * width;
+    if (ep.done_ctr) {  // row blocks complete early, so a dependent pass can start on them
+      m_blk = f / n_tiles;
+      n0 = (f % n_tiles) * BN + part * width;
+    } else {
+      m_blk = f % m_tiles;
+      n0 = (f / m_tiles) * BN + part * width;
+    }
   };
   const int kblocks = static_cast<int>((K + BK - 1) / BK);
 
@@ -672,6 +680,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      if constexpr (EPI == RDX_EPI_RESID_F32) {
+        if (ep.done_ctr && lane == 0) {
+          // this warp's reduce-adds are complete and visible: publish its columns of the slab
+          const int64_t c0 = n0 + ch * (width / 2);
+          const int64_t cols = N - c0 < width / 2 ? (N - c0 > 0 ? N - c0 : 0) : width / 2;
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          atomicAdd(ep.done_ctr + (e.row0 >> 5), static_cast<uint32_t>(cols));
+        }
+      }
       st_b += clock64() - st_tb;
       ++n_t;
     }
@@ -816,6 +835,7 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   ep.ldhb = a.ldo_bf16;
   ep.ss_out = a.ss_out;
   ep.ss_out_parts = static_cast<int>(a.n / kNormGroup);
+  ep.done_ctr = EPI == RDX_EPI_RESID_F32 ? a.done_ctr : nullptr;
   const int64_t tiles = ((a.m + BM * CG - 1) / (BM * CG)) * ((a.n + BN - 1) / BN);
   const int64_t units_max = num_sms() / CG;
   const int64_t units = tiles < units_max ? tiles : units_max;

@@ -256,6 +256,53 @@ rmsnorm_rows_pipe_kernel(const float* __restrict__ x, int64_t ld_x, const uint32
   }
 }
 
+// rmsnorm of rows still being produced by the preceding residual GEMM (launched as
+// its programmatic dependent, no griddepcontrol.wait): row j is read once its
+// 32-row slab counter reaches `target` (acquire), in row order, so the blocks that
+// land on SMs the GEMM's last round leaves idle work on the row blocks it has
+// already finished.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int V>
+__global__ void __launch_bounds__(256)
+rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_rows, const float* __restrict__ w,
+                          float eps, __nv_bfloat16* __restrict__ out, int64_t ld_out,
+                          const uint32_t* __restrict__ done_ctr, uint32_t target) {
+  constexpr int D = 128 * V;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  int64_t ready = -1;  // slabs below this one are known complete
+  for (int64_t j = warp0; j < n_rows; j += nwarps) {
+    const int64_t slab = j >> 5;
+    if (slab > ready) {
+      while (ld_acquire_u32(done_ctr + slab) < target) __nanosleep(64);
+      ready = slab;
+    }
+    const float4* xr = reinterpret_cast<const float4*>(x + j * ld_x);
+    float4 v[V];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      v[i] = __ldcg(xr + lane + 32 * i);
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
+    ss = warp_sum(ss);
+    const float inv = rsqrtf(ss / static_cast<float>(D) + eps);
+    uint2* orow = reinterpret_cast<uint2*>(out + j * ld_out);
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * i);
+      orow[lane + 32 * i] = make_uint2(pack_bf16x2(v[i].x * inv * g.x, v[i].y * inv * g.y),
+                                       pack_bf16x2(v[i].z * inv * g.z, v[i].w * inv * g.w));
+    }
+  }
+}
+
 // blocked = 0: table[j][i]; blocked = 1: the QKV epilogue's lane-coalesced layout
 // (see rdx_rope_table_blocked): float2 (j, i) at 2*(((j/32)*(half/2) + i/2)*32 + j%32) + i%2.
 __global__ void rope_table_kernel(const uint32_t* __restrict__ pos, int64_t n_rows, int half,
@@ -381,6 +428,40 @@ extern "C" int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* ro
     default:
       RDX_LAUNCH_PDL(rmsnorm_rows_kernel, grid, 256, 0, st, x, ld_x, rows, n_rows, d, w, eps, o, ld_out);
   }
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}
+
+extern "C" int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_rows, int64_t d, const float* w,
+                                      float eps, void* out_bf16, int64_t ld_out, const uint32_t* done_ctr,
+                                      uint32_t target, void* stream) {
+  using namespace rdx;
+  if (n_rows < 0 || d <= 0 || (d % 8) != 0 || (ld_x % 4) != 0 || (ld_out % 8) != 0) return RDX_ERR_SHAPE_MISMATCH;
+  if (n_rows == 0) return RDX_OK;
+  if (!done_ctr) return RDX_ERR_INVALID_ARGUMENT;
+  if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) != 0) return RDX_ERR_UNSUPPORTED;
+  const int grid = grid_for_rows(n_rows, 8);
+  __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out_bf16);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(256);
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // always: it overlaps the GEMM's tail
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  switch (d) {
+    case 256: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<2>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
+    case 512: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<4>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
+    case 1024: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<8>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
+    case 2048: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<16>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
+    case 2560: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<20>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
+    case 4096: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<32>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
+    default: return RDX_ERR_UNSUPPORTED;
+  }
+  if (e != cudaSuccess) return set_cuda_error(e);
   RDX_LAUNCH_CHECK();
   return RDX_OK;
 }

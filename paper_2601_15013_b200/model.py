@@ -41,6 +41,7 @@ read-out); ``logits="all"`` returns the reference's [N, vocab].
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, fields
 
 import numpy as np
@@ -355,6 +356,8 @@ class RadixQwen3:
         # Off by default: measured on B200 it does not beat the TMA reduce-add epilogue +
         # rmsnorm pass (C2 7.48-7.58 vs 7.66-7.68 ms, C4 551 vs 556 ms).
         self.fused_norm = False if fused_norm is None else fused_norm
+        # rmsnorm passes overlap the residual GEMM's last round (RDX_NORM_OVERLAP=0: stream-ordered)
+        self.norm_overlap = os.environ.get("RDX_NORM_OVERLAP", "1") != "0"
         if self.fused_norm:
             if config.hidden_size % 64:
                 raise ShapeMismatch("fused_norm needs hidden_size % 64 == 0")
@@ -369,7 +372,7 @@ class RadixQwen3:
         return fn()
 
     def _gemm(self, name, a, w, epi, out, *, m, stream, qkv=False, rope=None, layer=None, row_ss=None,
-              hb=None, ss_out=None):
+              hb=None, ss_out=None, done=None):
         cfg = self.config
         args = _native.GemmArgs()
         args.a = a.data_ptr()
@@ -396,6 +399,8 @@ class RadixQwen3:
             args.q_heads = cfg.num_heads
             args.kv_heads = cfg.num_kv_heads
             args.eps = cfg.norm_eps
+        if done is not None:  # per-32-row-slab completion counter for rdx_rmsnorm_rows_after
+            args.done_ctr = done.data_ptr()
         if row_ss is not None:  # RMSNorm of the A rows fused in (weight folded into w)
             args.row_ss = row_ss.data_ptr()
             args.ss_parts = row_ss.shape[1]
@@ -421,6 +426,18 @@ class RadixQwen3:
                                         n_rows, x.shape[1], w.data_ptr(), self.config.norm_eps,
                                         out.data_ptr(), out.stride(0), stream)
             _native.check(code, "rdx_rmsnorm_rows")
+
+        self._op("rmsnorm", launch)
+
+    def _rmsnorm_after(self, x, w, out, ctr, target, stream=None):
+        """rmsnorm overlapping the tail of the residual GEMM that feeds it (slab counters)."""
+        lib = _native.lib()
+
+        def launch():
+            code = lib.rdx_rmsnorm_rows_after(x.data_ptr(), x.stride(0), x.shape[0], x.shape[1], w.data_ptr(),
+                                              self.config.norm_eps, out.data_ptr(), out.stride(0), ctr.data_ptr(),
+                                              target, stream)
+            _native.check(code, "rdx_rmsnorm_rows_after")
 
         self._op("rmsnorm", launch)
 
@@ -625,6 +642,19 @@ class RadixQwen3:
             ends = cu64[1:] - 1
             last_rows = (scatter[ends] if mode != "plain" else ends).to(torch.int32).contiguous()
         att_flops = 4.0 * qd * getattr(self, "_att_pairs", 0.0)
+        # ln2 / next ln1 start on the row blocks the residual GEMM has finished (its last
+        # round leaves SMs idle): 32-row slab counters, one target step of d per use
+        overlap = self.norm_overlap and not fused and d in (256, 512, 1024, 2048, 2560, 4096)
+        ctr = torch.zeros(-(-m // 32), dtype=torch.int32, device=dev) if overlap else None
+        uses = 0
+
+        def norm_after(wt):
+            nonlocal uses
+            if overlap:
+                uses += 1
+                self._rmsnorm_after(h, wt, hn, ctr, uses * d, stream=st)
+            else:
+                self._rmsnorm(h, wt, hn, stream=st)
 
         for i in range(cfg.num_layers):
             pre = f"layers.{i}."
@@ -641,14 +671,15 @@ class RadixQwen3:
                 a = self._gather("gather_attn", a_full, gather, stream)
             a = a.reshape(m, qd)
             self._gemm("o_proj", a, T[pre + "wo"], resid_epi, h, m=m, stream=st, hb=hn if fused else None,
-                       ss_out=ss)
+                       ss_out=ss, done=ctr)
             if not fused:
-                self._rmsnorm(h, T[pre + "ln2"], hn, stream=st)
+                norm_after(T[pre + "ln2"])
             self._gemm("gate_up", hn, T[pre + "w_gu" + sfx], _native.EPI_SWIGLU, act, m=m, stream=st, row_ss=ss)
+            last = i + 1 == cfg.num_layers
             self._gemm("down", act, T[pre + "w_down"], resid_epi, h, m=m, stream=st, hb=hn if fused else None,
-                       ss_out=ss)
-            if not fused and i + 1 < cfg.num_layers:
-                self._rmsnorm(h, T[f"layers.{i + 1}.ln1"], hn, stream=st)
+                       ss_out=ss, done=None if last else ctr)
+            if not fused and not last:
+                norm_after(T[f"layers.{i + 1}.ln1"])
 
         vocab = cfg.vocab_size
         vpad = -(-vocab // 8) * 8  # 16-byte aligned logits rows
