@@ -4,6 +4,7 @@
 //   rdx_rmsnorm_rows    RMSNorm of (selected) fp32 rows (model.py:147-152)
 //   rdx_rope_table      fp64 RoPE tables on compact positions (model.py:165-172)
 //   rdx_rerank_scores   last-token reranker read-out (DESIGN.md scoring contract)
+#include <cstdlib>
 #include "common.cuh"
 
 namespace rdx {
@@ -273,32 +274,42 @@ rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_r
                           float eps, __nv_bfloat16* __restrict__ out, int64_t ld_out,
                           const uint32_t* __restrict__ done_ctr, uint32_t target) {
   constexpr int D = 128 * V;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  int64_t ready = -1;  // slabs below this one are known complete
-  for (int64_t j = warp0; j < n_rows; j += nwarps) {
-    const int64_t slab = j >> 5;
-    if (slab > ready) {
-      while (ld_acquire_u32(done_ctr + slab) < target) __nanosleep(64);
-      ready = slab;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // A block takes 8 consecutive rows (one per warp) per step.  One thread polls
+  // their slab counters (acquire, backing off) so waiting blocks add almost no L2
+  // traffic.  No cross-step prefetch: a block must not wait on a later, unfinished
+  // row block while it holds rows that are ready.
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * 8; base < n_rows; base += static_cast<int64_t>(gridDim.x) * 8) {
+    if (threadIdx.x == 0) {
+      const int64_t last = base + 7 < n_rows ? base + 7 : n_rows - 1;
+      for (int64_t slab = base >> 5; slab <= (last >> 5); ++slab) {
+        unsigned ns = 128;
+        while (ld_acquire_u32(done_ctr + slab) < target) {
+          __nanosleep(ns);
+          ns = ns < 2048 ? 2 * ns : ns;
+        }
+      }
     }
-    const float4* xr = reinterpret_cast<const float4*>(x + j * ld_x);
-    float4 v[V];
-    float ss = 0.f;
+    __syncthreads();
+    const int64_t j = base + warp;
+    if (j < n_rows) {
+      const float4* xr = reinterpret_cast<const float4*>(x + j * ld_x);
+      float4 v[V];
+      float ss = 0.f;
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      v[i] = __ldcg(xr + lane + 32 * i);
-      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
-    }
-    ss = warp_sum(ss);
-    const float inv = rsqrtf(ss / static_cast<float>(D) + eps);
-    uint2* orow = reinterpret_cast<uint2*>(out + j * ld_out);
+      for (int i = 0; i < V; ++i) {
+        v[i] = __ldcg(xr + lane + 32 * i);
+        ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+      }
+      ss = warp_sum(ss);
+      const float inv = rsqrtf(ss / static_cast<float>(D) + eps);
+      uint2* orow = reinterpret_cast<uint2*>(out + j * ld_out);
 #pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const float4 g = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * i);
-      orow[lane + 32 * i] = make_uint2(pack_bf16x2(v[i].x * inv * g.x, v[i].y * inv * g.y),
-                                       pack_bf16x2(v[i].z * inv * g.z, v[i].w * inv * g.w));
+      for (int i = 0; i < V; ++i) {
+        const float4 g = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * i);
+        orow[lane + 32 * i] = make_uint2(pack_bf16x2(v[i].x * inv * g.x, v[i].y * inv * g.y),
+                                         pack_bf16x2(v[i].z * inv * g.z, v[i].w * inv * g.w));
+      }
     }
   }
 }
@@ -440,15 +451,18 @@ extern "C" int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_ro
   if (n_rows == 0) return RDX_OK;
   if (!done_ctr) return RDX_ERR_INVALID_ARGUMENT;
   if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) != 0) return RDX_ERR_UNSUPPORTED;
-  const int grid = grid_for_rows(n_rows, 8);
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out_bf16);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.gridDim = dim3(static_cast<unsigned>(grid_for_rows(n_rows, 8)));
   cfg.blockDim = dim3(256);
   cfg.stream = as_stream(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // always: it overlaps the GEMM's tail
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static const int pdl = [] {
+    const char* v = std::getenv("RDX_NORM_AFTER_PDL");
+    return v && v[0] == '0' ? 0 : 1;
+  }();
+  attr[0].val.programmaticStreamSerializationAllowed = pdl;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;

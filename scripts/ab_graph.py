@@ -1,5 +1,5 @@
 """A/B of a library switch on the C2 CUDA-graph step: two models captured with the switch on / off,
-replays interleaved (same box, same clocks).  python scripts/ab_graph.py [pdl|tail]"""
+replays interleaved (same box, same clocks).  python scripts/ab_graph.py [pdl|tail|norm] [c2|c3|c4]"""
 import os
 import sys
 
@@ -13,7 +13,11 @@ from paper_2601_15013_b200.rerank import RadixReranker  # noqa: E402
 what = sys.argv[1] if len(sys.argv) > 1 else "pdl"
 cfg_name = sys.argv[2] if len(sys.argv) > 2 else "c2"
 lib = _native.lib()
-setter = lib.rdx_debug_pdl if what == "pdl" else lib.rdx_gemm_debug_tail_split
+if what == "norm":  # model-level switch: rmsnorm overlapping the residual GEMM's tail
+    def setter(on):
+        os.environ["RDX_NORM_OVERLAP"] = str(on)
+else:
+    setter = lib.rdx_debug_pdl if what == "pdl" else lib.rdx_gemm_debug_tail_split
 config, _, batch, _ = bench.build_config(cfg_name, 1)
 w = DeviceWeights.random(config, seed=0)
 db = DeviceBatch.from_batch(batch)
