@@ -255,6 +255,11 @@ int rdx_gemm_debug_tail_split(int on);
  * RDX_GEMM_SHAPE="cg,bn" environment variable sets the same override). */
 int rdx_gemm_debug_shape(int cg, int block_n);
 
+/* Debug: tile raster of later GEMM launches -- groups of group_m row blocks with
+ * the row block varying fastest inside a group (0 = default; RDX_GEMM_GROUP_M in
+ * the environment sets the same).  Returns the previous setting. */
+int rdx_gemm_debug_group_m(int group_m);
+
 /* Debug: clock64 role counters of builds made with -DRDX_GEMM_STATS_BUILD (MMA
  * waits / epilogue waits and busy cycles, see gemm.cu); RDX_ERR_UNSUPPORTED
  * otherwise.  out8 may be NULL; reset != 0 zeroes the counters. */

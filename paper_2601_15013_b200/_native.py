@@ -41,6 +41,7 @@ EXPORTS = (
     "rdx_gemm_debug_tail_split",
     "rdx_gemm_debug_stats",
     "rdx_gemm_debug_shape",
+    "rdx_gemm_debug_group_m",
     "rdx_debug_pdl",
     "rdx_attention",
     "rdx_attention_debug_stats",
@@ -130,6 +131,7 @@ _SIGNATURES = {
     "rdx_gemm_debug_tail_split": (ctypes.c_int, [ctypes.c_int]),
     "rdx_gemm_debug_stats": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rdx_gemm_debug_shape": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "rdx_gemm_debug_group_m": (ctypes.c_int, [ctypes.c_int]),
     "rdx_debug_pdl": (ctypes.c_int, [ctypes.c_int]),
     "rdx_rerank_scores": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
     "rdx_attention": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i64,

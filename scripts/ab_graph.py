@@ -13,7 +13,10 @@ from paper_2601_15013_b200.rerank import RadixReranker  # noqa: E402
 what = sys.argv[1] if len(sys.argv) > 1 else "pdl"
 cfg_name = sys.argv[2] if len(sys.argv) > 2 else "c2"
 lib = _native.lib()
-if what == "norm":  # model-level switch: rmsnorm overlapping the residual GEMM's tail
+if what == "group":  # GEMM raster: G_ON vs G_OFF row blocks per group (captured into each arm's graph)
+    def setter(on):
+        lib.rdx_gemm_debug_group_m(int(os.environ.get("G_ON", "16") if on else os.environ.get("G_OFF", "0")))
+elif what == "norm":  # model-level switch: rmsnorm overlapping the residual GEMM's tail
     def setter(on):
         os.environ["RDX_NORM_OVERLAP"] = str(on)
 else:
