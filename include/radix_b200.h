@@ -156,7 +156,8 @@ int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t
  * preceding rdx_gemm (RDX_EPI_RESID_F32 with done_ctr) on the same stream: the
  * kernel is launched as a programmatic dependent of that GEMM (it can start on
  * SMs the GEMM's last round leaves idle) and processes row r once
- * done_ctr[r / 32] >= target.  d must be 128 * V for V in {2, 4, 8, 16, 20, 32}
+ * done_ctr[r / 32] >= target (a slab still incomplete after ~8 s traps: the
+ * counters and targets did not match).  d must be 128 * V for V in {2, 4, 8, 16, 20, 32}
  * (else RDX_ERR_UNSUPPORTED: use rdx_rmsnorm_rows after a stream-ordered GEMM). */
 int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_rows, int64_t d, const float* w, float eps,
                            void* out_bf16, int64_t ld_out, const uint32_t* done_ctr, uint32_t target,
@@ -239,7 +240,8 @@ typedef struct rdx_gemm_args {
   /* RDX_EPI_RESID_F32: when done_ctr != NULL, tiles run in row-block-major order and,
    * once a warp's reduce-adds have completed, done_ctr[row / 32] is incremented by
    * the number of columns it wrote for those 32 rows (a 32-row slab is complete
-   * when its counter has grown by N).  Feeds rdx_rmsnorm_rows_after. */
+   * when its counter has grown by N); done_ctr holds ceil(M / 32) counters.
+   * Feeds rdx_rmsnorm_rows_after. */
   uint32_t* done_ctr;
 } rdx_gemm_args;
 

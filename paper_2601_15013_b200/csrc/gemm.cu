@@ -684,7 +684,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
       if constexpr (EPI == RDX_EPI_RESID_F32) {
-        if (ep.done_ctr && lane == 0) {
+        if (ep.done_ctr && lane == 0 && e.row0 < M) {  // slabs past M do not exist
           // this warp's reduce-adds are complete and visible: publish its columns of the slab
           const int64_t c0 = n0 + ch * (width / 2);
           const int64_t cols = N - c0 < width / 2 ? (N - c0 > 0 ? N - c0 : 0) : width / 2;

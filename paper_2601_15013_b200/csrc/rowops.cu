@@ -284,9 +284,11 @@ rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_r
       const int64_t last = base + 7 < n_rows ? base + 7 : n_rows - 1;
       for (int64_t slab = base >> 5; slab <= (last >> 5); ++slab) {
         unsigned ns = 128;
+        uint32_t spins = 0;
         while (ld_acquire_u32(done_ctr + slab) < target) {
           __nanosleep(ns);
           ns = ns < 2048 ? 2 * ns : ns;
+          if (++spins > (1u << 22)) __trap();  // ~8 s: the producing GEMM never completed this slab -> fail loudly
         }
       }
     }
