@@ -425,3 +425,31 @@ def test_resid_done_counter_and_rmsnorm_after(m, d, k):
             assert (ctr == d).all()
     torch.cuda.synchronize()
     assert (ctr == 2 * d).all()
+
+
+@pytest.mark.parametrize("epi_name", ["EPI_RESID_F32", "EPI_SWIGLU", "EPI_STORE_BF16"])
+def test_tile_raster_bit_identical(epi_name):
+    """The tile raster (groups of row blocks) only reorders whole tiles: same bits."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    lib = _native.lib()
+    epi = getattr(_native, epi_name)
+    m, n, k = 17000, 2048, 512  # 67 pair row blocks: the grouped raster is the default here
+    a, w = _rand(m, k, 61), _rand(n, k, 62, 0.05)
+    shape = (m, n // 2) if epi == _native.EPI_SWIGLU else (m, n)
+    dt = torch.float32 if epi == _native.EPI_RESID_F32 else torch.bfloat16
+    base = torch.randn(shape, device="cuda").to(dt)
+    outs = []
+    for g in (0, 1, 3, 16, 1000):
+        prev = lib.rdx_gemm_debug_group_m(g)
+        try:
+            o = base.clone()
+            _gemm(a, w, epi, o)
+            torch.cuda.synchronize()
+        finally:
+            lib.rdx_gemm_debug_group_m(prev)
+        outs.append(o)
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)

@@ -160,3 +160,35 @@ def test_fused_norm_path_matches_reference():
     err = float(np.abs(out - ref).max() / np.abs(ref).max())
     assert err <= 2e-2, err
     torch.cuda.synchronize()
+
+
+def test_norm_overlap_bit_identical():
+    """rmsnorm overlapped with the residual GEMM (slab counters + programmatic dependent
+    launch, the default) gives the same logits as the stream-ordered passes, eager and
+    under CUDA graphs, dedup on and off."""
+    import torch
+
+    from paper_2601_15013_b200 import DeviceWeights, RadixQwen3
+    from paper_2601_15013_b200.model import QWEN3_PRESETS, DeviceBatch, Qwen3Config
+    from paper_2601_15013_b200.plan import build_plan_device
+    from paper_2601_15013_b200.workloads import RerankSpec, msmarco_rerank_batch
+
+    base = QWEN3_PRESETS["qwen3-0.6b"]
+    cfg = Qwen3Config(3, base.hidden_size, base.intermediate_size, base.num_heads, base.num_kv_heads, base.head_dim,
+                      base.vocab_size, base.rope_theta, base.norm_eps)
+    w = DeviceWeights.random(cfg, seed=3)
+    batch = msmarco_rerank_batch(RerankSpec(passages_per_query=16))
+    db = DeviceBatch.from_batch(batch)
+    plan = build_plan_device(db.tok, db.pos, db.cu)
+    outs = {}
+    for graphs in (False, True):
+        for overlap in (True, False):
+            m = RadixQwen3(cfg, w, use_graphs=graphs)
+            m.norm_overlap = overlap
+            for p in (plan, None):
+                o = m.prefill(db, p, logits="last")
+                o = m.prefill(db, p, logits="last").clone()  # second call: graph replay
+                torch.cuda.synchronize()
+                outs[(graphs, overlap, p is None)] = o
+    for key, o in outs.items():
+        assert torch.equal(o, outs[(False, False, key[2])]), key
