@@ -161,6 +161,37 @@ __device__ __forceinline__ void emit_bf16x32(EpiWarp<NB>& e, const float* v, con
   epi_issue(e, map, c0, false);
 }
 
+// Two 32-column bf16 boxes behind one proxy fence and one bulk group.  Used by
+// the QKV epilogue (HD >= 64), which then emits only pairs: with every group two
+// boxes, the two ring slots about to be written (the 4th and 3rd most recent) are
+// free once at most one group is still being read.
+template <int NB>
+__device__ __forceinline__ void emit_bf16x32_pair(EpiWarp<NB>& e, const float* v1, int32_t c1, const float* v2,
+                                                  int32_t c2, const CUtensorMap* map) {
+  static_assert(NB == 4, "pair emits assume a ring of four boxes");
+  if (e.lane == 0) bulk_wait_read<1>();
+  __syncwarp();
+  const int sw = (e.lane >> 1) & 3;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const float* v = b ? v2 : v1;
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+    const uint32_t base = smem_u32(e.base + ((e.cur + b) % NB) * (kEpiWarpBytes / NB)) + e.lane * 64;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st_shared_v4(base + ((j ^ sw) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (e.lane == 0) {
+    tma_store_2d(map, e.base + e.cur * (kEpiWarpBytes / NB), c1, e.row0);
+    tma_store_2d(map, e.base + ((e.cur + 1) % NB) * (kEpiWarpBytes / NB), c2, e.row0);
+    bulk_commit();
+  }
+  e.cur = (e.cur + 2) % NB;
+}
+
 // 32 fp32 columns -> 128 B row of a SWIZZLE_128B box -> TMA store or reduce-add.
 template <int NB>
 __device__ __forceinline__ void emit_f32x32(EpiWarp<NB>& e, const float* v, const CUtensorMap* map, int32_t c0,
@@ -219,13 +250,14 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
       const int kind = col0 < ep.q_dim ? 0 : (col0 < ep.q_dim + ep.kv_dim ? 1 : 2);
       if (kind == 2) {
 #pragma unroll 1
-        for (int c = 0; c < HD; c += 32) {
-          float v[32];
+        for (int c = 0; c < HD; c += 64) {
+          float v[64];
           tmem_ld32p(taddr + h0 + c, v);
+          tmem_ld32p(taddr + h0 + c + 32, v + 32);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= rs;
-          emit_bf16x32(e, v, map, static_cast<int32_t>(col0 + c));
+          for (int j = 0; j < 64; ++j) v[j] *= rs;
+          emit_bf16x32_pair(e, v, static_cast<int32_t>(col0 + c), v + 32, static_cast<int32_t>(col0 + c + 32), map);
         }
         continue;
       }
@@ -276,8 +308,7 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
           tmem_wait_ld();
           rope_pair32(x1, x2, w + c, w + H + c, inv, rope_row + c * ep.rope_ps, ep.rope_ps);
         }
-        emit_bf16x32(e, x1, map, static_cast<int32_t>(col0 + c));
-        emit_bf16x32(e, x2, map, static_cast<int32_t>(col0 + H + c));
+        emit_bf16x32_pair(e, x1, static_cast<int32_t>(col0 + c), x2, static_cast<int32_t>(col0 + H + c), map);
       }
     }
   } else {
