@@ -806,7 +806,7 @@ int make_map_3d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void*
 // RDX_GEMM_GROUP_M (env) / rdx_gemm_debug_group_m: row blocks per raster group (0 = default).
 int g_group_m = -1;
 int group_m_setting() {
-  if (g_group_m < 0) {
+  if (g_group_m == -1) {  // unset: read the environment once
     const char* e = getenv("RDX_GEMM_GROUP_M");
     g_group_m = e ? atoi(e) : 0;
   }
@@ -885,8 +885,8 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
     // Default raster: with many row blocks (C3/C4 scale: A = M x K no longer fits L2)
     // groups of 16 row blocks keep each group's A rows L2-resident while the group
     // walks the column blocks, so A is read from HBM once and B m_tiles/16 times
-    // (measured: C3 step +10.5 %, C4 +13 % over column-block-major; 8 vs 16 within
-    // noise).  Few row blocks (C2): the legacy orders (row-block-major when a
+    // (measured: C3 step +10.5 %, C4 +13 % over column-block-major; 8, 24, 32 and a
+    // K-scaled group size (A rows of a group ~48 MB) were equal or slower).  Few row blocks (C2): the legacy orders (row-block-major when a
     // completion counter is attached).
     int gm = group_m_setting();
     if (gm <= 0) gm = m_tiles >= 64 ? 16 : (ep.done_ctr ? 1 : static_cast<int>(m_tiles));
