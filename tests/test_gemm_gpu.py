@@ -453,3 +453,43 @@ def test_tile_raster_bit_identical(epi_name):
         outs.append(o)
     for o in outs[1:]:
         assert torch.equal(outs[0], o)
+
+
+def test_gemm_shape_fuzz():
+    """Seeded random shapes through every tile shape, raster and the slab counters:
+    STORE_F32 / RESID_F32 against torch fp32, counters == N per slab."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    lib = _native.lib()
+    rng = np.random.default_rng(7)
+    for trial in range(14):
+        m = int(rng.integers(1, 20000))
+        n = int(rng.integers(1, 96)) * 64
+        k = int(rng.integers(1, 40)) * 64
+        shape = [(0, 0), (1, 128), (1, 256), (2, 128), (2, 256)][trial % 5]
+        group = [0, 1, 3, 16][trial % 4]
+        a, w = _rand(m, k, 100 + trial), _rand(n, k, 200 + trial, 0.05)
+        ref = a.float() @ w.float().T
+        lib.rdx_gemm_debug_shape(*shape)
+        prev_g = lib.rdx_gemm_debug_group_m(group)
+        try:
+            out = torch.full((m, n), float("nan"), device="cuda")
+            _gemm(a, w, _native.EPI_STORE_F32, out)
+            h0 = torch.randn(m, n, device="cuda")
+            h = h0.clone()
+            ctr = torch.zeros(-(-m // 32), dtype=torch.int32, device="cuda")
+            args = _native.GemmArgs()
+            args.a, args.b, args.m, args.n, args.k = a.data_ptr(), w.data_ptr(), m, n, k
+            args.lda, args.ldb, args.epi, args.out, args.ldo = k, k, _native.EPI_RESID_F32, h.data_ptr(), n
+            args.done_ctr = ctr.data_ptr()
+            _native.check(lib.rdx_gemm(args, _native.stream_handle()), "gemm")
+            torch.cuda.synchronize()
+        finally:
+            lib.rdx_gemm_debug_shape(0, 0)
+            lib.rdx_gemm_debug_group_m(prev_g)
+        tol = 1e-3 * ref.abs().max().item() + 1e-4
+        assert (out - ref).abs().max().item() <= tol, (m, n, k, shape, group)
+        assert (h - (h0 + ref)).abs().max().item() <= tol, (m, n, k, shape, group)
+        assert (ctr == n).all(), (m, n, k, shape, group)
