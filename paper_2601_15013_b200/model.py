@@ -502,13 +502,14 @@ class RadixQwen3:
             from .errors import IndexOutOfRange
 
             raise IndexOutOfRange("token id outside [0, vocab_size)")
-        if ledger is None:
-            ledger = FlopLedger()
         lay = self._layout(db, plan, attention)
         mode = "plain" if not lay.dedup else ("suffix" if attention == "suffix" and lay.suffix_ok else "full")
-        self._fill_ledger(ledger, lay, db, mode, logits)
-        self._att_pairs = self._attention_pairs(db, lay, mode)
-        if not self.use_graphs or self.op_hook is not None:
+        if ledger is not None:  # row accounting only when the caller asked for it (host time on the hot path)
+            self._fill_ledger(ledger, lay, db, mode, logits)
+        eager = not self.use_graphs or self.op_hook is not None
+        if eager or self._graph_key(db, lay, mode, logits) not in self._graphs:
+            self._att_pairs = self._attention_pairs(db, lay, mode)  # FLOP accounting of the launches
+        if eager:
             out, err = self._body(db.tok, lay.gather, lay.scatter, lay.positions, db.cu32, db.cu, lay.cu_q32,
                                   lay.m, db.n, db.b, lay.n_compact, lay.max_q, db.max_len, mode, logits, stream)
             if db.max_token < 0 and int(err.item()):
@@ -518,10 +519,14 @@ class RadixQwen3:
             return out
         return self._replay(db, lay, mode, logits, stream)
 
+    @staticmethod
+    def _graph_key(db, lay, mode, logits):
+        return (lay.m, db.n, db.b, lay.n_compact, lay.max_q, db.max_len, mode, logits)
+
     def _replay(self, db, lay, mode, logits, stream):
         import torch
 
-        key = (lay.m, db.n, db.b, lay.n_compact, lay.max_q, db.max_len, mode, logits)
+        key = self._graph_key(db, lay, mode, logits)
         g = self._graphs.get(key)
         dyn = {"tok": db.tok, "gather": lay.gather, "scatter": lay.scatter, "pos": lay.positions,
                "cu32": db.cu32, "cu": db.cu, "cu_q32": lay.cu_q32}
@@ -541,6 +546,8 @@ class RadixQwen3:
                                     lay.n_compact, lay.max_q, db.max_len, mode, logits, None)
             g = _Graph(graph, inputs, out)
             self._graphs[key] = g
+        # always copy: device buffers written through the C ABI do not bump torch's
+        # version counters, so "same tensor" cannot prove "same contents"
         for k, v in dyn.items():
             if v is not None:
                 g.inputs[k].copy_(v, non_blocking=True)
