@@ -253,7 +253,30 @@ def test_gemm_error_codes():
     out = torch.zeros(4, 8, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ShapeMismatch):
         _gemm(a, w, _native.EPI_STORE_BF16, out)
-    np.testing.assert_equal(1, 1)
+    # rdx_rmsnorm_rows_after: unsupported width, missing counters, QKV rope_pos head_dim
+    lib, st = _native.lib(), _native.stream_handle()
+    x = torch.zeros(64, 384, device="cuda")
+    wn = torch.ones(384, device="cuda")
+    o = torch.empty(64, 384, dtype=torch.bfloat16, device="cuda")
+    ctr = torch.zeros(2, dtype=torch.int32, device="cuda")
+    assert lib.rdx_rmsnorm_rows_after(x.data_ptr(), 384, 64, 384, wn.data_ptr(), 1e-6, o.data_ptr(), 384,
+                                      ctr.data_ptr(), 384, st) == 13  # RDX_ERR_UNSUPPORTED
+    assert lib.rdx_rmsnorm_rows_after(x.data_ptr(), 384, 64, 384, wn.data_ptr(), 1e-6, o.data_ptr(), 384,
+                                      None, 384, st) == 12  # RDX_ERR_INVALID_ARGUMENT
+    assert lib.rdx_rmsnorm_rows_after(x.data_ptr(), 384, 0, 384, wn.data_ptr(), 1e-6, o.data_ptr(), 384,
+                                      None, 0, st) == 0  # no rows: nothing to do
+    aq = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
+    wq = torch.zeros(6 * 32, 64, dtype=torch.bfloat16, device="cuda")
+    oq = torch.zeros(8, 6 * 32, dtype=torch.bfloat16, device="cuda")
+    pos = torch.zeros(8, dtype=torch.int32, device="cuda")
+    qn = torch.ones(32, device="cuda")
+    args = _native.GemmArgs()
+    args.a, args.b, args.m, args.n, args.k, args.lda, args.ldb = aq.data_ptr(), wq.data_ptr(), 8, 192, 64, 64, 64
+    args.epi, args.out, args.ldo = _native.EPI_QKV, oq.data_ptr(), 192
+    args.q_norm_w = args.k_norm_w = qn.data_ptr()
+    args.head_dim, args.q_heads, args.kv_heads, args.eps = 32, 2, 2, 1e-6
+    args.rope_pos, args.rope_theta = pos.data_ptr(), 1e6  # positions mode needs head_dim 64 or 128
+    assert lib.rdx_gemm(args, st) == 12
 
 
 def _gemm_norm(a, w, epi, out, block_n=0, row_ss=None, norm_dim=0, eps=1e-6, hb=None, ss_out=None):
