@@ -123,7 +123,8 @@ def score_stream(reranker, batches):
         ready.record(side)
         return db, plan, ready
 
-    results = []
+    results = [None] * len(batches)
+    pending = None  # (index, pinned buffer, event) of the batch whose scores are still in flight
     nxt = prepare(batches[0], 0)
     for t in range(len(batches)):
         db, plan, ready = nxt
@@ -141,6 +142,14 @@ def score_stream(reranker, batches):
         done.record(main)
         if t + 1 < len(batches):
             nxt = prepare(batches[t + 1], (t + 1) & 1)  # overlaps the prefill of batch t
-        done.synchronize()
-        results.append(np.array(buf.numpy(), copy=True))
+        # collect batch t-1 only now: batch t's prefill is already queued behind it, so the
+        # GPU never idles on the host's read-back (slot (t-1)&1 is reused by batch t+1)
+        if pending is not None:
+            pt, pbuf, pdone = pending
+            pdone.synchronize()
+            results[pt] = np.array(pbuf.numpy(), copy=True)
+        pending = (t, buf, done)
+    pt, pbuf, pdone = pending
+    pdone.synchronize()
+    results[pt] = np.array(pbuf.numpy(), copy=True)
     return results
