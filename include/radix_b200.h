@@ -64,7 +64,9 @@ typedef enum rdx_status {
   RDX_ERR_CUDA = 100
 } rdx_status;
 
-/* Library version (major*10000 + minor*100 + patch). */
+/* Library version (major*10000 + minor*100 + patch): 200 = 0.2.0, whose
+ * rdx_gemm_args ends at done_ctr.  Check it against RDX_VERSION before use. */
+#define RDX_VERSION 200
 int rdx_version(void);
 /* Stable name of a status code ("RDX_OK", "IndexOutOfRange", …). */
 const char* rdx_status_name(int status);
@@ -203,6 +205,7 @@ typedef enum rdx_epilogue {
                              is folded into the next GEMM's B, see row_ss)          */
 } rdx_epilogue;
 
+/* Zero-initialise (fields are appended between versions; 0 / NULL = feature off). */
 typedef struct rdx_gemm_args {
   const void* a;       /* bf16 [M, lda] */
   const void* b;       /* bf16 [N, ldb] */

@@ -39,7 +39,7 @@ bool pdl_enabled() {
 
 }  // namespace rdx
 
-extern "C" int rdx_version(void) { return 100; }  // 0.1.0
+extern "C" int rdx_version(void) { return 200; }  // 0.2.0: rdx_gemm_args grew (rope_blocked, rope_pos, rope_theta, done_ctr)
 
 extern "C" const char* rdx_status_name(int status) {
   switch (status) {
