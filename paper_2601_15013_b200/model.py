@@ -42,6 +42,7 @@ from __future__ import annotations
 
 import math
 import os
+from collections import OrderedDict
 from dataclasses import dataclass, fields
 
 import numpy as np
@@ -328,10 +329,11 @@ class _Layout:
 class _Graph:
     """One captured prefill body plus its static input buffers."""
 
-    def __init__(self, graph, inputs: dict, output):
+    def __init__(self, graph, inputs: dict, output, err):
         self.graph = graph
         self.inputs = inputs
         self.output = output
+        self.err = err
 
 
 class RadixQwen3:
@@ -339,13 +341,18 @@ class RadixQwen3:
 
     ``prefill`` resolves the plan (GPU planner: one small D2H read for N'),
     then runs the layer stack.  With ``use_graphs=True`` the layer stack is
-    captured once per shape key (rows, tokens, sequences, max lengths, modes)
-    into a CUDA graph and replayed, removing per-launch host overhead; pad
-    plans to a bucket (``pad_plan``) to bound the number of distinct keys.
+    captured into a CUDA graph per shape BUCKET and replayed, removing
+    per-launch host overhead: N' is padded to a multiple of 256 rows the way
+    ``pad_plan`` pads (repeating gather[0] / compact_positions[0]), the batch
+    to a multiple of 16 sequences with empty ones, and the index buffers /
+    attention grid to bucketed token counts and lengths.  All captures share
+    one memory pool, at most ``max_graphs`` graphs are kept (least recently
+    used evicted) and ``graph_captures`` counts captures.  A graph's output
+    is valid until the next ``prefill`` call on the same model.
     """
 
     def __init__(self, config: ModelConfig, weights: DeviceWeights, use_graphs: bool = False,
-                 fused_norm: bool | None = None):
+                 fused_norm: bool | None = None, max_graphs: int = 8):
         _check_kernel_shapes(config)
         self.config = config
         self.w = weights
@@ -363,7 +370,10 @@ class RadixQwen3:
                 raise ShapeMismatch("fused_norm needs hidden_size % 64 == 0")
             weights.fold_norms()
         self.op_hook = None  # optional callable(name, launch_fn, flops) (bench.py per-op CUDA events)
-        self._graphs: dict = {}
+        self._graphs: OrderedDict = OrderedDict()  # bucket key -> _Graph, least recently used first
+        self._graph_pool = None
+        self.max_graphs = max_graphs
+        self.graph_captures = 0
 
     # ------------------------------------------------------------ launches
     def _op(self, name, fn, flops=0.0):
@@ -506,7 +516,7 @@ class RadixQwen3:
         mode = "plain" if not lay.dedup else ("suffix" if attention == "suffix" and lay.suffix_ok else "full")
         if ledger is not None:  # row accounting only when the caller asked for it (host time on the hot path)
             self._fill_ledger(ledger, lay, db, mode, logits)
-        eager = not self.use_graphs or self.op_hook is not None
+        eager = not self.use_graphs or self.op_hook is not None or db.n == 0
         if eager or self._graph_key(db, lay, mode, logits) not in self._graphs:
             self._att_pairs = self._attention_pairs(db, lay, mode)  # FLOP accounting of the launches
         if eager:
@@ -519,40 +529,99 @@ class RadixQwen3:
             return out
         return self._replay(db, lay, mode, logits, stream)
 
+    # CUDA-graph buckets (pad_plan semantics, trie.py:206-233): one graph
+    # serves every batch whose padded shape falls in the same bucket.  M_BUCKET = 256 is the
+    # CTA-pair GEMM row tile, so padding N' up to it adds no GEMM tile; the other buckets
+    # only size index buffers and the attention unit grid (empty units cost a skip).
+    M_BUCKET, N_BUCKET, B_BUCKET, LEN_BUCKET = 256, 2048, 16, 64
+
     @staticmethod
-    def _graph_key(db, lay, mode, logits):
-        return (lay.m, db.n, db.b, lay.n_compact, lay.max_q, db.max_len, mode, logits)
+    def _round(x, q):
+        return -(-max(int(x), 1) // q) * q
+
+    def _graph_shape(self, db, lay, mode):
+        """(m_b, n_b, b_b, max_q_b, max_k_b) of the bucket a batch falls in."""
+        r = self._round
+        if mode == "plain":
+            m_b = n_b = r(db.n, self.M_BUCKET)
+        else:
+            m_b, n_b = r(lay.m, self.M_BUCKET), r(db.n, self.N_BUCKET)
+        max_k = r(db.max_len, self.LEN_BUCKET)
+        max_q = max_k if mode == "plain" else r(lay.max_q, self.LEN_BUCKET)
+        return m_b, n_b, r(db.b, self.B_BUCKET), max_q, max_k
+
+    def _graph_key(self, db, lay, mode, logits):
+        return (mode, logits) + self._graph_shape(db, lay, mode)
+
+    @staticmethod
+    def _fill(dst, src, pad_from_end=False):
+        """dst[:len(src)] = src; the rest repeats src[0] (or src[-1]): device-side, no sync."""
+        k = src.shape[0]
+        dst[:k].copy_(src, non_blocking=True)
+        if k < dst.shape[0]:
+            edge = src[k - 1:k] if pad_from_end else src[:1]
+            dst[k:].copy_(edge.expand(dst.shape[0] - k), non_blocking=True)
 
     def _replay(self, db, lay, mode, logits, stream):
         import torch
 
         key = self._graph_key(db, lay, mode, logits)
+        m_b, n_b, b_b, max_q_b, max_k_b = key[2:]
         g = self._graphs.get(key)
-        dyn = {"tok": db.tok, "gather": lay.gather, "scatter": lay.scatter, "pos": lay.positions,
-               "cu32": db.cu32, "cu": db.cu, "cu_q32": lay.cu_q32}
         if g is None:
-            inputs = {k: (None if v is None else v.clone()) for k, v in dyn.items()}
+            dev = db.tok.device
+            i32 = dict(dtype=torch.int32, device=dev)
+            inputs = {"tok": torch.zeros(n_b, **i32), "pos": torch.zeros(m_b, **i32),
+                      "cu32": torch.zeros(b_b + 1, **i32), "cu": torch.zeros(b_b + 1, dtype=torch.int64, device=dev),
+                      "gather": None, "scatter": None, "cu_q32": None}
+            if mode != "plain":
+                inputs.update(gather=torch.zeros(m_b, **i32), scatter=torch.zeros(n_b, **i32),
+                              cu_q32=torch.zeros(b_b + 1, **i32))
+            self._stage(inputs, db, lay, mode)
+            cu_q = inputs["cu32"] if mode == "plain" else inputs["cu_q32"]
+            args = (inputs["tok"], inputs["gather"], inputs["scatter"], inputs["pos"], inputs["cu32"], inputs["cu"],
+                    cu_q, m_b, n_b, b_b, 0, max_q_b, max_k_b, mode, logits, None)
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):  # warm-up outside capture (allocator, lazy init)
-                self._body(inputs["tok"], inputs["gather"], inputs["scatter"], inputs["pos"], inputs["cu32"],
-                           inputs["cu"], inputs["cu_q32"], lay.m, db.n, db.b, lay.n_compact, lay.max_q,
-                           db.max_len, mode, logits, None)
+                self._body(*args)
             torch.cuda.current_stream().wait_stream(side)
+            if self._graph_pool is None:  # one memory pool shared by every captured bucket
+                self._graph_pool = torch.cuda.graph_pool_handle()
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                out, _ = self._body(inputs["tok"], inputs["gather"], inputs["scatter"], inputs["pos"],
-                                    inputs["cu32"], inputs["cu"], inputs["cu_q32"], lay.m, db.n, db.b,
-                                    lay.n_compact, lay.max_q, db.max_len, mode, logits, None)
-            g = _Graph(graph, inputs, out)
+            with torch.cuda.graph(graph, pool=self._graph_pool):
+                out, err = self._body(*args)
+            g = _Graph(graph, inputs, out, err)
             self._graphs[key] = g
-        # always copy: device buffers written through the C ABI do not bump torch's
-        # version counters, so "same tensor" cannot prove "same contents"
-        for k, v in dyn.items():
-            if v is not None:
-                g.inputs[k].copy_(v, non_blocking=True)
+            self.graph_captures += 1
+            while len(self._graphs) > self.max_graphs:  # LRU bound
+                self._graphs.popitem(last=False)
+        else:
+            self._graphs.move_to_end(key)
+            # always copy: device buffers written through the C ABI do not bump torch's
+            # version counters, so "same tensor" cannot prove "same contents"
+            self._stage(g.inputs, db, lay, mode)
         g.graph.replay()
-        return g.output
+        if db.max_token < 0 and int(g.err.item()):
+            from .errors import IndexOutOfRange
+
+            raise IndexOutOfRange("token id outside [0, vocab_size)")
+        rows = db.b if logits == "last" else db.n
+        return g.output[:rows]
+
+    def _stage(self, inputs, db, lay, mode):
+        """Copy one batch into a bucket's static buffers, padding as pad_plan does."""
+        self._fill(inputs["tok"], db.tok)
+        self._fill(inputs["cu32"], db.cu32, pad_from_end=True)   # padded sequences are empty
+        self._fill(inputs["cu"], db.cu, pad_from_end=True)
+        if mode == "plain":
+            self._fill(inputs["pos"], db.pos)
+        else:
+            self._fill(inputs["gather"], lay.gather)              # pad rows repeat gather[0] ...
+            self._fill(inputs["pos"], lay.positions)              # ... and compact_positions[0]
+            self._fill(inputs["scatter"], lay.scatter)
+            if lay.cu_q32 is not None:
+                self._fill(inputs["cu_q32"], lay.cu_q32, pad_from_end=True)
 
     def _fill_ledger(self, ledger, lay, db, mode, logits):
         """Row counters exactly as the reference's forward records them (model.py:331-411)."""
@@ -642,8 +711,8 @@ class RadixQwen3:
         qkv = torch.empty(m, qd + 2 * kvd, dtype=bf, device=dev)
         act = torch.empty(m, self.di_pad, dtype=bf, device=dev)
         attn_out = torch.empty(m, qd, dtype=bf, device=dev)
-        if mode == "suffix" and m > n_compact:
-            attn_out[n_compact:] = 0  # padded plan rows are never attention queries
+        if mode != "full" and m > n_compact:
+            attn_out[n_compact:] = 0  # padded rows are never attention queries (n_compact = 0: graph buckets)
         last_rows = None
         if logits == "last":
             ends = cu64[1:] - 1

@@ -67,7 +67,11 @@ class RadixReranker:
         cu_host = np.asarray(batch.cu_seqlens, dtype=np.int64)
         lens = np.diff(cu_host)
         self.h2d_bytes = tok.numel() * 4 + pos.numel() * 4 + cu.numel() * 8
-        return DeviceBatch(dt, dp, dc, dc.to(torch.int32), cu_host, n, b, int(lens.max()) if lens.size else 0)
+        # host max token id (O(N) next to the copy): out-of-vocab ids raise IndexOutOfRange before
+        # any launch, on the eager and the CUDA-graph path alike
+        max_token = int(batch.token_ids.max()) if n else -1
+        return DeviceBatch(dt, dp, dc, dc.to(torch.int32), cu_host, n, b, int(lens.max()) if lens.size else 0,
+                           max_token)
 
     def plan(self, db: DeviceBatch):
         """GPU plan of a device batch (None when dedup is off)."""

@@ -192,3 +192,45 @@ def test_norm_overlap_bit_identical():
                 outs[(graphs, overlap, p is None)] = o
     for key, o in outs.items():
         assert torch.equal(o, outs[(False, False, key[2])]), key
+
+
+def test_graph_buckets_distinct_batches():
+    """A stream of DISTINCT batches (different N, N', B, lengths) through CUDA-graph buckets:
+    every result equals the eager forward bit for bit, batches of one bucket share a graph,
+    the cache stays within max_graphs (LRU) and out-of-vocab ids raise on the graph path."""
+    import torch
+
+    from paper_2601_15013_b200 import DeviceWeights, IndexOutOfRange, RadixQwen3
+    from paper_2601_15013_b200.model import DeviceBatch, Qwen3Config
+    from paper_2601_15013_b200.plan import build_plan_device
+    from paper_2601_15013_b200.workloads import RerankSpec, msmarco_rerank_batch
+
+    cfg = Qwen3Config(2, 256, 512, 4, 2, 64, 4096, 1e6, 1e-6)
+    w = DeviceWeights.random(cfg, seed=5)
+    eager = RadixQwen3(cfg, w)
+    graphs = RadixQwen3(cfg, w, use_graphs=True, max_graphs=3)
+    specs = [RerankSpec(passages_per_query=p, vocab=4096, seed=s) for s, p in
+             ((0, 16), (1, 16), (2, 17), (3, 30), (4, 16), (5, 33), (6, 9), (7, 16))]
+    keys = set()
+    for spec in specs:
+        db = DeviceBatch.from_batch(msmarco_rerank_batch(spec))
+        plan = build_plan_device(db.tok, db.pos, db.cu)
+        for p in (plan, None):
+            ref = eager.prefill(db, p, logits="last")
+            got = graphs.prefill(db, p, logits="last")
+            torch.cuda.synchronize()
+            assert got.shape == ref.shape
+            assert torch.equal(got, ref), (spec, p is None)
+            lay = graphs._layout(db, p, "suffix")
+            keys.add(graphs._graph_key(db, lay, "suffix" if p is not None else "plain", "last"))
+        assert len(graphs._graphs) <= 3
+    assert graphs.graph_captures >= len(keys) and len(keys) < 2 * len(specs)
+    # all-logits output through a bucket (padded rows sliced off)
+    db = DeviceBatch.from_batch(msmarco_rerank_batch(specs[0]))
+    plan = build_plan_device(db.tok, db.pos, db.cu)
+    assert torch.equal(graphs.prefill(db, plan), eager.prefill(db, plan))
+    # device batch with an unknown max token id and an out-of-vocab id: the graph path checks on device
+    bad = DeviceBatch(db.tok.clone(), db.pos, db.cu, db.cu32, db.cu_host, db.n, db.b, db.max_len, -1)
+    bad.tok[5] = cfg.vocab_size + 3
+    with pytest.raises(IndexOutOfRange):
+        graphs.prefill(bad, build_plan_device(bad.tok, bad.pos, bad.cu), logits="last")

@@ -100,3 +100,64 @@ def test_gather_scores_world2_gloo(tmp_path):
     want = np.array([float(b.token_ids[cu[i]:cu[i + 1]].astype(np.int64).sum() % 9973)
                      for i in range(b.num_sequences)], dtype=np.float32)
     assert np.array_equal(got, want)
+
+
+def _brute_makespan(lens, lcps, world):
+    """Exhaustive minimum over all contiguous splits (small cases)."""
+    import itertools
+
+    b = len(lens)
+    best = None
+    for cut in itertools.combinations(range(1, b), world - 1):
+        cuts = [0, *cut, b]
+        costs = []
+        for r in range(world):
+            lo, hi = cuts[r], cuts[r + 1]
+            costs.append(int(lens[lo:hi].sum() - lcps[lo:hi - 1].sum()))
+        mk = max(costs)
+        best = mk if best is None else min(best, mk)
+    return best
+
+
+def test_partition_minimises_makespan():
+    from paper_2601_15013_b200.shard import _makespan_cuts
+
+    rng = np.random.default_rng(4)
+    for _ in range(40):
+        b = int(rng.integers(2, 9))
+        world = int(rng.integers(1, b + 1))
+        lens = rng.integers(5, 40, size=b)
+        lcps = np.array([rng.integers(0, min(lens[i], lens[i + 1]) + 1) for i in range(b - 1)], dtype=np.int64)
+        cuts = _makespan_cuts(lens.astype(np.int64), lcps, world)
+        assert cuts[0] == 0 and cuts[-1] == b and all(cuts[i] < cuts[i + 1] for i in range(world))
+        costs = [int(lens[cuts[r]:cuts[r + 1]].sum() - lcps[cuts[r]:cuts[r + 1] - 1].sum()) for r in range(world)]
+        assert max(costs) == _brute_makespan(lens, lcps, world)
+
+
+def test_strong_scaling_shards_balanced_c4():
+    """C4 (128 x (2048 + 256)) at 8 GPUs: 16 sequences each, N'_g = 2048 + 16*256."""
+    from paper_2601_15013_b200.shard import partition_by_subtree, shard_report
+    from paper_2601_15013_b200.workloads import long_prefix_batch
+
+    rep = shard_report(partition_by_subtree(long_prefix_batch(seed=0), 8))
+    assert [r["sequences"] for r in rep] == [16] * 8
+    assert all(r["N_compact"] == 2048 + 16 * 256 for r in rep)
+
+
+@pytest.mark.parametrize("argv", [["--gpus", "2"], ["--gpus", "4", "--config", "c4"],
+                                  ["--gpus", "3", "--config", "c3"]])
+def test_bench_launcher_selftest(argv):
+    """bench.py --gpus N re-executes itself under torch.distributed.run (N ranks, gloo here),
+    partitions the workload by trie subtree and all-gathers per-sequence scores."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    r = subprocess.run([sys.executable, "bench.py", *argv, "--selftest-launcher"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["ok"] and line["n_ranks"] == int(argv[1])
+    assert sum(s["sequences"] for s in line["shards"]) == line["global_batch"]
