@@ -794,10 +794,11 @@ def run_ours(args):
     line = None
     if rank == 0:
         steps_b = max(3, min(args.steps, 10))
-        by = op_breakdown(model, step_radix, steps_b)
+        # per-op events on this rank's own work (no collective: the other ranks wait at the final barrier)
+        by = op_breakdown(model, lambda: rr.score_device(db), steps_b)
         ms_step = ms_radix / args.steps
         roof = roofline(by, steps_b, ms_step, peaks, peaks_src, args.config)
-        by_base = op_breakdown(model, step_base, 3)
+        by_base = op_breakdown(model, lambda: rr_base.score_device(db), 3)
         breakdown = {k: {"us_per_step": round(v[1] * 1e3 / steps_b, 1), "launches_per_step": v[2] // steps_b,
                          **({"tflops": round(v[0] / (v[1] * 1e-3) / 1e12, 1)} if v[0] else {})}
                      for k, v in sorted(by.items(), key=lambda kv: -kv[1][1])}

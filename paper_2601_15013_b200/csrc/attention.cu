@@ -303,28 +303,53 @@ struct Unit {
   int nkt0, nkt1;  // key tiles of query tile h (0 = tile absent)
 };
 
-__device__ __forceinline__ bool load_unit(const Args& a, int u, Unit& it) {
+__device__ __forceinline__ void unit_geometry(const Args& a, int u, int k0, int k1, int q0, int q1, Unit& it) {
   const int per = a.nseq * a.kv_heads;
   const int pair = a.max_pairs - 1 - u / per;
   const int rem = u - (u / per) * per;
   it.s = rem / a.kv_heads;
   it.g = rem - it.s * a.kv_heads;
-  it.k0 = __ldg(a.cu + it.s);
-  it.L = __ldg(a.cu + it.s + 1) - it.k0;
-  it.q0 = __ldg(a.cu_q + it.s);
-  it.qlen = __ldg(a.cu_q + it.s + 1) - it.q0;
+  it.k0 = k0;
+  it.L = k1 - k0;
+  it.q0 = q0;
+  it.qlen = q1 - q0;
   it.lcp = it.L - it.qlen;
   it.mb0 = 2 * pair;
   const int mb1 = it.mb0 + 1;
   it.nkt0 = it.mb0 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (it.mb0 + 1) * a.qpt) + BK - 1) / BK : 0;
   it.nkt1 = mb1 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (mb1 + 1) * a.qpt) + BK - 1) / BK : 0;
-  return it.nkt0 > 0;
 }
 
-// Next valid unit of this CTA at or after u (returns n_units when done).
+// Next valid unit of this CTA at or after u (returns n_units when done).  Four
+// candidates are fetched per step (independent loads, one L2 round trip), so a
+// run of empty units (e.g. the mostly-empty longest pair level) costs one
+// latency per four, not one each.
+constexpr int kScan = 2;
 __device__ __forceinline__ int next_unit(const Args& a, int u, Unit& it) {
-  for (; u < a.n_units; u += gridDim.x)
-    if (load_unit(a, u, it)) return u;
+  for (; u < a.n_units; u += kScan * static_cast<int>(gridDim.x)) {
+    int k0[kScan], k1[kScan], q0[kScan], q1[kScan];
+    const int per = a.nseq * a.kv_heads;
+#pragma unroll
+    for (int i = 0; i < kScan; ++i) {
+      const int c = u + i * static_cast<int>(gridDim.x);
+      const int cc = c < a.n_units ? c : u;
+      const int s = (cc - (cc / per) * per) / a.kv_heads;
+      k0[i] = __ldg(a.cu + s);
+      k1[i] = __ldg(a.cu + s + 1);
+      q0[i] = __ldg(a.cu_q + s);
+      q1[i] = __ldg(a.cu_q + s + 1);
+    }
+#pragma unroll
+    for (int i = 0; i < kScan; ++i) {
+      const int c = u + i * static_cast<int>(gridDim.x);
+      if (c >= a.n_units) return a.n_units;
+      const int pair = a.max_pairs - 1 - c / per;
+      if (2 * pair * a.qpt < q1[i] - q0[i]) {  // query tile 0 of the pair exists
+        unit_geometry(a, c, k0[i], k1[i], q0[i], q1[i], it);
+        return c;
+      }
+    }
+  }
   return a.n_units;
 }
 
@@ -573,24 +598,26 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       };
       auto wait_tile = [&](uint32_t seqno) { RDX_TWAIT(&t_full[seqno % NSLOT], (seqno / NSLOT) & 1, st_t); };
 
-      Unit tmp;
+      Unit tmp, pre;
       int ucur = next_unit(a, blockIdx.x, tmp);
       int c0 = tmp.nkt0, c1 = tmp.nkt1, call = max(tmp.nkt0, tmp.nkt1);  // key tiles of the current unit
       int jcur = 0;
+      int upre = a.n_units;  // the unit after the current one, fetched while S/softmax of this one run
       if (ucur < a.n_units) {
         wait_tile(2 * gt);
         if (c0 > 0) issue_S(0, c0, 0, gt);
         if (c1 > 0) issue_S(1, c1, 0, gt);
         commit_elect(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
+        upre = next_unit(a, ucur + gridDim.x, pre);
       }
       while (ucur < a.n_units) {
         int unxt = ucur, jnxt = jcur + 1, n0 = c0, n1 = c1, nall = call;
         if (jnxt >= call) {
-          unxt = next_unit(a, ucur + gridDim.x, tmp);
+          unxt = upre;
           jnxt = 0;
-          n0 = tmp.nkt0;
-          n1 = tmp.nkt1;
-          nall = max(tmp.nkt0, tmp.nkt1);
+          n0 = pre.nkt0;
+          n1 = pre.nkt1;
+          nall = max(pre.nkt0, pre.nkt1);
         }
         const bool has_next = unxt < a.n_units;
         const uint32_t tnext = gt + 1;
@@ -606,12 +633,15 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           if (jnxt < n1) issue_S(1, n1, jnxt, tnext);
           commit_elect(&t_free[(2 * tnext) % NSLOT]);  // K(next) consumed by both S
         }
+        const bool switched = unxt != ucur;
         ucur = unxt;
         jcur = jnxt;
         c0 = n0;
         c1 = n1;
         call = nall;
         ++gt;
+        // new current unit: its S tiles are issued, so fetching the one after it overlaps the softmax
+        if (switched && ucur < a.n_units) upre = next_unit(a, ucur + gridDim.x, pre);
       }
       if (lane == 0) RDX_EV_FLUSH();
       if (RDX_STATS_ON && lane == 0) {

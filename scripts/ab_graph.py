@@ -21,7 +21,7 @@ elif what == "norm":  # model-level switch: rmsnorm overlapping the residual GEM
         os.environ["RDX_NORM_OVERLAP"] = str(on)
 else:
     setter = lib.rdx_debug_pdl if what == "pdl" else lib.rdx_gemm_debug_tail_split
-config, _, batch, _ = bench.build_config(cfg_name, 1)
+config, _, batch, _ = bench.workload(cfg_name, 1, "weak")
 w = DeviceWeights.random(config, seed=0)
 db = DeviceBatch.from_batch(batch)
 arms = {}

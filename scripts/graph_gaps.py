@@ -12,7 +12,7 @@ from paper_2601_15013_b200 import DeviceBatch, DeviceWeights, RadixQwen3  # noqa
 from paper_2601_15013_b200.rerank import RadixReranker  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-config, _, batch, _ = bench.build_config(cfg_name, 1)
+config, _, batch, _ = bench.workload(cfg_name, 1, "weak")
 rr = RadixReranker(RadixQwen3(config, DeviceWeights.random(config, seed=0), use_graphs=True))
 db = DeviceBatch.from_batch(batch)
 plan = rr.plan(db)

@@ -10,7 +10,7 @@ import bench  # noqa: E402
 from paper_2601_15013_b200 import DeviceBatch, DeviceWeights, RadixQwen3  # noqa: E402
 from paper_2601_15013_b200.rerank import RadixReranker  # noqa: E402
 
-config, _, batch, _ = bench.build_config("c2", 1)
+config, _, batch, _ = bench.workload("c2", 1, "weak")
 rr = RadixReranker(RadixQwen3(config, DeviceWeights.random(config, seed=0), use_graphs=True))
 db = DeviceBatch.from_batch(batch)
 for _ in range(5):

@@ -39,7 +39,7 @@ def test_sharded_scores_match_single_pass(world, tmp_path):
 
 def test_bench_two_ranks_one_gpu():
     r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--share-gpu", "--steps", "3", "--warmup", "3",
-                        "--no-cpu"], cwd=ROOT, capture_output=True, text=True, timeout=1500)
+                        "--no-cpu"], cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["scaling"] == "weak"

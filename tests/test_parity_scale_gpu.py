@@ -38,12 +38,10 @@ def maxrel(a, b):
 
 
 def _record(name, payload):
-    """Keep the measured errors next to the run (gpurun_out/ is the scratch dir that comes back)."""
-    from conftest import ROOT
-
-    out = os.path.join(ROOT, "gpurun_out")
-    if os.path.isdir(out):
-        with open(os.path.join(out, "parity_scale.jsonl"), "a") as f:
+    """Keep the measured errors (RDX_PARITY_LOG=<path>: appended as JSON lines)."""
+    path = os.environ.get("RDX_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
             f.write(json.dumps({"test": name, **payload}) + "\n")
     print(name, payload)
 
