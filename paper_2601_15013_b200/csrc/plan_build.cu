@@ -12,7 +12,7 @@
 //      rows of sequence s are the contiguous suffix [cu[s] + lcp_s, cu[s+1])
 //      and compact ids are ranks in (sequence, depth) order.
 //
-// Algorithm (one cooperative persistent launch, phases split by grid.sync):
+// Algorithm (one persistent launch, phases split by grid-wide barriers):
 //   P0  validate cu; seg[i] (binary search); m_i = mix(tok, pos, depth, seed)
 //   P1  global inclusive scan of m (wrapping u64 adds) -> P; block sums
 //   P2  path hash H_i = P_i - P_{start(s)-1} (exact in Z/2^64); insert H_i
@@ -40,6 +40,13 @@ constexpr int kPlanWarps = kPlanThreads / 32;
 constexpr int kMaxAttempts = 4;
 constexpr int kTokensPerBlockTarget = 512;
 constexpr int64_t kSingleCtaTokens = 1024;  // up to here one CTA beats a cooperative grid (launch + grid barriers)
+// Up to here the grid is ONE thread-block cluster (<= 16 CTAs on one GPC): the phase
+// barriers are hardware cluster barriers (barrier.cluster, release/acquire at cluster
+// scope, which orders the global-memory phases too) instead of cooperative grid syncs,
+// which cost microseconds each.  Beyond it: the cooperative grid (512 tokens per CTA).
+constexpr int64_t kClusterTokens = 65536;
+
+enum PlanMode { kSingle = 0, kCluster = 1, kGrid = 2 };
 
 __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
   k ^= k >> 33;
@@ -129,15 +136,21 @@ __device__ uint64_t block_sum_u64(uint64_t v, uint64_t* warp_tot) {
   return total;
 }
 
-// SINGLE = one CTA (small batches): phases are separated by __syncthreads
-// instead of cooperative grid barriers, and the launch is an ordinary one.
-template <bool SINGLE>
+// kSingle = one CTA (small batches): phases are separated by __syncthreads and
+// the launch is an ordinary one; kCluster = the grid is one cluster (cluster
+// barriers); kGrid = cooperative launch (grid barriers).
+template <int MODE>
 __global__ void __launch_bounds__(kPlanThreads)
 plan_build_kernel(PlanArgs a, PlanScratch s) {
   struct Sync {
     __device__ void sync() {
-      if constexpr (SINGLE) __syncthreads();
-      else cg::this_grid().sync();
+      if constexpr (MODE == kSingle) {
+        __syncthreads();
+      } else if constexpr (MODE == kCluster) {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+      } else {
+        cg::this_grid().sync();
+      }
     }
   } grid;
   __shared__ uint64_t warp_tot[kPlanWarps];
@@ -325,10 +338,41 @@ int max_coop_blocks() {
   static int cached = 0;
   if (cached == 0) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_build_kernel<false>, kPlanThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_build_kernel<kGrid>, kPlanThreads, 0) !=
         cudaSuccess)
       return 0;
     cached = per_sm * num_sms();
+  }
+  return cached;
+}
+
+// Largest cluster (16, non-portable, else 8) the planner can be launched as; 0 = none.
+int cluster_ctas() {
+  static int cached = -1;
+  if (cached < 0) {
+    cached = 0;
+    auto kern = plan_build_kernel<kCluster>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+    }
+    for (int c : {16, 8}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c);
+      cfg.blockDim = dim3(kPlanThreads);
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = c;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters > 0) {
+        cached = c;
+        break;
+      }
+      cudaGetLastError();
+    }
   }
   return cached;
 }
@@ -392,11 +436,27 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
   const int grid = static_cast<int>(want < mg ? want : mg);
   void* params[] = {&a, &s};
   if (n_tokens <= kSingleCtaTokens) {  // small batch: one CTA, no grid-wide barriers
-    plan_build_kernel<true><<<1, kPlanThreads, 0, as_stream(stream)>>>(a, s);
+    plan_build_kernel<kSingle><<<1, kPlanThreads, 0, as_stream(stream)>>>(a, s);
     RDX_LAUNCH_CHECK();
     return RDX_OK;
   }
-  RDX_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_build_kernel<false>), dim3(grid),
+  const int cl = cluster_ctas();
+  if (n_tokens <= kClusterTokens && cl > 0) {  // mid-size batch: one cluster, hardware barriers
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(kPlanThreads);
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cl;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, plan_build_kernel<kCluster>, a, s));
+    return RDX_OK;
+  }
+  RDX_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_build_kernel<kGrid>), dim3(grid),
                                            dim3(kPlanThreads), params, 0, as_stream(stream)));
   return RDX_OK;
 }

@@ -97,7 +97,9 @@ def _weights(cfg, seed, layers):
                     p + "w_down": u(d, di)})
         for nm, n in (("ln1", d), ("ln2", d), ("q_norm", cfg.head_dim), ("k_norm", cfg.head_dim)):
             dev[p + nm] = torch.ones(n, device="cuda")
-    dw = DeviceWeights.from_tensors(cfg, lambda n: dev[n])
+    from dataclasses import replace
+
+    dw = DeviceWeights.from_tensors(replace(cfg, num_layers=layers), lambda n: dev[n])
     host = {k: v.float().cpu().numpy() for k, v in dev.items() if k != "embed"}
     return dw, host, dev["embed"]
 
