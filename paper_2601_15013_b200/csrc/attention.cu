@@ -66,6 +66,10 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O only when th
 #endif
 constexpr uint32_t kEmulated = RDX_ATTN_EMU;  // pairs (mod 8) whose exp2 runs on the FMA pipe (bitmask)
 constexpr int kShortUnitTiles = 4;         // <= this many key tiles per unit: double-buffered Q
+constexpr int kRing = 8;                   // unit descriptors the scheduler warp runs ahead
+constexpr int kUnitWords = 12;             // ints per ring entry (Unit + its index)
+constexpr int kSchedWarp = 14;             // walks this CTA's units and publishes the valid ones
+constexpr int kUnitConsumers = 14;         // warps that read each entry: softmax 8, loader, epilogue 4, MMA
 
 // NQB = Q buffers per query tile, NSLOT = K/V ring slots (K and V tiles alternate).
 template <int HDP, int NQB, int NSLOT>
@@ -77,7 +81,8 @@ struct Tile {
   static constexpr int T_OFF = 2 * NQB * Q_BYTES;
   static constexpr int L_OFF = T_OFF + NSLOT * T_BYTES;  // fp32 [2 h][2 slots][128] row sums
   static constexpr int BAR_OFF = L_OFF + 2 * 2 * BQ * 4;
-  static constexpr int SMEM = BAR_OFF + 256;
+  static constexpr int RING_OFF = BAR_OFF + 256;               // unit ring (scheduler warp -> roles)
+  static constexpr int SMEM = RING_OFF + kRing * kUnitWords * 4 + 2 * kRing * 8;
   static_assert(SMEM <= 232448, "shared memory budget");
   static constexpr uint32_t IDESC_S = umma_idesc_bf16(BQ, BK);
   static constexpr uint32_t IDESC_PV = umma_idesc_bf16(BQ, HDP) | (1u << 16);  // B (V) MN-major
@@ -320,37 +325,79 @@ __device__ __forceinline__ void unit_geometry(const Args& a, int u, int k0, int 
   it.nkt1 = mb1 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (mb1 + 1) * a.qpt) + BK - 1) / BK : 0;
 }
 
-// Next valid unit of this CTA at or after u (returns n_units when done).  Four
-// candidates are fetched per step (independent loads, one L2 round trip), so a
-// run of empty units (e.g. the mostly-empty longest pair level) costs one
-// latency per four, not one each.
-constexpr int kScan = 2;
-__device__ __forceinline__ int next_unit(const Args& a, int u, Unit& it) {
-  for (; u < a.n_units; u += kScan * static_cast<int>(gridDim.x)) {
-    int k0[kScan], k1[kScan], q0[kScan], q1[kScan];
-    const int per = a.nseq * a.kv_heads;
-#pragma unroll
-    for (int i = 0; i < kScan; ++i) {
-      const int c = u + i * static_cast<int>(gridDim.x);
-      const int cc = c < a.n_units ? c : u;
-      const int s = (cc - (cc / per) * per) / a.kv_heads;
-      k0[i] = __ldg(a.cu + s);
-      k1[i] = __ldg(a.cu + s + 1);
-      q0[i] = __ldg(a.cu_q + s);
-      q1[i] = __ldg(a.cu_q + s + 1);
+// The CTA's units are u = blockIdx.x + k * gridDim.x in order; the scheduler
+// warp evaluates 32 candidates per step (one L2 round trip), publishes the valid
+// ones into a shared-memory ring (kRing entries, full/empty mbarriers) and ends
+// with a sentinel (u = n_units).  Every role reads its next unit from the ring,
+// so no role ever waits on global loads to find its work.
+struct Ring {
+  int* units;          // [kRing][kUnitWords]
+  uint64_t* full;      // [kRing], 1 arrival (scheduler)
+  uint64_t* empty;     // [kRing], kUnitConsumers arrivals
+};
+
+__device__ __forceinline__ void sched_units(const Args& a, const Ring& r, int lane) {
+  int k = 0;
+  const int grid = static_cast<int>(gridDim.x);
+  const int per = a.nseq * a.kv_heads;
+  auto publish = [&](int u, const Unit& it) {
+    const int slot = k % kRing;
+    if (k >= kRing) mbar_wait(&r.empty[slot], ((k / kRing) - 1) & 1);
+    if (lane == 0) {
+      int* e = r.units + slot * kUnitWords;
+      e[0] = u; e[1] = it.s; e[2] = it.g; e[3] = it.k0; e[4] = it.L; e[5] = it.q0; e[6] = it.qlen;
+      e[7] = it.lcp; e[8] = it.mb0; e[9] = it.nkt0; e[10] = it.nkt1;
+      mbar_arrive(&r.full[slot]);  // release: the entry is visible to the waiters
     }
-#pragma unroll
-    for (int i = 0; i < kScan; ++i) {
-      const int c = u + i * static_cast<int>(gridDim.x);
-      if (c >= a.n_units) return a.n_units;
+    __syncwarp();
+    ++k;
+  };
+  for (int base = static_cast<int>(blockIdx.x); base < a.n_units; base += 32 * grid) {
+    const int c = base + lane * grid;
+    bool ok = false;
+    Unit it;
+    if (c < a.n_units) {
+      const int sq = (c - (c / per) * per) / a.kv_heads;
+      const int q0 = __ldg(a.cu_q + sq), q1 = __ldg(a.cu_q + sq + 1);
       const int pair = a.max_pairs - 1 - c / per;
-      if (2 * pair * a.qpt < q1[i] - q0[i]) {  // query tile 0 of the pair exists
-        unit_geometry(a, c, k0[i], k1[i], q0[i], q1[i], it);
-        return c;
-      }
+      ok = 2 * pair * a.qpt < q1 - q0;  // query tile 0 of the pair exists
+      if (ok) unit_geometry(a, c, __ldg(a.cu + sq), __ldg(a.cu + sq + 1), q0, q1, it);
+    }
+    uint32_t valid = __ballot_sync(0xffffffffu, ok);
+    while (valid) {
+      const int l = __ffs(valid) - 1;
+      valid &= valid - 1;
+      Unit v;
+      v.s = __shfl_sync(0xffffffffu, it.s, l);
+      v.g = __shfl_sync(0xffffffffu, it.g, l);
+      v.k0 = __shfl_sync(0xffffffffu, it.k0, l);
+      v.L = __shfl_sync(0xffffffffu, it.L, l);
+      v.q0 = __shfl_sync(0xffffffffu, it.q0, l);
+      v.qlen = __shfl_sync(0xffffffffu, it.qlen, l);
+      v.lcp = __shfl_sync(0xffffffffu, it.lcp, l);
+      v.mb0 = __shfl_sync(0xffffffffu, it.mb0, l);
+      v.nkt0 = __shfl_sync(0xffffffffu, it.nkt0, l);
+      v.nkt1 = __shfl_sync(0xffffffffu, it.nkt1, l);
+      publish(base + l * grid, v);
     }
   }
-  return a.n_units;
+  Unit none;
+  none.nkt0 = none.nkt1 = 0;
+  none.s = none.g = none.k0 = none.L = none.q0 = none.qlen = none.lcp = none.mb0 = 0;
+  publish(a.n_units, none);  // sentinel
+}
+
+// Entry k of the ring (blocking until published); the calling warp releases the slot.
+__device__ __forceinline__ int ring_unit(const Ring& r, int k, Unit& it, int lane) {
+  const int slot = k % kRing;
+  mbar_wait(&r.full[slot], (k / kRing) & 1);
+  const int* e = r.units + slot * kUnitWords;
+  const int u = e[0];
+  it.s = e[1]; it.g = e[2]; it.k0 = e[3]; it.L = e[4]; it.q0 = e[5]; it.qlen = e[6];
+  it.lcp = e[7]; it.mb0 = e[8]; it.nkt0 = e[9]; it.nkt1 = e[10];
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&r.empty[slot]);
+  return u;
 }
 
 template <int HDP, int NQB, int NSLOT, uint32_t EMU>
@@ -375,6 +422,10 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
   uint64_t* l_full = o_free + 2;                 // [2 h][2 slots]: one barrier per sL slot, so the
                                                  // softmax can never run two phases ahead of a waiter
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(l_full + 4);
+  Ring ring;
+  ring.units = reinterpret_cast<int*>(smem + T::RING_OFF);
+  ring.full = reinterpret_cast<uint64_t*>(smem + T::RING_OFF + kRing * kUnitWords * 4);
+  ring.empty = ring.full + kRing;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -395,6 +446,10 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       mbar_init(&o_free[i], 128);
       mbar_init(&l_full[2 * i], 128);
       mbar_init(&l_full[2 * i + 1], 128);
+    }
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(&ring.full[i], 1);
+      mbar_init(&ring.empty[i], kUnitConsumers);
     }
     fence_mbar_init();
   }
@@ -421,7 +476,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       int q_cnt0 = 0, q_cnt1 = 0;
       uint32_t seq = 0;  // K/V ring sequence number (K and V tiles alternate)
       Unit it;
-      for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
+      for (int k = 0; ring_unit(ring, k, it, lane) < a.n_units; ++k) {
         // Q tiles of this unit
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -599,7 +654,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       auto wait_tile = [&](uint32_t seqno) { RDX_TWAIT(&t_full[seqno % NSLOT], (seqno / NSLOT) & 1, st_t); };
 
       Unit tmp, pre;
-      int ucur = next_unit(a, blockIdx.x, tmp);
+      int kcur = 0;  // ring entry of the current unit
+      int ucur = ring_unit(ring, 0, tmp, lane);
       int c0 = tmp.nkt0, c1 = tmp.nkt1, call = max(tmp.nkt0, tmp.nkt1);  // key tiles of the current unit
       int jcur = 0;
       int upre = a.n_units;  // the unit after the current one, fetched while S/softmax of this one run
@@ -608,7 +664,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         if (c0 > 0) issue_S(0, c0, 0, gt);
         if (c1 > 0) issue_S(1, c1, 0, gt);
         commit_elect(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
-        upre = next_unit(a, ucur + gridDim.x, pre);
+        upre = ring_unit(ring, kcur + 1, pre, lane);
       }
       while (ucur < a.n_units) {
         int unxt = ucur, jnxt = jcur + 1, n0 = c0, n1 = c1, nall = call;
@@ -640,8 +696,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         c1 = n1;
         call = nall;
         ++gt;
-        // new current unit: its S tiles are issued, so fetching the one after it overlaps the softmax
-        if (switched && ucur < a.n_units) upre = next_unit(a, ucur + gridDim.x, pre);
+        // new current unit: its S tiles are issued; the entry after it is already in the ring
+        if (switched) {
+          ++kcur;
+          if (ucur < a.n_units) upre = ring_unit(ring, kcur + 1, pre, lane);
+        }
       }
       if (lane == 0) RDX_EV_FLUSH();
       if (RDX_STATS_ON && lane == 0) {
@@ -652,6 +711,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         atomicAdd(a.stats + ST_MMA_ISSUE, static_cast<unsigned long long>(st_iss));
         atomicAdd(a.stats + ST_MMA_TOTAL, static_cast<unsigned long long>(clock64() - st_t0));
       }
+    } else if (warp == kSchedWarp) {
+      sched_units(a, ring, lane);
     } else if (warp >= 9 && warp <= 12) {
       // ---------------------------------------------------------------- epilogue: O_h / l -> bf16 compact rows
       const int q4 = warp & 3;            // TMEM lane quarter of this warp
@@ -663,7 +724,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       evl.n = 0;
       int cnt0 = 0, cnt1 = 0;
       Unit it;
-      for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
+      for (int k = 0; ring_unit(ring, k, it, lane) < a.n_units; ++k) {
 #pragma unroll 1
         for (int h = 0; h < 2; ++h) {
           if (!(h ? it.nkt1 : it.nkt0)) continue;
@@ -723,7 +784,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
     EvLog evl;
     evl.n = 0;
     Unit it;
-    for (int u = next_unit(a, blockIdx.x, it); u < a.n_units; u = next_unit(a, u + gridDim.x, it)) {
+    for (int k = 0; ring_unit(ring, k, it, lane) < a.n_units; ++k) {
       const int nkt_h = h ? it.nkt1 : it.nkt0;
       if (!nkt_h) continue;
       const int mb = it.mb0 + h;

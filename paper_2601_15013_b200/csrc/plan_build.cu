@@ -47,6 +47,9 @@ constexpr int64_t kSingleCtaTokens = 1024;  // up to here one CTA beats a cooper
 constexpr int64_t kClusterTokens = 65536;
 
 enum PlanMode { kSingle = 0, kCluster = 1, kGrid = 2 };
+// cu is staged in shared memory (per CTA) when it has at most this many entries: the
+// per-token sequence lookups (binary search, starts) then cost no L2 round trips.
+constexpr int64_t kSmemCu = 4096;
 
 __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
   k ^= k >> 33;
@@ -165,7 +168,13 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
   const uint64_t tmask = s.table_mask;
   const uint32_t* __restrict__ tok = a.tok;
   const uint32_t* __restrict__ pos = a.pos;
+  extern __shared__ int64_t s_cu[];  // [nseq + 1] when staged (dynamic smem sized by the launch)
   const int64_t* __restrict__ cu = a.cu;
+  if (nseq + 1 <= kSmemCu) {
+    for (int64_t q = threadIdx.x; q <= nseq; q += blockDim.x) s_cu[q] = a.cu[q];
+    __syncthreads();
+    cu = s_cu;
+  }
 
   // ---- validation of cu (device-side mirror of ragged.validate_batch) ----
   // bit0 start!=0, bit1 decrease, bit2 empty, bit3 end!=n
@@ -338,7 +347,8 @@ int max_coop_blocks() {
   static int cached = 0;
   if (cached == 0) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_build_kernel<kGrid>, kPlanThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plan_build_kernel<kGrid>, kPlanThreads,
+                                                      8 * kSmemCu) !=
         cudaSuccess)
       return 0;
     cached = per_sm * num_sms();
@@ -359,6 +369,7 @@ int cluster_ctas() {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(c);
       cfg.blockDim = dim3(kPlanThreads);
+      cfg.dynamicSmemBytes = 8 * kSmemCu;
       cudaLaunchAttribute attr;
       attr.id = cudaLaunchAttributeClusterDimension;
       attr.val.clusterDim.x = c;
@@ -435,8 +446,9 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
   if (want < 1) want = 1;
   const int grid = static_cast<int>(want < mg ? want : mg);
   void* params[] = {&a, &s};
+  const size_t dsmem = n_seqs + 1 <= kSmemCu ? static_cast<size_t>(8 * (n_seqs + 1)) : 0;
   if (n_tokens <= kSingleCtaTokens) {  // small batch: one CTA, no grid-wide barriers
-    plan_build_kernel<kSingle><<<1, kPlanThreads, 0, as_stream(stream)>>>(a, s);
+    plan_build_kernel<kSingle><<<1, kPlanThreads, dsmem, as_stream(stream)>>>(a, s);
     RDX_LAUNCH_CHECK();
     return RDX_OK;
   }
@@ -445,6 +457,7 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl);
     cfg.blockDim = dim3(kPlanThreads);
+    cfg.dynamicSmemBytes = dsmem;
     cfg.stream = as_stream(stream);
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
@@ -457,6 +470,6 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
     return RDX_OK;
   }
   RDX_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_build_kernel<kGrid>), dim3(grid),
-                                           dim3(kPlanThreads), params, 0, as_stream(stream)));
+                                           dim3(kPlanThreads), params, dsmem, as_stream(stream)));
   return RDX_OK;
 }

@@ -121,6 +121,26 @@ class _Workspace:
 _WORKSPACE = _Workspace()
 
 
+_PINNED = threading.local()
+
+
+def _read_info(info_cu, stream):
+    """D2H of (N', status, attempts, -, cu_q) through a reused pinned buffer (thread-local,
+    so concurrent planners on different threads do not share it)."""
+    import torch
+
+    k = info_cu.numel()
+    buf = getattr(_PINNED, "buf", None)
+    if buf is None or buf.numel() < k:
+        buf = torch.empty(max(k, 1024), dtype=torch.int32, pin_memory=True)
+        _PINNED.buf = buf
+    st = torch.cuda.current_stream(info_cu.device) if stream is None else stream
+    with torch.cuda.stream(st):
+        buf[:k].copy_(info_cu, non_blocking=True)
+    st.synchronize()
+    return buf[:k].numpy().copy()
+
+
 def build_plan_device(tok, pos, cu, *, allow_empty: bool = False, stream=None,
                       n_original: int | None = None) -> DevicePlan:
     """GPU planner on device tensors (tok/pos int32-viewed u32 [N], cu int64 [B+1]).
@@ -136,11 +156,12 @@ def build_plan_device(tok, pos, cu, *, allow_empty: bool = False, stream=None,
     b = int(cu.shape[0]) - 1
     if n >= (1 << 32) - 1:
         raise CapacityExceeded(f"{n} tokens exceed 32-bit index range")
-    gather = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    scatter = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    cpos = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
-    info_cu = torch.empty(4 + b + 1, dtype=torch.int32, device=dev)
-    lcp = torch.empty(max(b, 1), dtype=torch.int32, device=dev)
+    # one allocation for every output: gather | scatter | compact_positions | info+cu_q | lcp
+    nn, nb = max(n, 1), max(b, 1)
+    buf = torch.empty(3 * nn + (4 + b + 1) + nb, dtype=torch.int32, device=dev)
+    gather, scatter, cpos = buf[:nn], buf[nn:2 * nn], buf[2 * nn:3 * nn]
+    info_cu = buf[3 * nn:3 * nn + 4 + b + 1]
+    lcp = buf[3 * nn + 4 + b + 1:]
     scratch_bytes = int(lib.rdx_plan_scratch_bytes(n, b))
     scratch = _WORKSPACE.get(dev, scratch_bytes)
     flags = _native.RDX_PLAN_ALLOW_EMPTY if allow_empty else 0
@@ -152,7 +173,7 @@ def build_plan_device(tok, pos, cu, *, allow_empty: bool = False, stream=None,
         scratch.data_ptr(), ctypes.c_size_t(scratch.numel()), st,
     )
     _native.check(code, "rdx_plan_build")
-    host = info_cu.cpu().numpy()  # the one synchronising read
+    host = _read_info(info_cu, stream)  # the one synchronising read
     n_compact, status, attempts = int(host[0]), int(host[1]), int(host[2])
     raise_for_status(status, "rdx_plan_build")
     return DevicePlan(

@@ -33,7 +33,7 @@ st = torch.cuda.current_stream().cuda_stream
 
 
 def call(k):
-    libs[k].rdx_attention(ctypes.c_void_p(qkv.data_ptr()), ctypes.c_int64(qkv.stride(0)), ctypes.c_int64(m),
+    return libs[k].rdx_attention(ctypes.c_void_p(qkv.data_ptr()), ctypes.c_int64(qkv.stride(0)), ctypes.c_int64(m),
                           ctypes.c_void_p(sc.data_ptr()), ctypes.c_void_p(cu_t.data_ptr()),
                           ctypes.c_void_p(cuq_t.data_ptr()), ctypes.c_int64(B), ctypes.c_int32(maxq),
                           ctypes.c_int32(maxk), ctypes.c_int32(H), ctypes.c_int32(KV), ctypes.c_int32(hd),
@@ -44,7 +44,8 @@ def call(k):
 res = {k: [] for k in libs}
 for k in libs:
     for _ in range(3):
-        call(k)
+        rc = call(k)
+        assert rc == 0, (k, rc)
 torch.cuda.synchronize()
 for it in range(iters):
     for k in libs:
