@@ -264,6 +264,8 @@ int rdx_gemm_debug_shape(int cg, int block_n);
  * the row block varying fastest inside a group (0 = default; RDX_GEMM_GROUP_M in
  * the environment sets the same).  Returns the previous setting. */
 int rdx_gemm_debug_group_m(int group_m);
+/* Debug: raster group (row blocks) for GEMMs with K >= 8192 (default 16); returns the previous value. */
+int rdx_gemm_debug_group_m_bigk(int group_m);
 
 /* Debug: clock64 role counters of builds made with -DRDX_GEMM_STATS_BUILD (MMA
  * waits / epilogue waits and busy cycles, see gemm.cu); RDX_ERR_UNSUPPORTED
@@ -303,6 +305,8 @@ int rdx_attention_debug_stats(unsigned long long* host, int n);
 /* Debug: event log of CTA 0 of the last launch in the same mode:
  * [count, (clock, code) x min(count, 4096)] as 32-bit words. */
 int rdx_attention_debug_trace(uint32_t* host, int n_words);
+/* Debug (stats builds): per-CTA [start ns, end ns, units] of the last launch, n_ctas <= 1024 entries. */
+int rdx_attention_debug_cta_times(unsigned long long* host, int n_ctas);
 
 /* ---------------------------------------------------------------------
  * Reranker scores from last-token logits (fp32 [B, ld]):

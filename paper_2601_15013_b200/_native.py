@@ -46,6 +46,8 @@ EXPORTS = (
     "rdx_attention",
     "rdx_attention_debug_stats",
     "rdx_attention_debug_trace",
+    "rdx_attention_debug_cta_times",
+    "rdx_gemm_debug_group_m_bigk",
     "rdx_rerank_scores",
     "rdx_num_sms",
 )
@@ -138,6 +140,8 @@ _SIGNATURES = {
                                       _vp]),
     "rdx_attention_debug_stats": (ctypes.c_int, [_vp, _i32]),
     "rdx_attention_debug_trace": (ctypes.c_int, [_vp, _i32]),
+    "rdx_attention_debug_cta_times": (ctypes.c_int, [_vp, _i32]),
+    "rdx_gemm_debug_group_m_bigk": (ctypes.c_int, [_i32]),
     "rdx_num_sms": (ctypes.c_int, []),
 }
 

@@ -246,7 +246,9 @@ struct Args {
   int use_tma;               // head_dim % 64 == 0: whole 128-byte column boxes, TMA tile loads
   float scale_log2;          // softmax scale * log2(e)
   unsigned long long* stats; // debug (RDX_ATTN_STATS_BUILD + RDX_ATTN_STATS=1): summed clocks per role
-  uint32_t* trace;           // debug: CTA 0 event log [count, (clock, code) x 4096]
+  uint32_t* trace;           // debug: event log of CTA trace_cta [count, (clock, code) x 4096]
+  int trace_cta;             // debug: which CTA the event log follows (RDX_ATTN_TRACE_CTA, default 0)
+  unsigned long long* cta_times;  // debug: per CTA [start, end, units] (globaltimer ns)
 };
 
 // Stats slots (summed over CTAs): see rdx_attention_debug_stats.
@@ -276,7 +278,7 @@ struct EvLog {
 };
 #define RDX_EV(role, ev, payload)                                                    \
   do {                                                                               \
-    if (RDX_STATS_ON && a.trace && blockIdx.x == 0 && evl.n < 96) {                  \
+    if (RDX_STATS_ON && a.trace && blockIdx.x == a.trace_cta && evl.n < 96) {        \
       evl.tm[evl.n] = static_cast<uint32_t>(clock64());                              \
       evl.code[evl.n] = ((role) << 12) | ((ev) << 8) | ((payload) & 0xFF);           \
       ++evl.n;                                                                       \
@@ -284,7 +286,7 @@ struct EvLog {
   } while (0)
 #define RDX_EV_FLUSH()                                                               \
   do {                                                                               \
-    if (RDX_STATS_ON && a.trace && blockIdx.x == 0 && evl.n > 0) {                   \
+    if (RDX_STATS_ON && a.trace && blockIdx.x == a.trace_cta && evl.n > 0) {         \
       const uint32_t _b = atomicAdd(a.trace, static_cast<uint32_t>(evl.n));          \
       for (int _i = 0; _i < evl.n; ++_i)                                             \
         if (_b + _i < 4096) {                                                        \
@@ -385,6 +387,7 @@ __device__ __forceinline__ void sched_units(const Args& a, const Ring& r, int la
   none.nkt0 = none.nkt1 = 0;
   none.s = none.g = none.k0 = none.L = none.q0 = none.qlen = none.lcp = none.mb0 = 0;
   publish(a.n_units, none);  // sentinel
+  if (RDX_STATS_ON && a.cta_times && lane == 0) a.cta_times[3 * blockIdx.x + 2] = static_cast<unsigned long long>(k - 1);
 }
 
 // Entry k of the ring (blocking until published); the calling warp releases the slot.
@@ -464,6 +467,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
   // barrier init + TMEM alloc overlapped the previous kernel's tail (PDL); inputs from here on
   pdl_wait();
   pdl_launch_dependents();
+  if (RDX_STATS_ON && a.cta_times && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.cta_times[3 * blockIdx.x] = t;
+  }
 
   if (warp >= 8) {
     setmaxnreg_dec<80>();
@@ -897,6 +905,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
   }
   tc_fence_before();
   __syncthreads();
+  if (RDX_STATS_ON && a.cta_times && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.cta_times[3 * blockIdx.x + 1] = t;
+  }
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
@@ -904,6 +917,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 }
 
 unsigned long long* g_stats = nullptr;  // debug counters (RDX_ATTN_STATS=1)
+unsigned long long* g_cta_times = nullptr;  // debug per-CTA [start, end, units]
 uint32_t* g_trace = nullptr;            // debug event log of CTA 0 (RDX_ATTN_STATS=1)
 
 template <int HDP, int NQB, int NSLOT, uint32_t EMU>
@@ -977,6 +991,8 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
               qkv_rows < (int64_t(1) << 31) && ld_qkv < (int64_t(1) << 31);
   a.stats = nullptr;
   a.trace = nullptr;
+  a.trace_cta = 0;
+  a.cta_times = nullptr;
   if (const char* e = std::getenv("RDX_ATTN_STATS")) {
     if (e[0] == '1') {
       if (!g_stats) {
@@ -987,6 +1003,9 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
       if (!g_trace) RDX_CUDA_TRY(cudaMalloc(&g_trace, (2 + 2 * 4096) * sizeof(uint32_t)));
       RDX_CUDA_TRY(cudaMemsetAsync(g_trace, 0, 2 * sizeof(uint32_t), as_stream(stream)));
       a.trace = g_trace;
+      if (const char* tc = std::getenv("RDX_ATTN_TRACE_CTA")) a.trace_cta = atoi(tc);
+      if (!g_cta_times) RDX_CUDA_TRY(cudaMalloc(&g_cta_times, 3 * 1024 * sizeof(unsigned long long)));
+      a.cta_times = g_cta_times;
     }
   }
   // short units (few key tiles): double-buffer Q; long units: deeper K/V ring
@@ -1005,6 +1024,14 @@ extern "C" int rdx_attention_debug_stats(unsigned long long* host, int n) {
   const int m = n < ST_N ? n : ST_N;
   RDX_CUDA_TRY(cudaMemcpy(host, g_stats, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   RDX_CUDA_TRY(cudaMemset(g_stats, 0, ST_N * sizeof(unsigned long long)));
+  return RDX_OK;
+}
+
+// Debug: per-CTA [start ns, end ns, units] of the last launch (stats builds), n_ctas entries.
+extern "C" int rdx_attention_debug_cta_times(unsigned long long* host, int n_ctas) {
+  using namespace rdx::attn;
+  if (!g_cta_times || n_ctas <= 0 || n_ctas > 1024) return RDX_ERR_INVALID_ARGUMENT;
+  RDX_CUDA_TRY(cudaMemcpy(host, g_cta_times, 3 * n_ctas * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   return RDX_OK;
 }
 

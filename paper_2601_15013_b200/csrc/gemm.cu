@@ -813,6 +813,19 @@ int group_m_setting() {
   return g_group_m;
 }
 
+// Row blocks per raster group for K >= 8192 (the C4 down projection, K = 12288): a
+// 16-row-block group of A is 100 MB there and does not stay L2-resident next to B.
+// RDX_GEMM_GROUP_M_BIGK (env) / rdx_gemm_debug_group_m_bigk for A/B runs.
+int g_group_m_bigk = -1;
+int group_m_bigk_setting() {
+  if (g_group_m_bigk == -1) {
+    const char* e = getenv("RDX_GEMM_GROUP_M_BIGK");
+    g_group_m_bigk = e ? atoi(e) : 16;
+    if (g_group_m_bigk <= 0) g_group_m_bigk = 16;
+  }
+  return g_group_m_bigk;
+}
+
 // RDX_GEMM_TAIL_SPLIT=0 (env) or rdx_gemm_debug_tail_split(0) disables the tail split (A/B runs).
 int g_tail_split = -1;
 bool tail_split_enabled() {
@@ -889,7 +902,8 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
     // K-scaled group size (A rows of a group ~48 MB) were equal or slower).  Few row blocks (C2): the legacy orders (row-block-major when a
     // completion counter is attached).
     int gm = group_m_setting();
-    if (gm <= 0) gm = m_tiles >= 64 ? 16 : (ep.done_ctr ? 1 : static_cast<int>(m_tiles));
+    if (gm <= 0) gm = m_tiles >= 64 ? (a.k >= 8192 ? group_m_bigk_setting() : 16)
+                                     : (ep.done_ctr ? 1 : static_cast<int>(m_tiles));
     ep.group_m = static_cast<int>(gm < m_tiles ? gm : m_tiles);
   }
   const int64_t tiles = ((a.m + BM * CG - 1) / (BM * CG)) * ((a.n + BN - 1) / BN);
@@ -1074,6 +1088,12 @@ extern "C" int rdx_gemm_debug_stats(unsigned long long* out8, int reset) {
 extern "C" int rdx_gemm_debug_group_m(int group_m) {
   const int prev = rdx::gemm::group_m_setting();
   rdx::gemm::g_group_m = group_m < 0 ? 0 : group_m;
+  return prev;
+}
+
+extern "C" int rdx_gemm_debug_group_m_bigk(int group_m) {
+  const int prev = rdx::gemm::group_m_bigk_setting();
+  rdx::gemm::g_group_m_bigk = group_m <= 0 ? 16 : group_m;
   return prev;
 }
 

@@ -16,6 +16,9 @@ lib = _native.lib()
 if what == "group":  # GEMM raster: G_ON vs G_OFF row blocks per group (captured into each arm's graph)
     def setter(on):
         lib.rdx_gemm_debug_group_m(int(os.environ.get("G_ON", "16") if on else os.environ.get("G_OFF", "0")))
+elif what == "groupk":  # raster group of the K >= 8192 GEMMs only (C4 down): G_ON vs G_OFF
+    def setter(on):
+        lib.rdx_gemm_debug_group_m_bigk(int(os.environ.get("G_ON", "6") if on else os.environ.get("G_OFF", "16")))
 elif what == "norm":  # model-level switch: rmsnorm overlapping the residual GEMM's tail
     def setter(on):
         os.environ["RDX_NORM_OVERLAP"] = str(on)

@@ -132,3 +132,22 @@ if os.environ.get("RDX_ATTN_TRACE") == "1":
         role, e, pl = code >> 12, (code >> 8) & 15, code & 255
         print(f"{(tt - t0) & 0xffffffff:9d} {roles.get(role, role)} {names.get((role, e), e):9s} h={pl >> 4} j={pl & 15}"
               + (f" [{'box' if pl & 0x80 else 'r16' if pl & 0x40 else 'g4'}]" if role == 0 else ""))
+if os.environ.get("RDX_ATTN_STATS") == "1":
+    import ctypes
+
+    ours()
+    torch.cuda.synchronize()
+    nct = torch.cuda.get_device_properties(0).multi_processor_count
+    buf = (ctypes.c_ulonglong * (3 * nct))()
+    if lib.rdx_attention_debug_cta_times(buf, nct) == 0:
+        st = np.array([buf[3 * i] for i in range(nct)], dtype=np.float64)
+        en = np.array([buf[3 * i + 1] for i in range(nct)], dtype=np.float64)
+        un = np.array([buf[3 * i + 2] for i in range(nct)])
+        t0 = st.min()
+        print("CTA start us: min 0 max %.2f | end us: min %.2f median %.2f max %.2f (CTA %d)" %
+              ((st.max() - t0) / 1e3, (en.min() - t0) / 1e3, np.median(en - t0) / 1e3, (en.max() - t0) / 1e3,
+               int(en.argmax())))
+        for u in sorted(set(un.tolist())):
+            sel = un == u
+            print(f"  {int(sel.sum()):4d} CTAs with {u} units: end us median {np.median(en[sel] - t0) / 1e3:.2f} "
+                  f"max {(en[sel] - t0).max() / 1e3:.2f}; busy us median {np.median(en[sel] - st[sel]) / 1e3:.2f}")
