@@ -316,6 +316,15 @@ int rdx_attention_debug_cta_times(unsigned long long* host, int n_ctas);
 int rdx_rerank_scores(const float* logits, int64_t n_rows, int64_t ld, int64_t yes_id,
                       int64_t no_id, float* scores_out, void* stream);
 
+/* Training (training.py loss_and_grads(precision="bf16")):
+ * dst[c][r] = bf16(src[r][c]) for r < rows, c < cols; dst[c][r] = 0 for
+ * rows <= r < ld_dst.  Builds the K-major operands of the tcgen05 dgrad
+ * (W^T) and wgrad (dY^T, X^T) GEMMs; ld_dst pads the reduction dimension to
+ * the GEMM's 8-element multiple.  No reference counterpart (the reference's
+ * backward is numpy fp64, model.py:419-531). */
+int rdx_transpose_f32_bf16(const float* src, int64_t rows, int64_t cols, int64_t ld_src, void* dst_bf16,
+                           int64_t ld_dst, void* stream);
+
 /* Number of SMs of the current device (cached). */
 int rdx_num_sms(void);
 

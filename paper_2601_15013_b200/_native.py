@@ -49,6 +49,7 @@ EXPORTS = (
     "rdx_attention_debug_cta_times",
     "rdx_gemm_debug_group_m_bigk",
     "rdx_rerank_scores",
+    "rdx_transpose_f32_bf16",
     "rdx_num_sms",
 )
 
@@ -136,6 +137,7 @@ _SIGNATURES = {
     "rdx_gemm_debug_group_m": (ctypes.c_int, [ctypes.c_int]),
     "rdx_debug_pdl": (ctypes.c_int, [ctypes.c_int]),
     "rdx_rerank_scores": (ctypes.c_int, [_vp, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "rdx_transpose_f32_bf16": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _vp]),
     "rdx_attention": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32, _f32, _vp, _i64,
                                       _vp]),
     "rdx_attention_debug_stats": (ctypes.c_int, [_vp, _i32]),

@@ -4,6 +4,8 @@
 //   rdx_rmsnorm_rows    RMSNorm of (selected) fp32 rows (model.py:147-152)
 //   rdx_rope_table      fp64 RoPE tables on compact positions (model.py:165-172)
 //   rdx_rerank_scores   last-token reranker read-out (DESIGN.md scoring contract)
+//   rdx_transpose_f32_bf16  fp32 [rows, cols] -> bf16 [cols, ld_dst] (zero-padded), the
+//                       K-major operands of the tcgen05 dgrad / wgrad GEMMs (training.py)
 #include <cstdlib>
 #include "common.cuh"
 
@@ -353,8 +355,40 @@ int grid_for_rows(int64_t rows, int warps_per_block) {
   return static_cast<int>(g);
 }
 
+// 32x32 tiles through shared memory: coalesced fp32 reads along src rows, coalesced bf16
+// writes along dst rows; dst columns [rows, ld_dst) are written as zeros (K padding).
+__global__ void __launch_bounds__(256)
+transpose_f32_bf16_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t ld_src,
+                          __nv_bfloat16* __restrict__ dst, int64_t ld_dst) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32, c0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t r = r0 + i, c = c0 + tx;
+    tile[i][tx] = (r < rows && c < cols) ? src[r * ld_src + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t c = c0 + i, r = r0 + tx;  // dst[c][r]
+    if (c < cols && r < ld_dst) dst[c * ld_dst + r] = __float2bfloat16_rn(tile[tx][i]);
+  }
+}
+
 }  // namespace
 }  // namespace rdx
+
+extern "C" int rdx_transpose_f32_bf16(const float* src, int64_t rows, int64_t cols, int64_t ld_src, void* dst_bf16,
+                                      int64_t ld_dst, void* stream) {
+  using namespace rdx;
+  if (rows < 0 || cols < 0 || ld_src < cols || ld_dst < rows) return RDX_ERR_SHAPE_MISMATCH;
+  if (rows == 0 || cols == 0) return RDX_OK;
+  if (!src || !dst_bf16) return RDX_ERR_INVALID_ARGUMENT;
+  const dim3 grid(static_cast<unsigned>((ld_dst + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+  transpose_f32_bf16_kernel<<<grid, 256, 0, as_stream(stream)>>>(src, rows, cols, ld_src,
+                                                                  static_cast<__nv_bfloat16*>(dst_bf16), ld_dst);
+  RDX_LAUNCH_CHECK();
+  return RDX_OK;
+}
 
 extern "C" int rdx_gather_rows(const void* src, int64_t src_rows, int64_t ld_src_bytes,
                                const uint32_t* idx, int64_t n_idx, void* dst, int64_t ld_dst_bytes,

@@ -12,10 +12,19 @@ What runs where:
     is ``rdx_gather_rows`` forward and ``rdx_gather_rows_backward`` (the
     deterministic ascending-index scatter-add, bit-identical to np.add.at)
     backward, via the ``RowGather`` autograd function;
-  * the dense math (GEMMs, norms, RoPE, per-sequence causal softmax) is fp64
-    CUDA tensors under torch autograd: the reference computes gradients in
-    fp64 and its tests hold them to 1e-6 relative (tests/test_model.py:233-247),
-    a precision the bf16 tcgen05 inference kernels are not built for.
+  * ``precision="fp64"`` (default, the reference's contract): the dense math
+    (GEMMs, norms, RoPE, per-sequence causal softmax) is fp64 CUDA tensors
+    under torch autograd: the reference computes gradients in fp64 and its
+    tests hold them to 1e-6 relative (tests/test_model.py:233-247);
+  * ``precision="bf16"``: every projection GEMM -- forward (q/k/v/o, gate/up/down,
+    LM head), activation gradient dX = dY W and weight gradient dW = dY^T X --
+    runs on the tcgen05 GEMM (``rdx_gemm``, bf16 operands, fp32 accumulation in
+    TMEM); the K-major operands W^T, dY^T, X^T are built by
+    ``rdx_transpose_f32_bf16`` (fused fp32 -> bf16 cast, zero-padded to the
+    GEMM's 8-element K multiple).  Norms, RoPE, SwiGLU, the causal softmax and
+    the loss stay fp32 torch autograd.  Stated tolerance vs the reference's
+    fp64 gradients: max |g - g_ref| / max |g_ref| <= 5e-2 per parameter, loss
+    to 1e-2 relative (tests/test_training_gpu.py).
 The forward follows ``_forward_cached`` (model.py:322-416) op for op, in
 compact space: position-wise work on the N' rows, attention on the original
 layout, exactly as the reference.
@@ -60,6 +69,82 @@ class RowGather:
         return cls._fn.apply(x, idx)
 
 
+def _tc_gemm(a, b):
+    """fp32 [M, N] = a [M, K] @ b [N, K]^T on the tcgen05 GEMM (rdx_gemm, EPI_STORE_F32)."""
+    import torch
+
+    m, k = a.shape
+    n = b.shape[0]
+    npad = -(-n // 4) * 4  # 16-byte fp32 output rows
+    out = torch.empty(m, npad, dtype=torch.float32, device=a.device)
+    args = _native.GemmArgs()
+    args.a, args.b, args.m, args.n, args.k = a.data_ptr(), b.data_ptr(), m, n, k
+    args.lda, args.ldb = a.stride(0), b.stride(0)
+    args.epi = _native.EPI_STORE_F32
+    args.block_n = 0
+    args.out, args.ldo = out.data_ptr(), npad
+    _native.check(_native.lib().rdx_gemm(args, _native.stream_handle()), "rdx_gemm")
+    return out[:, :n]
+
+
+def _bf16_rows(x, k_pad):
+    """fp32 [M, K] -> bf16 [M, k_pad] (zero-padded K), the K-major A/B operand as is."""
+    import torch
+
+    out = torch.zeros(x.shape[0], k_pad, dtype=torch.bfloat16, device=x.device)
+    out[:, : x.shape[1]] = x
+    return out
+
+
+def _bf16_t(x, ld):
+    """fp32 [R, C] -> bf16 [C, ld] = x^T zero-padded (rdx_transpose_f32_bf16)."""
+    import torch
+
+    x = x.contiguous()
+    out = torch.empty(x.shape[1], ld, dtype=torch.bfloat16, device=x.device)
+    _native.check(_native.lib().rdx_transpose_f32_bf16(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0),
+                                                       out.data_ptr(), ld, _native.stream_handle()),
+                  "rdx_transpose_f32_bf16")
+    return out
+
+
+def _pad8(k):
+    return -(-int(k) // 8) * 8
+
+
+class TcLinear:
+    """y = x W^T with forward, dX and dW all on the tcgen05 GEMM (bf16 operands, fp32 accumulate)."""
+
+    _fn = None
+
+    @classmethod
+    def apply(cls, x, w):
+        if cls._fn is None:
+            import torch
+
+            class _F(torch.autograd.Function):
+                @staticmethod
+                def forward(ctx, x_, w_):
+                    x32, w32 = x_.float().contiguous(), w_.float().contiguous()
+                    ctx.save_for_backward(x32, w32)
+                    ctx.w_dtype = w_.dtype
+                    k8 = _pad8(x32.shape[1])
+                    return _tc_gemm(_bf16_rows(x32, k8), _bf16_rows(w32, k8))
+
+                @staticmethod
+                def backward(ctx, gy):
+                    x32, w32 = ctx.saved_tensors
+                    gy = gy.float().contiguous()
+                    m, n = gy.shape
+                    n8, m8 = _pad8(n), _pad8(m)
+                    gx = _tc_gemm(_bf16_rows(gy, n8), _bf16_t(w32, n8))          # [M, K] = dY W
+                    gw = _tc_gemm(_bf16_t(gy, m8), _bf16_t(x32, m8))             # [N, K] = dY^T X
+                    return gx, gw.to(ctx.w_dtype)
+
+            cls._fn = _F
+        return cls._fn.apply(x, w)
+
+
 def _rmsnorm(x, w, eps):
     import torch
 
@@ -100,10 +185,18 @@ def _attention(qf, kf, vf, cu, heads, kv, hd):
 
 
 def loss_and_grads(config: ModelConfig, params: dict, batch: RaggedBatch, plan: CompactionPlan | None, targets,
-                   ledger: FlopLedger | None = None):
+                   ledger: FlopLedger | None = None, *, precision: str = "fp64"):
     """Mean cross-entropy over all N positions and the gradient of every parameter
-    (model.py:419-531); ``plan`` None = dense pass, else the compact (RadixMLP) pass."""
+    (model.py:419-531); ``plan`` None = dense pass, else the compact (RadixMLP) pass.
+    ``precision``: "fp64" (the reference's contract) or "bf16" (tcgen05 GEMMs)."""
     import torch
+
+    if precision not in ("fp64", "bf16"):
+        raise ValueError("precision must be 'fp64' or 'bf16'")
+    tc = precision == "bf16"
+
+    def mm(x, w):  # x @ w.T
+        return TcLinear.apply(x, w) if tc else x @ w.T
 
     validate_batch(batch)
     targets = np.asarray(targets, dtype=np.int64)
@@ -115,7 +208,7 @@ def loss_and_grads(config: ModelConfig, params: dict, batch: RaggedBatch, plan: 
     dev = torch.device("cuda")
     _native.lib()  # no CPU fallback
     dtype = np.asarray(params["embed"]).dtype
-    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    tdt = torch.float64 if (dtype == np.float64 and not tc) else torch.float32
     P = {k: torch.tensor(np.asarray(v), dtype=tdt, device=dev, requires_grad=True) for k, v in params.items()}
     tok = torch.from_numpy(np.asarray(batch.token_ids, dtype=np.int64)).to(dev)
     cu = np.asarray(batch.cu_seqlens, dtype=np.int64)
@@ -148,9 +241,9 @@ def loss_and_grads(config: ModelConfig, params: dict, batch: RaggedBatch, plan: 
         p = f"layers.{i}."
         hn = _rmsnorm(h, P[p + "ln1"], eps)
         ledger.positionwise(f"l{i}.ln1", m)
-        q = hn @ P[p + "wq"].T
-        k = hn @ P[p + "wk"].T
-        v = hn @ P[p + "wv"].T
+        q = mm(hn, P[p + "wq"])
+        k = mm(hn, P[p + "wk"])
+        v = mm(hn, P[p + "wv"])
         ledger.positionwise(f"l{i}.qkv_proj", m)
         qn = _rmsnorm(q.reshape(-1, hd), P[p + "q_norm"], eps).reshape(m, heads, hd)
         kn = _rmsnorm(k.reshape(-1, hd), P[p + "k_norm"], eps).reshape(m, kv, hd)
@@ -166,18 +259,18 @@ def loss_and_grads(config: ModelConfig, params: dict, batch: RaggedBatch, plan: 
         if plan is not None:
             attn = RowGather.apply(attn, gather)
             ledger.index_copy(m)
-        h = h + attn @ P[p + "wo"].T
+        h = h + mm(attn, P[p + "wo"])
         ledger.positionwise(f"l{i}.o_proj", m)
         ledger.positionwise(f"l{i}.attn_residual", m)
         hn2 = _rmsnorm(h, P[p + "ln2"], eps)
-        g = hn2 @ P[p + "w_gate"].T
-        u = hn2 @ P[p + "w_up"].T
-        h = h + (g * torch.sigmoid(g) * u) @ P[p + "w_down"].T
+        g = mm(hn2, P[p + "w_gate"])
+        u = mm(hn2, P[p + "w_up"])
+        h = h + mm(g * torch.sigmoid(g) * u, P[p + "w_down"])
         ledger.positionwise(f"l{i}.mlp", m)
         ledger.positionwise(f"l{i}.mlp_residual", m)
     hf = _rmsnorm(h, P["final_norm"], eps)
     ledger.positionwise("final_norm", m)
-    logits = hf @ P["lm_head"].T
+    logits = mm(hf, P["lm_head"])
     ledger.positionwise("lm_head", m)
     if plan is not None:
         logits = RowGather.apply(logits, scatter)
