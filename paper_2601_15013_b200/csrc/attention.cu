@@ -327,11 +327,16 @@ __device__ __forceinline__ void unit_geometry(const Args& a, int u, int k0, int 
   it.nkt1 = mb1 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (mb1 + 1) * a.qpt) + BK - 1) / BK : 0;
 }
 
-// The CTA's units are u = blockIdx.x + k * gridDim.x in order; the scheduler
-// warp evaluates 32 candidates per step (one L2 round trip), publishes the valid
-// ones into a shared-memory ring (kRing entries, full/empty mbarriers) and ends
-// with a sentinel (u = n_units).  Every role reads its next unit from the ring,
-// so no role ever waits on global loads to find its work.
+// Work distribution.  The valid units (a query-tile pair that exists) are
+// numbered densely in (pair level descending, sequence, kv head) order -- the
+// longest key ranges first -- and dealt to the CTAs in snake order (round r
+// gives dense unit r*G + c to CTA c when r is even, r*G + G-1-c when odd), so
+// every CTA gets the same number of units up to one, heavy ones spread evenly.
+// Each CTA's scheduler warp walks the (level, sequence) grid 32 sequences per
+// step (one L2 round trip for cu_q), picks out its own units, publishes them
+// into a shared-memory ring (kRing entries, full/empty mbarriers) and ends with
+// a sentinel (u = n_units).  Every role reads its next unit from the ring, so no
+// role ever waits on global loads to find its work.
 struct Ring {
   int* units;          // [kRing][kUnitWords]
   uint64_t* full;      // [kRing], 1 arrival (scheduler)
@@ -340,8 +345,7 @@ struct Ring {
 
 __device__ __forceinline__ void sched_units(const Args& a, const Ring& r, int lane) {
   int k = 0;
-  const int grid = static_cast<int>(gridDim.x);
-  const int per = a.nseq * a.kv_heads;
+  const int G = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
   auto publish = [&](int u, const Unit& it) {
     const int slot = k % kRing;
     if (k >= kRing) mbar_wait(&r.empty[slot], ((k / kRing) - 1) & 1);
@@ -354,33 +358,42 @@ __device__ __forceinline__ void sched_units(const Args& a, const Ring& r, int la
     __syncwarp();
     ++k;
   };
-  for (int base = static_cast<int>(blockIdx.x); base < a.n_units; base += 32 * grid) {
-    const int c = base + lane * grid;
-    bool ok = false;
-    Unit it;
-    if (c < a.n_units) {
-      const int sq = (c - (c / per) * per) / a.kv_heads;
-      const int q0 = __ldg(a.cu_q + sq), q1 = __ldg(a.cu_q + sq + 1);
-      const int pair = a.max_pairs - 1 - c / per;
-      ok = 2 * pair * a.qpt < q1 - q0;  // query tile 0 of the pair exists
-      if (ok) unit_geometry(a, c, __ldg(a.cu + sq), __ldg(a.cu + sq + 1), q0, q1, it);
-    }
-    uint32_t valid = __ballot_sync(0xffffffffu, ok);
-    while (valid) {
-      const int l = __ffs(valid) - 1;
-      valid &= valid - 1;
-      Unit v;
-      v.s = __shfl_sync(0xffffffffu, it.s, l);
-      v.g = __shfl_sync(0xffffffffu, it.g, l);
-      v.k0 = __shfl_sync(0xffffffffu, it.k0, l);
-      v.L = __shfl_sync(0xffffffffu, it.L, l);
-      v.q0 = __shfl_sync(0xffffffffu, it.q0, l);
-      v.qlen = __shfl_sync(0xffffffffu, it.qlen, l);
-      v.lcp = __shfl_sync(0xffffffffu, it.lcp, l);
-      v.mb0 = __shfl_sync(0xffffffffu, it.mb0, l);
-      v.nkt0 = __shfl_sync(0xffffffffu, it.nkt0, l);
-      v.nkt1 = __shfl_sync(0xffffffffu, it.nkt1, l);
-      publish(base + l * grid, v);
+  int64_t dense = 0;  // dense index of the first unit of the current chunk
+  for (int pair = a.max_pairs - 1; pair >= 0; --pair) {
+    for (int s0 = 0; s0 < a.nseq; s0 += 32) {
+      const int sq = s0 + lane;
+      int k0 = 0, k1 = 0, q0 = 0, q1 = 0;
+      bool ok = false;
+      if (sq < a.nseq) {
+        q0 = __ldg(a.cu_q + sq);
+        q1 = __ldg(a.cu_q + sq + 1);
+        ok = 2 * pair * a.qpt < q1 - q0;  // query tile 0 of the pair exists
+        if (ok) {
+          k0 = __ldg(a.cu + sq);
+          k1 = __ldg(a.cu + sq + 1);
+        }
+      }
+      const uint32_t bits = __ballot_sync(0xffffffffu, ok);
+      const int64_t cnt = static_cast<int64_t>(__popc(bits)) * a.kv_heads;
+      // this CTA's dense indices in [dense, dense + cnt): one candidate per snake round
+      for (int64_t rd = dense / G; rd * G < dense + cnt; ++rd) {
+        const int64_t d = rd * G + ((rd & 1) ? (G - 1 - c) : c);
+        if (d < dense || d >= dense + cnt) continue;
+        const int e = static_cast<int>(d - dense);
+        const int nth = e / a.kv_heads;  // nth valid sequence of the chunk
+        int l = 0;
+        uint32_t b = bits;
+        for (int i = 0; i < nth; ++i) b &= b - 1;
+        l = __ffs(b) - 1;
+        Unit it;
+        const int qa = __shfl_sync(0xffffffffu, q0, l), qb = __shfl_sync(0xffffffffu, q1, l);
+        const int ka = __shfl_sync(0xffffffffu, k0, l), kb = __shfl_sync(0xffffffffu, k1, l);
+        const int g = e - nth * a.kv_heads;
+        const int u = (a.max_pairs - 1 - pair) * (a.nseq * a.kv_heads) + (s0 + l) * a.kv_heads + g;
+        unit_geometry(a, u, ka, kb, qa, qb, it);
+        publish(u, it);
+      }
+      dense += cnt;
     }
   }
   Unit none;
@@ -807,22 +820,32 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         RDX_TWAIT(&s_full[h], s_cnt & 1, st_s);
         if (t == 0) RDX_EV(2, 1, h * 16 + j);  // softmax: S_h(j) ready
         tc_fence_after();
+        const int kbase = j * BK;
+        // warp-uniform column classes of this tile (32-column chunks): chunks at or past
+        // vis_warp are masked for every row of the warp (never loaded, max'ed or exp'ed);
+        // chunks below lo_vis are visible for every row (no per-element mask)
+        const int vis_warp = pos_max - kbase + 1;
+        const int lo_vis = pos_min - kbase + 1;
         float sv[BK];
 #pragma unroll
-        for (int c = 0; c < BK; c += 32) tmem_ld32p(s_addr + c, sv + c);
+        for (int c = 0; c < BK; c += 32)
+          if (c < vis_warp) tmem_ld32p(s_addr + c, sv + c);
         tmem_wait_ld();
         if (t == 0) RDX_EV(2, 3, static_cast<int>(sv[0] != 12345.f));  // softmax: S in registers
-        const int kbase = j * BK;
-        if (kbase + BK - 1 > pos_min) {  // warp-uniform: some key of this warp's rows is masked
-          const int nvis = pos - kbase + 1;  // visible keys of this row in the tile
-#pragma unroll
-          for (int c = 0; c < BK; ++c) sv[c] = c < nvis ? sv[c] : -INFINITY;
-        }
+        const int nvis = pos - kbase + 1;  // visible keys of this row in the tile
         float mx[8];
 #pragma unroll
-        for (int u8 = 0; u8 < 8; ++u8) mx[u8] = sv[u8];
+        for (int u8 = 0; u8 < 8; ++u8) mx[u8] = -INFINITY;
 #pragma unroll
-        for (int c = 8; c < BK; ++c) mx[c & 7] = fmaxf(mx[c & 7], sv[c]);
+        for (int c0 = 0; c0 < BK; c0 += 32) {
+          if (c0 >= vis_warp) continue;  // whole chunk masked for the warp (column 0 is always visible)
+          if (c0 + 32 > lo_vis) {         // the diagonal crosses this chunk: per-element mask
+#pragma unroll
+            for (int c = c0; c < c0 + 32; ++c) sv[c] = c < nvis ? sv[c] : -INFINITY;
+          }
+#pragma unroll
+          for (int c = c0; c < c0 + 32; ++c) mx[c & 7] = fmaxf(mx[c & 7], sv[c]);
+        }
         const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * a.scale_log2;
         const bool need = mt > m_run + kRescaleThreshold;
@@ -849,7 +872,6 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         if (t == 0) RDX_EV(2, 4, h * 16 + j);  // softmax: max done
         const uint64_t scale2 = f2pack(a.scale_log2, a.scale_log2), negm2 = f2pack(-m_run, -m_run);
         uint64_t ls[4] = {0, 0, 0, 0};  // pairs of fp32 partial row sums (+0.0f bits)
-        const int vis_warp = pos_max - kbase + 1;  // columns >= vis_warp are masked for the whole warp
 #pragma unroll
         for (int c = 0; c < BK; c += 32) {
           uint32_t pw[16];

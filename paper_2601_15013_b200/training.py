@@ -23,7 +23,7 @@ What runs where:
     ``rdx_transpose_f32_bf16`` (fused fp32 -> bf16 cast, zero-padded to the
     GEMM's 8-element K multiple).  Norms, RoPE, SwiGLU, the causal softmax and
     the loss stay fp32 torch autograd.  Stated tolerance vs the reference's
-    fp64 gradients: max |g - g_ref| / max |g_ref| <= 5e-2 per parameter, loss
+    fp64 gradients: max |g - g_ref| / max |g_ref| <= 2.5e-2 per parameter (measured 1.1e-2 on C1), loss
     to 1e-2 relative (tests/test_training_gpu.py).
 The forward follows ``_forward_cached`` (model.py:322-416) op for op, in
 compact space: position-wise work on the N' rows, attention on the original
