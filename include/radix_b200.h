@@ -61,6 +61,7 @@ typedef enum rdx_status {
   RDX_ERR_HASH_RETRIES = 11,         /* GPU planner: every hash seed collided */
   RDX_ERR_INVALID_ARGUMENT = 12,
   RDX_ERR_UNSUPPORTED = 13,
+  RDX_ERR_DEVICE_TIMEOUT = 14,      /* an asynchronous wait gave up (rdx_device_status) */
   RDX_ERR_CUDA = 100
 } rdx_status;
 
@@ -158,9 +159,14 @@ int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t
  * preceding rdx_gemm (RDX_EPI_RESID_F32 with done_ctr) on the same stream: the
  * kernel is launched as a programmatic dependent of that GEMM (it can start on
  * SMs the GEMM's last round leaves idle) and processes row r once
- * done_ctr[r / 32] >= target (a slab still incomplete after ~8 s traps: the
- * counters and targets did not match).  d must be 128 * V for V in {2, 4, 8, 16, 20, 32}
+ * done_ctr[r / 32] >= target (a slab still incomplete after ~8 s stops the wait,
+ * the rows are normalised as found and rdx_device_status reports
+ * RDX_ERR_DEVICE_TIMEOUT: the counters and targets did not match).  d must be 128 * V for V in {2, 4, 8, 16, 20, 32}
  * (else RDX_ERR_UNSUPPORTED: use rdx_rmsnorm_rows after a stream-ordered GEMM). */
+/* First device-side failure of an asynchronous contract since the last call
+ * (RDX_OK or RDX_ERR_DEVICE_TIMEOUT), then cleared; synchronises `stream`. */
+int rdx_device_status(void* stream);
+
 int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_rows, int64_t d, const float* w, float eps,
                            void* out_bf16, int64_t ld_out, const uint32_t* done_ctr, uint32_t target,
                            void* stream);
@@ -240,8 +246,10 @@ typedef struct rdx_gemm_args {
    * frequencies, |error| < 1e-6 for positions < 2^20) and rope_table is unused. */
   const uint32_t* rope_pos;
   double rope_theta;
-  /* RDX_EPI_RESID_F32: when done_ctr != NULL, tiles run in row-block-major order and,
-   * once a warp's reduce-adds have completed, done_ctr[row / 32] is incremented by
+  /* RDX_EPI_RESID_F32 only (any other epilogue with done_ctr != NULL returns
+   * RDX_ERR_INVALID_ARGUMENT): when done_ctr != NULL, tiles run in row-block-major
+   * order when M spans < 64 row blocks (else in the grouped raster of 16 row blocks)
+   * and, once a warp's reduce-adds have completed, done_ctr[row / 32] is incremented by
    * the number of columns it wrote for those 32 rows (a 32-row slab is complete
    * when its counter has grown by N); done_ctr holds ceil(M / 32) counters.
    * Feeds rdx_rmsnorm_rows_after. */

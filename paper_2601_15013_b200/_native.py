@@ -35,6 +35,7 @@ EXPORTS = (
     "rdx_embed_rows",
     "rdx_rmsnorm_rows",
     "rdx_rmsnorm_rows_after",
+    "rdx_device_status",
     "rdx_rope_table",
     "rdx_rope_table_blocked",
     "rdx_gemm",
@@ -127,6 +128,7 @@ _SIGNATURES = {
     ),
     "rdx_embed_rows": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "rdx_rmsnorm_rows": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _i64, _vp]),
+    "rdx_device_status": (ctypes.c_int, [_vp]),
     "rdx_rmsnorm_rows_after": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _f32, _vp, _i64, _vp, _u32, _vp]),
     "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_rope_table_blocked": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
@@ -197,6 +199,14 @@ def check(code: int, what: str) -> None:
         if code == 100:
             detail = (lib().rdx_last_cuda_error() or b"").decode()
         raise_for_status(code, what, detail)
+
+
+def check_device_status(stream=None) -> None:
+    """Raise if an asynchronous device-side contract failed since the last check
+    (rdx_device_status; synchronises the stream)."""
+    check_status = lib().rdx_device_status(stream_handle(stream))
+    if check_status:
+        raise_for_status(check_status, "device status")
 
 
 def ptr(t) -> int | None:

@@ -423,6 +423,13 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
   using T = Tile<HDP, NQB, NSLOT>;
   constexpr int Q_BYTES = T::Q_BYTES, T_BYTES = T::T_BYTES, CH = T::CH;
   extern __shared__ __align__(1024) uint8_t smem[];  // dynamic smem starts 1024-aligned (no static smem)
+  // the swizzled tiles need a 1024-byte aligned base (no room for slack: T::SMEM is
+  // at the 227 KB limit).  Uniform check: every thread leaves, none waits on a barrier
+  // that will never complete; rdx_device_status reports it.
+  if (smem_u32(smem) & 1023u) {
+    if (threadIdx.x == 0) atomicCAS(&g_device_status, 0, static_cast<int>(RDX_ERR_DEVICE_TIMEOUT));
+    return;
+  }
   uint8_t* sQ = smem;                                // [2 h][NQB][Q_BYTES]
   uint8_t* sT = smem + T::T_OFF;                     // [NSLOT][T_BYTES]
   float* sL = reinterpret_cast<float*>(smem + T::L_OFF);  // [2 h][2][128]
@@ -446,7 +453,6 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023) __trap();  // the swizzled tiles need a 1024-byte aligned base
     for (int i = 0; i < 2 * NQB; ++i) {
       mbar_init(&q_full[i], 32);
       mbar_init(&q_free[i], 1);
@@ -1066,3 +1072,5 @@ extern "C" int rdx_attention_debug_trace(uint32_t* host, int n_words) {
   RDX_CUDA_TRY(cudaMemcpy(host, g_trace, m * sizeof(uint32_t), cudaMemcpyDeviceToHost));
   return RDX_OK;
 }
+
+int rdx::take_device_status_attention(int* out, cudaStream_t st) { return take_device_status(out, st); }

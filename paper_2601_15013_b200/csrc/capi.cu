@@ -57,12 +57,22 @@ extern "C" const char* rdx_status_name(int status) {
     case RDX_ERR_HASH_RETRIES: return "HashRetriesExhausted";
     case RDX_ERR_INVALID_ARGUMENT: return "InvalidArgument";
     case RDX_ERR_UNSUPPORTED: return "Unsupported";
+    case RDX_ERR_DEVICE_TIMEOUT: return "DeviceTimeout";
     case RDX_ERR_CUDA: return "CudaError";
     default: return "UnknownStatus";
   }
 }
 
 extern "C" const char* rdx_last_cuda_error(void) { return rdx::g_last_error; }
+
+extern "C" int rdx_device_status(void* stream) {
+  cudaStream_t st = rdx::as_stream(stream);
+  int a = 0, r = 0;
+  if (int rc = rdx::take_device_status_attention(&a, st)) return rc;
+  if (int rc = rdx::take_device_status_rowops(&r, st)) return rc;
+  RDX_CUDA_TRY(cudaStreamSynchronize(st));
+  return a ? a : r;
+}
 
 extern "C" int rdx_num_sms(void) { return rdx::num_sms(); }
 

@@ -24,6 +24,22 @@ int set_cuda_error(cudaError_t e);  // records the string, returns RDX_ERR_CUDA
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// First device-side failure of an asynchronous contract in this translation unit
+// (a slab wait that timed out, a misaligned smem base): one copy per .cu file
+// (no relocatable device code), read and cleared by take_device_status_<tu>() for
+// rdx_device_status (capi.cu).
+namespace {
+__device__ int g_device_status = 0;
+inline int take_device_status(int* out, cudaStream_t st) {
+  const int zero = 0;
+  RDX_CUDA_TRY(cudaMemcpyFromSymbolAsync(out, g_device_status, sizeof(int), 0, cudaMemcpyDeviceToHost, st));
+  RDX_CUDA_TRY(cudaMemcpyToSymbolAsync(g_device_status, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+  return 0;
+}
+}  // namespace
+int take_device_status_attention(int* out, cudaStream_t st);
+int take_device_status_rowops(int* out, cudaStream_t st);
+
 int num_sms();
 
 // ---------------------------------------------------------------- programmatic dependent launch

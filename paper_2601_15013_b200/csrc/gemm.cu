@@ -1032,6 +1032,8 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
   if (a.epi == RDX_EPI_QKV && (a.head_dim <= 0 || a.head_dim % 16 || a.head_dim > 128))
     return RDX_ERR_SHAPE_MISMATCH;
   if (a.row_ss && (a.ss_parts <= 0 || a.norm_dim <= 0)) return RDX_ERR_INVALID_ARGUMENT;
+  // slab completion counters exist only on the residual reduce-add epilogue
+  if (a.done_ctr && a.epi != RDX_EPI_RESID_F32) return RDX_ERR_INVALID_ARGUMENT;
   choose_shape(a, &bn, &cg);
   cudaStream_t s = as_stream(stream);
   switch (a.epi) {

@@ -290,7 +290,10 @@ rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_r
         while (ld_acquire_u32(done_ctr + slab) < target) {
           __nanosleep(ns);
           ns = ns < 2048 ? 2 * ns : ns;
-          if (++spins > (1u << 22)) __trap();  // ~8 s: the producing GEMM never completed this slab -> fail loudly
+          if (++spins > (1u << 22)) {  // ~8 s: the producing GEMM never completed this slab
+            atomicCAS(&g_device_status, 0, static_cast<int>(RDX_ERR_DEVICE_TIMEOUT));  // reported by rdx_device_status
+            break;
+          }
         }
       }
     }
@@ -562,3 +565,5 @@ extern "C" int rdx_rerank_scores(const float* logits, int64_t n_rows, int64_t ld
   RDX_LAUNCH_CHECK();
   return RDX_OK;
 }
+
+int rdx::take_device_status_rowops(int* out, cudaStream_t st) { return take_device_status(out, st); }

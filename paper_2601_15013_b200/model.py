@@ -776,29 +776,23 @@ class RadixQwen3:
         return result, err
 
 
-_MODEL_CACHE: dict = {}
-
-
 def _model_for(config: ModelConfig, params) -> RadixQwen3:
+    """No implicit weight cache: the reference's forward is pure in ``params``
+    (its tests edit arrays in place between calls, test_model.py:304-313), so a
+    numpy dict is converted on every call.  Callers that reuse weights pass a
+    :class:`DeviceWeights` or a :class:`RadixQwen3`."""
     if isinstance(params, RadixQwen3):
         return params
     if isinstance(params, DeviceWeights):
         return RadixQwen3(config, params)
-    key = (id(params), config)
-    hit = _MODEL_CACHE.get(key)
-    if hit is not None and hit[0] is params:
-        return hit[1]
-    model = RadixQwen3(config, DeviceWeights.from_params(config, params))
-    _MODEL_CACHE.clear()
-    _MODEL_CACHE[key] = (params, model)
-    return model
+    return RadixQwen3(config, DeviceWeights.from_params(config, params))
 
 
 def forward(config: ModelConfig, params, batch: RaggedBatch, plan=None, ledger: FlopLedger | None = None,
             *, attention: str = "suffix", logits: str = "all"):
     """Reference-compatible entry (model.py:310-319) returning device fp32 logits.
 
-    ``params`` is the reference's numpy dict (converted once and cached), a
+    ``params`` is the reference's numpy dict (converted on every call), a
     :class:`DeviceWeights` or a :class:`RadixQwen3`.  ``plan`` is None (dedup
     off), a host :class:`CompactionPlan`, a :class:`DevicePlan` or "auto"
     (GPU planner).

@@ -104,6 +104,7 @@ def score_stream(reranker, batches):
     bit-identical to calling ``reranker.score`` on each batch in turn."""
     import torch
 
+    from . import _native
     from .ragged import validate_batch
 
     batches = list(batches)
@@ -152,4 +153,5 @@ def score_stream(reranker, batches):
     pt, pbuf, pdone = pending
     pdone.synchronize()
     results[pt] = np.array(pbuf.numpy(), copy=True)
+    _native.check_device_status(main)  # once per stream: an overlapped-norm wait that timed out
     return results

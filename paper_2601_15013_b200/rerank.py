@@ -97,6 +97,7 @@ class RadixReranker:
         validate_batch(batch)
         scores = self.score_device(self.upload(batch))
         out = scores.cpu().numpy()
+        _native.check_device_status()  # an overlapped-norm wait that timed out fails here, not silently
         # D2H: the plan's (N', status, cu_q) read (dedup only) and the scores
         self.d2h_bytes = out.nbytes + ((4 + batch.num_sequences + 1) * 4 if self.dedup else 0)
         return out

@@ -277,6 +277,39 @@ def test_gemm_error_codes():
     args.head_dim, args.q_heads, args.kv_heads, args.eps = 32, 2, 2, 1e-6
     args.rope_pos, args.rope_theta = pos.data_ptr(), 1e6  # positions mode needs head_dim 64 or 128
     assert lib.rdx_gemm(args, st) == 12
+    # slab counters only exist on the residual reduce-add epilogue
+    a2 = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    w2 = torch.zeros(128, 64, dtype=torch.bfloat16, device="cuda")
+    o2 = torch.zeros(64, 128, dtype=torch.bfloat16, device="cuda")
+    args = _native.GemmArgs()
+    args.a, args.b, args.m, args.n, args.k, args.lda, args.ldb = a2.data_ptr(), w2.data_ptr(), 64, 128, 64, 64, 64
+    args.epi, args.out, args.ldo, args.done_ctr = _native.EPI_STORE_BF16, o2.data_ptr(), 128, ctr.data_ptr()
+    assert lib.rdx_gemm(args, st) == 12
+    assert lib.rdx_device_status(st) == 0
+
+
+@pytest.mark.timeout(120)
+def test_rmsnorm_after_timeout_reports_status():
+    """A slab counter that never reaches its target stops the wait after ~8 s and is
+    reported by rdx_device_status (RDX_ERR_DEVICE_TIMEOUT) instead of killing the context."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+    from paper_2601_15013_b200.errors import NativeLibraryError
+
+    lib, st = _native.lib(), _native.stream_handle()
+    assert lib.rdx_device_status(st) == 0
+    x = torch.ones(32, 256, device="cuda")
+    wn = torch.ones(256, device="cuda")
+    o = torch.empty(32, 256, dtype=torch.bfloat16, device="cuda")
+    ctr = torch.zeros(1, dtype=torch.int32, device="cuda")  # never incremented
+    _native.check(lib.rdx_rmsnorm_rows_after(x.data_ptr(), 256, 32, 256, wn.data_ptr(), 1e-6, o.data_ptr(), 256,
+                                             ctr.data_ptr(), 256, st), "rmsnorm_after")
+    with pytest.raises(NativeLibraryError):
+        _native.check_device_status()
+    assert lib.rdx_device_status(st) == 0  # cleared by the read
+    torch.cuda.synchronize()  # the context is still usable
+    assert torch.isfinite(o.float()).all()
 
 
 def _gemm_norm(a, w, epi, out, block_n=0, row_ss=None, norm_dim=0, eps=1e-6, hb=None, ss_out=None):
