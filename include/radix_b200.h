@@ -101,6 +101,17 @@ int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const int64_t* cu,
                    int32_t* cu_q_out, int32_t* lcp_out, uint32_t* info_out,
                    void* scratch, size_t scratch_bytes, void* stream);
 
+/* Debug: batches up to 16 x 4096 tokens (and at most 8191 sequences) run on the
+ * cluster-resident planner (one thread-block cluster, the whole working set in
+ * shared memory); 0 routes every batch to the L2-resident planners for A/B runs
+ * and tests, 1 back on.  Same outputs either way.  Returns the previous setting. */
+int rdx_plan_debug_smem(int on);
+
+/* Debug: when buf != NULL (device memory, >= 32 u64), later cluster-planner
+ * launches write %globaltimer stamps: [0..11] phase boundaries of CTA 0,
+ * [16 + r] the start of CTA r.  NULL turns it off. */
+int rdx_plan_debug_trace(void* buf);
+
 /* ---------------------------------------------------------------------
  * Row gather / scatter: dst[j, :] = src[idx[j], :] as a bit-exact byte copy
  * (scatter_rows is the same call with the scatter map, ops.py:64-66).
@@ -262,6 +273,13 @@ int rdx_gemm(const rdx_gemm_args* args, void* stream);
  * narrower tiles (same per-element K reduction, same bits); 0 turns that off
  * for A/B runs, 1 back on.  Returns the previous setting. */
 int rdx_gemm_debug_tail_split(int on);
+
+/* Debug: few-round launches (RDX_EPI_RESID_F32 / STORE) cut N into column tiles
+ * of two widths (multiples of 32) so the persistent grid's rounds stay balanced
+ * (same per-element K reduction, same bits); 0 turns that off for A/B runs,
+ * 1 back on.  Returns the previous setting; on = -1 changes nothing and returns
+ * the number of column tiles the last launch used (0 = no partition). */
+int rdx_gemm_debug_colpart(int on);
 
 /* Debug: pin the GEMM tile shape (cg = 1 or 2 CTAs, block_n = 128 or 256) for
  * later launches, or cg = 0 for the automatic choice (A/B experiments; the

@@ -28,6 +28,8 @@ EXPORTS = (
     "rdx_last_cuda_error",
     "rdx_plan_scratch_bytes",
     "rdx_plan_build",
+    "rdx_plan_debug_smem",
+    "rdx_plan_debug_trace",
     "rdx_gather_rows",
     "rdx_gather_rows_backward_scratch_bytes",
     "rdx_gather_rows_backward",
@@ -40,6 +42,7 @@ EXPORTS = (
     "rdx_rope_table_blocked",
     "rdx_gemm",
     "rdx_gemm_debug_tail_split",
+    "rdx_gemm_debug_colpart",
     "rdx_gemm_debug_stats",
     "rdx_gemm_debug_shape",
     "rdx_gemm_debug_group_m",
@@ -134,6 +137,9 @@ _SIGNATURES = {
     "rdx_rope_table_blocked": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmArgs), _vp]),
     "rdx_gemm_debug_tail_split": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_gemm_debug_colpart": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_plan_debug_smem": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_plan_debug_trace": (ctypes.c_int, [_vp]),
     "rdx_gemm_debug_stats": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rdx_gemm_debug_shape": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "rdx_gemm_debug_group_m": (ctypes.c_int, [ctypes.c_int]),

@@ -72,6 +72,12 @@ struct EpiParams {
   int64_t ldhb;
   float* ss_out;
   int ss_out_parts;
+  // Column partition (cp_ncol > 0): each row block is cut into cp_ncol column tiles of
+  // cp_wide (where bit c of cp_mask is set) or cp_narrow columns, multiples of 32 that
+  // sum to N.  Chosen on the host when the tile count is only a few rounds of the
+  // persistent grid, so the rounds stay balanced (see choose_colpart).
+  int cp_ncol, cp_wide, cp_narrow;
+  uint32_t cp_mask;
   // RDX_EPI_RESID_F32 with a completion counter: tiles in row-block-major order, and
   // per 32-row slab the number of columns whose stores have completed
   uint32_t* done_ctr;
@@ -365,12 +371,11 @@ __device__ __forceinline__ void resid_norm_prefetch(EpiWarp<NB>& e, const CUtens
 template <int BN, int EPI, int NB>
 // hw = columns per warp of this tile (BN/2, or BN/4 for a split tail tile),
 // n0 = the tile's first output-space column.
-__device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, int ch, int hw, int64_t gm_lane,
+__device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, int ch, int c_lo, int hw, int64_t gm_lane,
                                               int64_t M, int64_t n0, int64_t N, const EpiParams& ep,
                                               const float* s_qn, const float* s_kn, const CUtensorMap* map,
                                               const CUtensorMap* map_hb, float rs) {
-  constexpr int HALF = BN / 2;
-  const int c_lo = ch * hw;
+  constexpr int HALF = BN / 2;  // hw <= HALF; c_lo = ch * hw except in a column partition
   float v[HALF];
   if constexpr (EPI == RDX_EPI_SWIGLU) {
     // warp ch owns outputs [ch*hw/2, (ch+1)*hw/2) of the tile's width/2: output o of
@@ -516,7 +521,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const int64_t unit = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
   const int64_t n_units = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
   const int64_t m_tiles = (M + BM * CG - 1) / (BM * CG);
-  const int64_t n_tiles = (N + BN - 1) / BN;
+  const int64_t n_tiles = ep.cp_ncol > 0 ? ep.cp_ncol : (N + BN - 1) / BN;
   const int64_t full_tiles = m_tiles * n_tiles;
   // Tail split: the tiles of the last partial round (from tail_start on) run as
   // `split` narrower tiles each (width BN/split), so r leftover tiles occupy
@@ -538,7 +543,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int64_t g = f / gsz, r = f - g * gsz;
     const int64_t g_rows = m_tiles - g * ep.group_m < ep.group_m ? m_tiles - g * ep.group_m : ep.group_m;
     m_blk = g * ep.group_m + r % g_rows;
-    n0 = (r / g_rows) * BN + part * width;
+    const int cblk = static_cast<int>(r / g_rows);
+    if (ep.cp_ncol > 0) {
+      const bool wide = (ep.cp_mask >> cblk) & 1u;
+      width = wide ? ep.cp_wide : ep.cp_narrow;
+      n0 = static_cast<int64_t>(cblk) * ep.cp_narrow +
+           static_cast<int64_t>(__popc(ep.cp_mask & ((1u << cblk) - 1u))) * (ep.cp_wide - ep.cp_narrow);
+    } else {
+      n0 = static_cast<int64_t>(cblk) * BN + part * width;
+    }
   };
   const int kblocks = static_cast<int>((K + BK - 1) / BK);
 
@@ -600,11 +613,18 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         int64_t m_blk, n0;
         int width;
         decode(tile, m_blk, n0, width);
-        const int div = BN / width;  // 1, 2 or 4
+        // B rows this CTA stages: width / CG (1, 1/2 or 1/4 of B_ROWS, or a column-partition width)
+        const int b_rows = width / CG;
         const int32_t m0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM);
-        const int32_t nb0 = static_cast<int32_t>(n0 + rank * (C::B_ROWS / div));
-        const uint32_t bytes = C::A_BYTES + C::B_BYTES / div;
-        const CUtensorMap* mapb = div == 1 ? &tmB : (div == 2 ? &tmB2 : &tmB4);
+        const int32_t nb0 = static_cast<int32_t>(n0 + rank * b_rows);
+        const uint32_t bytes = C::A_BYTES + static_cast<uint32_t>(b_rows) * (BK * 2);
+        const CUtensorMap* mapb;
+        if (ep.cp_ncol > 0) {
+          mapb = width == ep.cp_wide ? &tmB2 : &tmB4;  // boxes of cp_wide / cp_narrow rows (host)
+        } else {
+          const int div = BN / width;  // 1, 2 or 4
+          mapb = div == 1 ? &tmB : (div == 2 ? &tmB2 : &tmB4);
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
@@ -638,7 +658,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         int64_t m_blk, n0;
         int width;
         decode(tile, m_blk, n0, width);
-        const uint32_t idesc = width == BN ? C::IDESC : (width == BN / 2 ? C::IDESC_HALF : C::IDESC_QUARTER);
+        const uint32_t idesc = ep.cp_ncol > 0 ? umma_idesc_bf16(BM * CG, width)
+                               : (width == BN ? C::IDESC : (width == BN / 2 ? C::IDESC_HALF : C::IDESC_QUARTER));
         GST_WAIT(st_te, mbar_wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -705,7 +726,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       const long long st_tb = clock64();
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      epilogue_tile<BN, EPI, NB>(e, taddr, ch, width / 2, gm, M, n0, N, ep, s_norm, s_norm + 128, &tmC, &tmD, rs);
+      // this warp's columns: halves of the tile, or in a column partition (widths in
+      // 32-column boxes, possibly odd) the first ceil(boxes/2) boxes and the rest
+      int c_lo = ch * (width / 2), hw = width / 2;
+      if (ep.cp_ncol > 0) {
+        const int w0 = ((width / 32 + 1) / 2) * 32;
+        c_lo = ch ? w0 : 0;
+        hw = ch ? width - w0 : w0;
+      }
+      epilogue_tile<BN, EPI, NB>(e, taddr, ch, c_lo, hw, gm, M, n0, N, ep, s_norm, s_norm + 128, &tmC, &tmD, rs);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -717,8 +746,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       if constexpr (EPI == RDX_EPI_RESID_F32) {
         if (ep.done_ctr && lane == 0 && e.row0 < M) {  // slabs past M do not exist
           // this warp's reduce-adds are complete and visible: publish its columns of the slab
-          const int64_t c0 = n0 + ch * (width / 2);
-          const int64_t cols = N - c0 < width / 2 ? (N - c0 > 0 ? N - c0 : 0) : width / 2;
+          const int64_t c0 = n0 + c_lo;
+          const int64_t cols = N - c0 < hw ? (N - c0 > 0 ? N - c0 : 0) : hw;
           bulk_wait_all();
           asm volatile("fence.proxy.async.global;" ::: "memory");
           __threadfence();
@@ -836,6 +865,110 @@ bool tail_split_enabled() {
   return g_tail_split == 1;
 }
 
+// RDX_GEMM_COLPART=0 (env) or rdx_gemm_debug_colpart(0) disables the column partition (A/B runs).
+int g_colpart = -1;
+int g_last_cp_ncol = 0;  // debug query (rdx_gemm_debug_colpart(-1))
+bool colpart_enabled() {
+  if (g_colpart < 0) {
+    const char* e = getenv("RDX_GEMM_COLPART");
+    g_colpart = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_colpart == 1;
+}
+
+// Column partition for few-round launches (the C2 o_proj / down shape: M = 7024 ->
+// 28 pair row blocks x 4 column tiles of 256 = 112 tiles on 74 CTA pairs, 1.51 rounds
+// run as 2).  Candidates cut N into ncol column tiles whose widths are multiples of 32
+// (<= BN, as equal as possible: `wide` tiles 32 columns wider than the rest) and place
+// the wide ones at every bit pattern; each is scored by the makespan of the kernel's
+// static round-robin schedule (tile t -> unit t % units, in the kernel's raster order)
+// with a per-tile cost of (width + kTileFixed) columns (A is streamed per tile whatever
+// its width; kTileFixed fitted to the measured 128- vs 256-wide pair tiles).  Still no
+// split-K: each output element is one CTA's full K reduction, same bits.
+constexpr int kTileFixed = 100;
+struct ColPart {
+  int ncol, wide_w, narrow_w;
+  uint32_t mask;
+};
+
+double sched_makespan(int64_t m_tiles, int ncol, const int* widths, int group_m, int64_t units) {
+  double load[1024];
+  if (units > 1024) return 1e30;
+  for (int64_t u = 0; u < units; ++u) load[u] = 0.0;
+  const int64_t tiles = m_tiles * ncol;
+  for (int64_t t = 0; t < tiles; ++t) {
+    const int64_t gsz = static_cast<int64_t>(group_m) * ncol;
+    const int64_t g = t / gsz, r = t - g * gsz;
+    const int64_t g_rows = m_tiles - g * group_m < group_m ? m_tiles - g * group_m : group_m;
+    load[t % units] += widths[r / g_rows] + kTileFixed;
+  }
+  double mx = 0.0;
+  for (int64_t u = 0; u < units; ++u) mx = load[u] > mx ? load[u] : mx;
+  return mx;
+}
+
+bool choose_colpart(int64_t m_tiles, int64_t n, int bn, int group_m, int64_t units, int64_t tail_rem,
+                    int tail_split, ColPart* out) {
+  if (n % 32 || n > 32 * 256) return false;
+  const int64_t tiles = m_tiles * ((n + bn - 1) / bn);
+  if (tiles > 6 * units || tiles <= units / 2) return false;
+  // baseline: bn-wide tiles, the last round possibly split (as the kernel runs it)
+  const int n_tiles = static_cast<int>((n + bn - 1) / bn);
+  double base;
+  {
+    int w[64];
+    for (int c = 0; c < n_tiles; ++c) w[c] = bn;
+    base = sched_makespan(m_tiles, n_tiles, w, group_m, units);
+    if (tail_split > 1 && tail_rem > 0) {  // full rounds + the split tail's rounds
+      const double full = static_cast<double>(tiles / units) * (bn + kTileFixed);
+      const int64_t narrow = tail_split * tail_rem;
+      base = full + static_cast<double>((narrow + units - 1) / units) * (bn / tail_split + kTileFixed);
+    }
+  }
+  struct Key {
+    int64_t m_tiles, n, units;
+    int bn, group_m;
+    ColPart cp;
+    bool ok;
+  };
+  static Key cache[16];
+  static int cache_n = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < cache_n; ++i) {
+    const Key& k = cache[i];
+    if (k.m_tiles == m_tiles && k.n == n && k.units == units && k.bn == bn && k.group_m == group_m) {
+      *out = k.cp;
+      return k.ok;
+    }
+  }
+  const int boxes = static_cast<int>(n / 32);
+  double best = base * 0.97;  // adopt only a predicted gain of >= 3 %
+  ColPart bestcp{0, 0, 0, 0};
+  for (int ncol = n_tiles; ncol <= n_tiles + 3 && ncol <= 32; ++ncol) {
+    const int nar = boxes / ncol, wide = boxes % ncol;
+    if (32 * (nar + (wide ? 1 : 0)) > bn || nar < 2) continue;
+    // every placement of the wide tiles (ncol <= 8 keeps this at most 70 patterns)
+    const uint32_t lim = ncol <= 12 ? (1u << ncol) : 0u;
+    for (uint32_t mask = 0; mask < lim; ++mask) {
+      if (__builtin_popcount(mask) != wide) continue;
+      int w[32];
+      for (int c = 0; c < ncol; ++c) w[c] = 32 * (nar + ((mask >> c) & 1u));
+      const double ms = sched_makespan(m_tiles, ncol, w, group_m, units);
+      if (ms < best - 1e-9) {
+        best = ms;
+        bestcp = ColPart{ncol, 32 * (nar + 1), 32 * nar, mask};
+      }
+    }
+  }
+  const bool ok = bestcp.ncol > 0;
+  Key k{m_tiles, n, units, bn, group_m, bestcp, ok};
+  if (cache_n < 16) cache[cache_n++] = k;
+  else cache[(m_tiles + n) & 15] = k;
+  *out = bestcp;
+  return ok;
+}
+
 template <int BN, int EPI, int CG>
 int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   using C = Cfg<BN, CG, EPI>;
@@ -931,9 +1064,30 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
       }
     }
   }
-  const int64_t tail_start = split > 1 ? tiles - rem : tiles;
+  int64_t tail_start = split > 1 ? tiles - rem : tiles;
+  ep.cp_ncol = ep.cp_wide = ep.cp_narrow = 0;
+  ep.cp_mask = 0;
+  if constexpr (EPI == RDX_EPI_RESID_F32 || EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32) {
+    ColPart cp;
+    const int64_t m_tiles = (a.m + BM * CG - 1) / (BM * CG);
+    if (colpart_enabled() && choose_colpart(m_tiles, a.n, BN, ep.group_m, units_max, rem, split, &cp)) {
+      ep.cp_ncol = cp.ncol;
+      ep.cp_wide = cp.wide_w;
+      ep.cp_narrow = cp.narrow_w;
+      ep.cp_mask = cp.mask;
+      split = 1;
+      tail_start = m_tiles * cp.ncol;
+      // B boxes of the two widths (per CTA: width / CG rows) in the tmB2 / tmB4 slots
+      int st2 = make_map(&mb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, cp.wide_w / CG);
+      if (st2) return st2;
+      st2 = make_map(&mb4, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, cp.narrow_w / CG);
+      if (st2) return st2;
+    }
+  }
+  const int64_t grid_units = ep.cp_ncol > 0 ? units_max : units;
+  g_last_cp_ncol = ep.cp_ncol;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(units * CG));
+  cfg.gridDim = dim3(static_cast<unsigned>(grid_units * CG));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
@@ -1109,6 +1263,13 @@ extern "C" int rdx_gemm_debug_shape(int cg, int block_n) {
   g_forced_cg = cg;
   g_forced_bn = block_n;
   return RDX_OK;
+}
+
+extern "C" int rdx_gemm_debug_colpart(int on) {
+  if (on < 0) return rdx::gemm::g_last_cp_ncol;  // query: column tiles of the last launch (0 = no partition)
+  const int prev = rdx::gemm::colpart_enabled() ? 1 : 0;
+  rdx::gemm::g_colpart = on ? 1 : 0;
+  return prev;
 }
 
 extern "C" int rdx_gemm_debug_tail_split(int on) {

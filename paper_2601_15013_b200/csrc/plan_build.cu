@@ -26,6 +26,7 @@
 //   P4  cu_q = exclusive scan of (L_s - lcp_s); N' = cu_q[B]
 //   P5  scatter[i] = cu_q[s_r] + depth - lcp_{s_r} (r = rep_i);
 //       gather[cid] = i and compact_positions[cid] = pos[i] for representatives.
+#include <climits>
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -337,6 +338,459 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
   }
 }
 
+// ---------------------------------------------------------------- cluster-resident planner
+// Batches up to kSmMaxCtas * kSmChunkMax tokens (and a staged cu) run as ONE
+// thread-block cluster whose whole working set lives in shared memory: each CTA
+// owns a contiguous chunk of tokens (tok, pos, seg, path prefix P, slot) and a
+// slice of the open-addressing table; every cross-token lookup (P at a sequence
+// start, the representative's tok/pos/seg, the slots of i-1 and rep-1, the table
+// itself) is a distributed-shared-memory access (~200 cycles) instead of an L2
+// round trip, and the phases are separated by 4 hardware cluster barriers (the
+// cooperative grid version has 7 grid barriers and L2 traffic in every phase).
+// Same algorithm, same seeds, same outputs as plan_build_kernel.
+constexpr int kSmThreads = 1024;
+constexpr int kSmWarps = kSmThreads / 32;
+constexpr int kSmPerThread = 4;                               // tokens per thread at most
+constexpr int64_t kSmChunkMax = kSmThreads * kSmPerThread;   // tokens per CTA
+constexpr int kSmMaxCtas = 16;
+constexpr size_t kSmBudget = 227 * 1024 - 2048;               // dynamic smem (static: ~1 KB)
+
+struct SmGeom {
+  int64_t chunk;   // tokens per CTA
+  int64_t tslots;  // hash slots per CTA
+  int64_t tsize;   // tslots * cluster size
+  uint32_t off_P, off_slot, off_seg, off_tok, off_pos, off_keys, off_vals, off_lcp, off_cuq;
+  uint32_t bytes;
+  unsigned long long* trace;  // debug (rdx_plan_debug_trace): phase timestamps of CTA 0, start of every CTA
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NW>
+__device__ uint64_t block_exclusive_scan_u64_w(uint64_t v, uint64_t* warp_tot, uint64_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t t = lane < NW ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < NW) warp_tot[lane] = t;
+  }
+  __syncthreads();
+  const uint64_t warp_prefix = warp == 0 ? 0 : warp_tot[warp - 1];
+  total = warp_tot[NW - 1];
+  __syncthreads();
+  return warp_prefix + x - v;
+}
+
+__global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs a, SmGeom g) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks());
+  const int me = static_cast<int>(cl.block_rank());
+  extern __shared__ __align__(16) uint8_t sm[];
+  int64_t* s_cu = reinterpret_cast<int64_t*>(sm);
+  uint64_t* s_P = reinterpret_cast<uint64_t*>(sm + g.off_P);
+  uint32_t* s_slot = reinterpret_cast<uint32_t*>(sm + g.off_slot);
+  uint32_t* s_seg = reinterpret_cast<uint32_t*>(sm + g.off_seg);
+  uint32_t* s_tok = reinterpret_cast<uint32_t*>(sm + g.off_tok);
+  uint32_t* s_pos = reinterpret_cast<uint32_t*>(sm + g.off_pos);
+  unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(sm + g.off_keys);
+  uint32_t* s_vals = reinterpret_cast<uint32_t*>(sm + g.off_vals);
+  int32_t* s_lcp = reinterpret_cast<int32_t*>(sm + g.off_lcp);
+  int32_t* s_cuq = reinterpret_cast<int32_t*>(sm + g.off_cuq);
+  __shared__ uint64_t s_wtot[kSmWarps];
+  __shared__ uint64_t s_carry[kSmMaxCtas];
+  __shared__ uint64_t s_total;
+  __shared__ uint32_t s_flags[kMaxAttempts + 1];  // [0] validation bits, [1 + t] attempt t failed (CTA 0's copy counts)
+
+  const int tid = threadIdx.x;
+  auto mark = [&](int k) {
+    if (g.trace && me == 0 && tid == 0) g.trace[k] = globaltimer_ns();
+  };
+  if (g.trace && tid == 0) g.trace[16 + me] = globaltimer_ns();
+  mark(0);
+  const int64_t n = a.n, nseq = a.nseq, chunk = g.chunk;
+  const int64_t lo = min(n, static_cast<int64_t>(me) * chunk);
+  const int64_t cnt = min(n, lo + chunk) - lo;
+  auto owner_of = [&](int64_t x) { return static_cast<int>(x / chunk); };
+
+  // ---- stage cu, tok, pos; validate cu (sequences spread over the cluster) ----
+  for (int64_t q = tid; q <= nseq; q += kSmThreads) s_cu[q] = a.cu[q];
+  for (int64_t j = tid; j < cnt; j += kSmThreads) {
+    s_tok[j] = a.tok[lo + j];
+    s_pos[j] = a.pos[lo + j];
+  }
+  if (tid <= kMaxAttempts) s_flags[tid] = 0;
+  __syncthreads();
+  {
+    uint32_t bits = 0;  // bit0 start!=0, bit1 decrease, bit2 empty, bit3 end!=n
+    if (me == 0 && tid == 0) {
+      if (s_cu[0] != 0) bits |= 1u;
+      if (s_cu[nseq] != n) bits |= 8u;
+    }
+    for (int64_t q = static_cast<int64_t>(me) * kSmThreads + tid; q < nseq; q += static_cast<int64_t>(C) * kSmThreads) {
+      const int64_t d = s_cu[q + 1] - s_cu[q];
+      if (d < 0) bits |= 2u;
+      if (d == 0 && !(a.flags & RDX_PLAN_ALLOW_EMPTY)) bits |= 4u;
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (bits && (tid & 31) == 0) atomicOr(cl.map_shared_rank(&s_flags[0], 0), bits);
+  }
+  if (me == 0)
+    for (int64_t q = tid; q < nseq; q += kSmThreads) s_lcp[q] = static_cast<int32_t>(s_cu[q + 1] - s_cu[q]);
+  mark(1);
+  cl_sync();  // B1
+  mark(2);
+  {
+    const uint32_t bits = *reinterpret_cast<volatile uint32_t*>(cl.map_shared_rank(&s_flags[0], 0));
+    if (bits) {
+      if (me == 0 && tid == 0) {
+        a.info[0] = 0;
+        a.info[1] = (bits & 1u) ? RDX_ERR_BOUNDARY_MISMATCH
+                    : (bits & 6u) ? RDX_ERR_NON_MONOTONE_OFFSETS
+                                  : RDX_ERR_BOUNDARY_MISMATCH;
+        a.info[2] = 0;
+      }
+      cl_sync();  // nobody leaves while another CTA may still read CTA 0's flag
+      return;
+    }
+  }
+  // seq of each own token: contiguous run per thread, found once
+  const int per = static_cast<int>((cnt + kSmThreads - 1) / kSmThreads);
+  const int64_t j0 = static_cast<int64_t>(tid) * per;
+  if (j0 < cnt) {
+    uint32_t sq = find_seq(s_cu, nseq, lo + j0);
+    for (int u = 0; u < per && j0 + u < cnt; ++u) {
+      const int64_t i = lo + j0 + u;
+      while (sq + 1 < nseq && s_cu[sq + 1] <= i) ++sq;
+      s_seg[j0 + u] = sq;
+    }
+  }
+
+  for (int attempt = 0; attempt < kMaxAttempts; ++attempt) {
+    const uint64_t seed = 0x243F6A8885A308D3ULL * static_cast<uint64_t>(2 * attempt + 1) + 0x13198A2E03707344ULL;
+    // ---- P0: clear the table slice; per-token elements; chunk-local inclusive scan ----
+    for (int64_t t = tid; t < g.tslots; t += kSmThreads) {
+      s_keys[t] = 0ULL;
+      s_vals[t] = 0xFFFFFFFFu;
+    }
+    if (me == 0 && attempt > 0)
+      for (int64_t q = tid; q < nseq; q += kSmThreads) s_lcp[q] = static_cast<int32_t>(s_cu[q + 1] - s_cu[q]);
+    {
+      uint64_t m[kSmPerThread];
+      uint64_t sum = 0;
+#pragma unroll
+      for (int u = 0; u < kSmPerThread; ++u) {
+        m[u] = 0;
+        const int64_t j = j0 + u;
+        if (u < per && j < cnt) {
+          const uint32_t sq = s_seg[j];
+          m[u] = token_element(s_tok[j], s_pos[j], static_cast<uint32_t>(lo + j - s_cu[sq]), seed);
+          sum += m[u];
+        }
+      }
+      uint64_t tot;
+      uint64_t run = block_exclusive_scan_u64_w<kSmWarps>(sum, s_wtot, tot);
+#pragma unroll
+      for (int u = 0; u < kSmPerThread; ++u) {
+        const int64_t j = j0 + u;
+        if (u < per && j < cnt) {
+          run += m[u];
+          s_P[j] = run;
+        }
+      }
+      if (tid == 0) s_total = tot;
+    }
+    mark(3);
+    cl_sync();  // B2: chunk prefixes and totals visible, tables clear
+    mark(4);
+    if (tid < C) s_carry[tid] = *cl.map_shared_rank(&s_total, tid);
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t acc = 0;
+      for (int c = 0; c < C; ++c) {
+        const uint64_t t = s_carry[c];
+        s_carry[c] = acc;
+        acc += t;
+      }
+    }
+    __syncthreads();
+
+    // Path prefix P at any token x (own chunk or remote) and the path hash of token x
+    // in sequence q: H = P_x - P_{cu[q]-1} (exact in Z/2^64).  Indices fit 32 bits.
+    auto P_at = [&](int64_t x) -> uint64_t {
+      if (x < 0) return 0ULL;
+      const uint32_t o = static_cast<uint32_t>(x) / static_cast<uint32_t>(chunk);
+      return *cl.map_shared_rank(&s_P[static_cast<uint32_t>(x) - o * static_cast<uint32_t>(chunk)], o) + s_carry[o];
+    };
+    auto key_of = [&](uint64_t h) -> unsigned long long {
+      const uint64_t k = fmix64(h ^ seed);
+      return k == 0 ? 1ULL : k;
+    };
+    const uint32_t tsl = static_cast<uint32_t>(g.tslots), tsz = static_cast<uint32_t>(g.tsize);
+    auto home = [&](unsigned long long key) -> uint32_t { return static_cast<uint32_t>(__umul64hi(key, tsz)); };
+
+    // ---- P2: insert only the tokens whose path differs from the same depth of the
+    // previous sequence (the first occurrence of a path is always such a token: an
+    // equal path one sequence earlier would be earlier still).  Reranking batches then
+    // insert ~N' distinct keys and the shared prefix costs one insert, not B contending
+    // atomics; every other token finds its key in P3 with plain loads. ----
+    for (int64_t j = tid; j < cnt; j += kSmThreads) {
+      const int64_t i = lo + j;
+      const uint32_t sq = s_seg[j];
+      const int64_t st = s_cu[sq];
+      const uint64_t h = s_P[j] + s_carry[me] - P_at(st - 1);
+      bool insert = true;
+      if (sq > 0) {
+        const int64_t pst = s_cu[sq - 1];
+        if (i - st < st - pst) insert = (P_at(pst + (i - st)) - P_at(pst - 1)) != h;
+      }
+      uint32_t t = 0xFFFFFFFFu;
+      if (insert) {
+        const unsigned long long key = key_of(h);
+        t = home(key);
+        while (true) {
+          const uint32_t o = t / tsl, lt = t - o * tsl;
+          const unsigned long long prev = atomicCAS(cl.map_shared_rank(&s_keys[lt], o), 0ULL, key);
+          if (prev == 0ULL || prev == key) {
+            atomicMin(cl.map_shared_rank(&s_vals[lt], o), static_cast<uint32_t>(i));
+            break;
+          }
+          t = t + 1 == tsz ? 0 : t + 1;
+        }
+      }
+      s_slot[j] = t;
+    }
+    mark(5);
+    cl_sync();  // B3: table final
+    mark(6);
+    auto vals_at = [&](uint32_t t) -> uint32_t {
+      const uint32_t o = t / tsl;
+      return *cl.map_shared_rank(&s_vals[t - o * tsl], o);
+    };
+
+    // ---- P3: representatives (table lookups), inductive verification, lcp ----
+    // rep(x) is a function of x's key (one slot per key, one first index per slot), so
+    // the inductive condition rep(i-1) == rep(rep_i - 1) is H_{i-1} == H_{rep_i - 1}.
+    uint32_t rr[kSmPerThread], srr[kSmPerThread];
+    uint32_t fail = 0;
+#pragma unroll
+    for (int u = 0; u < kSmPerThread; ++u) {
+      const int64_t j = tid + static_cast<int64_t>(u) * kSmThreads;
+      const bool live = j < cnt;
+      const int64_t i = lo + j;
+      uint32_t si = 0xFFFFFFFFu, r = 0, sr = 0;
+      int32_t mine = INT_MAX;
+      if (live) {
+        si = s_seg[j];
+        const int64_t st = s_cu[si];
+        const int64_t di = i - st;
+        const uint64_t pst1 = P_at(st - 1);
+        uint32_t t = s_slot[j];
+        bool lost = false;
+        if (t == 0xFFFFFFFFu) {  // not inserted: find the key
+          const unsigned long long key = key_of(s_P[j] + s_carry[me] - pst1);
+          t = home(key);
+          while (true) {
+            const uint32_t o = t / tsl;
+            const unsigned long long k = *cl.map_shared_rank(&s_keys[t - o * tsl], o);
+            if (k == key) break;
+            if (k == 0ULL) {  // cannot happen unless hashes collided: retry with a new seed
+              lost = true;
+              break;
+            }
+            t = t + 1 == tsz ? 0 : t + 1;
+          }
+        }
+        if (lost) fail = 1;
+        r = lost ? static_cast<uint32_t>(i) : vals_at(t);
+        sr = si;
+        if (r == static_cast<uint32_t>(i)) {
+          mine = static_cast<int32_t>(di);
+        } else {
+          const uint32_t o = r / static_cast<uint32_t>(chunk);
+          const uint32_t lr = r - o * static_cast<uint32_t>(chunk);
+          sr = *cl.map_shared_rank(&s_seg[lr], o);
+          const int64_t sst = s_cu[sr];
+          bool ok = (*cl.map_shared_rank(&s_tok[lr], o) == s_tok[j]) &&
+                    (*cl.map_shared_rank(&s_pos[lr], o) == s_pos[j]) && (static_cast<int64_t>(r) - sst == di);
+          if (ok && di > 0) ok = (P_at(i - 1) - pst1) == (P_at(static_cast<int64_t>(r) - 1) - P_at(sst - 1));
+          if (!ok) fail = 1;
+        }
+      }
+      rr[u] = r;
+      srr[u] = sr;
+      // lcp_s = min depth of a token that is its own representative: reduced per warp
+      // over the lanes of the same sequence, one remote atomicMin per group
+      const unsigned grp = __match_any_sync(0xffffffffu, si);
+      const int32_t mn = __reduce_min_sync(grp, mine);
+      if (live && mn != INT_MAX && (threadIdx.x & 31) == __ffs(grp) - 1)
+        atomicMin(cl.map_shared_rank(&s_lcp[si], 0), mn);
+    }
+    if (__syncthreads_or(fail) && tid == 0) atomicOr(cl.map_shared_rank(&s_flags[1 + attempt], 0), 1u);
+    mark(7);
+    cl_sync();  // B4: verification and lcp final
+    mark(8);
+    if (*reinterpret_cast<volatile uint32_t*>(cl.map_shared_rank(&s_flags[1 + attempt], 0)) != 0) continue;
+
+    // ---- P4: every CTA copies lcp from CTA 0 and scans cu_q itself (no further barrier) ----
+    if (me != 0)
+      for (int64_t q = tid; q < nseq; q += kSmThreads) s_lcp[q] = *cl.map_shared_rank(&s_lcp[q], 0);
+    __syncthreads();
+    // done with every other CTA's shared memory: let them leave once P5 is done
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    {
+      uint64_t carry = 0;
+      for (int64_t base = 0; base < nseq; base += kSmThreads) {
+        const int64_t q = base + tid;
+        const uint64_t v = q < nseq ? static_cast<uint64_t>(s_cu[q + 1] - s_cu[q] - s_lcp[q]) : 0;
+        uint64_t tile_total;
+        const uint64_t ex = block_exclusive_scan_u64_w<kSmWarps>(v, s_wtot, tile_total);
+        if (q < nseq) {
+          s_cuq[q] = static_cast<int32_t>(carry + ex);
+          if (me == 0) {
+            a.cu_q[q] = static_cast<int32_t>(carry + ex);
+            if (a.lcp_out) a.lcp_out[q] = s_lcp[q];
+          }
+        }
+        carry += tile_total;
+      }
+      if (tid == 0) {
+        s_cuq[nseq] = static_cast<int32_t>(carry);
+        if (me == 0) {
+          a.cu_q[nseq] = static_cast<int32_t>(carry);
+          a.info[0] = static_cast<uint32_t>(carry);
+          a.info[1] = RDX_OK;
+          a.info[2] = static_cast<uint32_t>(attempt + 1);
+        }
+      }
+    }
+    __syncthreads();
+    mark(9);
+    // ---- P5: emit (own tokens, representatives held in registers since P3) ----
+#pragma unroll
+    for (int u = 0; u < kSmPerThread; ++u) {
+      const int64_t j = tid + static_cast<int64_t>(u) * kSmThreads;
+      if (j >= cnt) continue;
+      const int64_t i = lo + j;
+      const int64_t depth = i - s_cu[s_seg[j]];
+      const uint32_t sr = srr[u];
+      const uint32_t cid = static_cast<uint32_t>(s_cuq[sr] + depth - s_lcp[sr]);
+      a.scatter[i] = cid;
+      if (rr[u] == static_cast<uint32_t>(i)) {
+        a.gather[cid] = static_cast<uint32_t>(i);
+        a.cpos[cid] = s_pos[j];
+      }
+    }
+    mark(10);
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    mark(11);
+    return;
+  }
+  if (me == 0 && tid == 0) {
+    a.info[0] = 0;
+    a.info[1] = RDX_ERR_HASH_RETRIES;
+    a.info[2] = kMaxAttempts;
+  }
+  cl_sync();
+}
+
+// Shared-memory geometry of the cluster planner for (n, nseq) on `ctas` CTAs; false
+// when it does not fit (the cooperative grid kernel takes the batch).
+bool sm_geometry(int64_t n, int64_t nseq, int ctas, SmGeom* g) {
+  if (ctas < 1 || nseq + 1 > 8192) return false;
+  const int64_t chunk = (n + ctas - 1) / ctas;
+  if (chunk > kSmChunkMax) return false;
+  int64_t tslots = (2 * n + ctas - 1) / ctas;
+  tslots = tslots < 2 ? 2 : tslots;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const uint32_t o = static_cast<uint32_t>(off);
+    off = (off + bytes + 15) & ~static_cast<size_t>(15);
+    return o;
+  };
+  take(8 * static_cast<size_t>(nseq + 1));  // cu at offset 0
+  g->off_P = take(8 * static_cast<size_t>(chunk));
+  g->off_keys = take(8 * static_cast<size_t>(tslots));
+  g->off_slot = take(4 * static_cast<size_t>(chunk));
+  g->off_seg = take(4 * static_cast<size_t>(chunk));
+  g->off_tok = take(4 * static_cast<size_t>(chunk));
+  g->off_pos = take(4 * static_cast<size_t>(chunk));
+  g->off_vals = take(4 * static_cast<size_t>(tslots));
+  g->off_lcp = take(4 * static_cast<size_t>(nseq > 0 ? nseq : 1));
+  g->off_cuq = take(4 * static_cast<size_t>(nseq + 1));
+  g->bytes = static_cast<uint32_t>(off);
+  g->chunk = chunk;
+  g->tslots = tslots;
+  g->tsize = tslots * ctas;
+  return off <= kSmBudget;
+}
+
+// Largest cluster the shared-memory planner can be launched as (16 non-portable, else 8).
+int sm_cluster_max() {
+  static int cached = -1;
+  if (cached < 0) {
+    cached = 0;
+    auto kern = plan_build_smem_kernel;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmBudget)) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return cached;
+    }
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      cudaGetLastError();
+    for (int c : {16, 8}) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c);
+      cfg.blockDim = dim3(kSmThreads);
+      cfg.dynamicSmemBytes = kSmBudget;
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = c;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) == cudaSuccess && nclusters > 0) {
+        cached = c;
+        break;
+      }
+      cudaGetLastError();
+    }
+  }
+  return cached;
+}
+
+// RDX_PLAN_SMEM=0 (env) or rdx_plan_debug_smem(0): route every batch to the L2 planners (A/B, tests).
+int g_plan_smem = -1;
+unsigned long long* g_plan_trace = nullptr;  // debug: device buffer of >= 32 u64 (rdx_plan_debug_trace)
+bool sm_planner_enabled() {
+  if (g_plan_smem < 0) {
+    const char* e = getenv("RDX_PLAN_SMEM");
+    g_plan_smem = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_plan_smem == 1;
+}
+
 uint64_t table_size(int64_t n) {
   uint64_t t = 64;
   while (t < static_cast<uint64_t>(2 * n)) t <<= 1;
@@ -447,6 +901,30 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
   const int grid = static_cast<int>(want < mg ? want : mg);
   void* params[] = {&a, &s};
   const size_t dsmem = n_seqs + 1 <= kSmemCu ? static_cast<size_t>(8 * (n_seqs + 1)) : 0;
+  // up to 16 x 4096 tokens: the cluster-resident planner (everything in shared memory)
+  if (sm_planner_enabled()) {
+    const int cmax = sm_cluster_max();
+    int ctas = 1;
+    while (ctas < cmax && ctas * static_cast<int64_t>(kSmThreads) < n_tokens) ctas *= 2;
+    SmGeom g;
+    g.trace = g_plan_trace;
+    if (cmax > 0 && sm_geometry(n_tokens, n_seqs, ctas, &g)) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(ctas);
+      cfg.blockDim = dim3(kSmThreads);
+      cfg.dynamicSmemBytes = g.bytes;
+      cfg.stream = as_stream(stream);
+      cudaLaunchAttribute attr;
+      attr.id = cudaLaunchAttributeClusterDimension;
+      attr.val.clusterDim.x = ctas;
+      attr.val.clusterDim.y = 1;
+      attr.val.clusterDim.z = 1;
+      cfg.attrs = &attr;
+      cfg.numAttrs = 1;
+      RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, plan_build_smem_kernel, a, g));
+      return RDX_OK;
+    }
+  }
   if (n_tokens <= kSingleCtaTokens) {  // small batch: one CTA, no grid-wide barriers
     plan_build_kernel<kSingle><<<1, kPlanThreads, dsmem, as_stream(stream)>>>(a, s);
     RDX_LAUNCH_CHECK();
@@ -472,4 +950,15 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
   RDX_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(plan_build_kernel<kGrid>), dim3(grid),
                                            dim3(kPlanThreads), params, dsmem, as_stream(stream)));
   return RDX_OK;
+}
+
+extern "C" int rdx_plan_debug_smem(int on) {
+  const int prev = rdx::sm_planner_enabled() ? 1 : 0;
+  rdx::g_plan_smem = on ? 1 : 0;
+  return prev;
+}
+
+extern "C" int rdx_plan_debug_trace(void* buf) {
+  rdx::g_plan_trace = static_cast<unsigned long long*>(buf);
+  return 0;
 }

@@ -22,6 +22,8 @@ elif what == "groupk":  # raster group of the K >= 8192 GEMMs only (C4 down): G_
 elif what == "norm":  # model-level switch: rmsnorm overlapping the residual GEMM's tail
     def setter(on):
         os.environ["RDX_NORM_OVERLAP"] = str(on)
+elif what == "colpart":  # GEMM column partition of few-round launches
+    setter = lib.rdx_gemm_debug_colpart
 else:
     setter = lib.rdx_debug_pdl if what == "pdl" else lib.rdx_gemm_debug_tail_split
 config, _, batch, _ = bench.workload(cfg_name, 1, "weak")

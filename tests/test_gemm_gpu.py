@@ -411,6 +411,58 @@ def test_tail_split_bit_identical(epi_name, m, n, k):
         assert (outs[0] - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
 
 
+@pytest.mark.parametrize("epi_name,m,n,k,shape,counters", [
+    ("EPI_RESID_F32", 7024, 1024, 2048, (0, 0), True),    # C2 o_proj (slab counters: row-block-major)
+    ("EPI_RESID_F32", 7024, 1024, 3072, (0, 0), False),   # C2 down, column-block-major raster
+    ("EPI_RESID_F32", 5000, 1024, 2048, (0, 0), True),    # 7 column tiles of 160/128
+    ("EPI_STORE_BF16", 6026, 1024, 1024, (0, 0), False),  # 6 column tiles of 192/160
+    ("EPI_STORE_F32", 7024, 1024, 512, (0, 0), False),
+    ("EPI_STORE_F32", 3500, 1024, 512, (1, 256), False),  # 1-CTA tiles
+    ("EPI_RESID_F32", 7000, 1056, 640, (0, 0), True),     # N not a multiple of 256
+])
+def test_column_partition_bit_identical(epi_name, m, n, k, shape, counters):
+    """Few-round launches cut N into column tiles of two widths (multiples of 32): same
+    bits as the plain 256-wide schedule, every slab counter reaches N, STORE_F32 == torch."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    lib = _native.lib()
+    epi = getattr(_native, epi_name)
+    a, w = _rand(m, k, 41), _rand(n, k, 42, 0.05)
+    dt = torch.bfloat16 if epi == _native.EPI_STORE_BF16 else torch.float32
+    base = torch.randn(m, n, device="cuda").to(dt) if epi == _native.EPI_RESID_F32 else torch.zeros(m, n, dtype=dt,
+                                                                                                   device="cuda")
+    outs, ncols = [], []
+    lib.rdx_gemm_debug_shape(*shape)
+    try:
+        for on in (1, 0):
+            prev = lib.rdx_gemm_debug_colpart(on)
+            try:
+                o = base.clone()
+                ctr = torch.zeros(-(-m // 32), dtype=torch.int32, device="cuda")
+                args = _native.GemmArgs()
+                args.a, args.b, args.m, args.n, args.k = a.data_ptr(), w.data_ptr(), m, n, k
+                args.lda, args.ldb, args.epi, args.out, args.ldo = k, k, epi, o.data_ptr(), n
+                if counters:
+                    args.done_ctr = ctr.data_ptr()
+                _native.check(lib.rdx_gemm(args, _native.stream_handle()), "gemm")
+                ncols.append(lib.rdx_gemm_debug_colpart(-1))
+                torch.cuda.synchronize()
+            finally:
+                lib.rdx_gemm_debug_colpart(prev)
+            outs.append(o)
+            if counters:
+                assert (ctr == n).all()
+    finally:
+        lib.rdx_gemm_debug_shape(0, 0)
+    assert ncols[0] > 0 and ncols[1] == 0, ncols  # the partition ran, then the plain schedule
+    assert torch.equal(outs[0], outs[1])
+    if epi == _native.EPI_STORE_F32:
+        ref = a.float() @ w.float().T
+        assert (outs[0] - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+
+
 @pytest.mark.parametrize("m,hd,H,KV", [(7024, 128, 16, 8), (34816, 128, 32, 8), (7024, 64, 16, 8)])
 def test_qkv_tail_split_bit_identical(m, hd, H, KV):
     """QKV tail tiles one head wide go to one warp per lane quarter: same bits as unsplit."""

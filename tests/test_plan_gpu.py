@@ -143,3 +143,79 @@ def test_cu_q_matches_suffix_structure():
     lcp = dp.lcp.cpu().numpy()
     assert np.array_equal(np.diff(dp.cu_q_host), np.diff(b.cu_seqlens) - lcp)
     assert isinstance(b, RaggedBatch)
+
+
+def _device_plan_arrays(b, allow_empty=False):
+    from paper_2601_15013_b200 import build_plan_device
+    from paper_2601_15013_b200.plan import upload_batch
+
+    tok, pos, cu = upload_batch(b)
+    dp = build_plan_device(tok, pos, cu, allow_empty=allow_empty)
+    return (dp.n_compact, dp.gather.cpu().numpy(), dp.scatter.cpu().numpy(), dp.compact_positions.cpu().numpy(),
+            dp.cu_q_host.copy(), dp.lcp.cpu().numpy())
+
+
+def _batches_for_both_planners():
+    from paper_2601_15013_b200 import RaggedBatch
+    from paper_2601_15013_b200.workloads import RerankSpec, SyntheticSpec, make_synthetic_batch, msmarco_rerank_batch
+
+    out = [msmarco_rerank_batch(RerankSpec()), msmarco_rerank_batch(RerankSpec(queries=4)),
+           msmarco_rerank_batch(RerankSpec(template_len=0, query_len=32, tail_len=0))]
+    for n, p in ((1000, 0.5), (4096, 0.0), (16384, 0.25), (65536, 0.75), (65536 + 512, 0.5)):
+        out.append(make_synthetic_batch(SyntheticSpec(B=max(n // 512, 1), prefix_len=int(512 * p),
+                                                      suffix_len=512 - int(512 * p), seed=5)))
+    rng = np.random.default_rng(19)
+    for n_seq, maxlen in ((6000, 8), (300, 300), (2, 30000)):  # many short / deep multi-level / two long
+        lens = rng.integers(1, maxlen, size=n_seq)
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        tok = rng.integers(0, 3, size=int(cu[-1])).astype(np.uint32)
+        pos = (np.arange(int(cu[-1])) - np.repeat(cu[:-1], lens)).astype(np.uint32)
+        out.append(RaggedBatch(tok, pos, cu))
+    return out
+
+
+def test_smem_planner_matches_l2_planner(oracle):
+    """The cluster-resident planner (whole working set in shared memory, <= 64K tokens)
+    and the L2-resident planners give the same bits on every batch shape; both match
+    the oracle."""
+    from paper_2601_15013_b200 import _native
+
+    lib = _native.lib()
+    for b in _batches_for_both_planners():
+        res = []
+        for on in (1, 0):
+            prev = lib.rdx_plan_debug_smem(on)
+            try:
+                res.append(_device_plan_arrays(b))
+            finally:
+                lib.rdx_plan_debug_smem(prev)
+        for x, y in zip(res[0], res[1]):
+            np.testing.assert_array_equal(np.asarray(x), np.asarray(y))
+        g, s, cp, m = oracle.build_plan_oracle(b.token_ids, b.position_ids, b.cu_seqlens)
+        assert res[0][0] == m
+        np.testing.assert_array_equal(res[0][1], g)
+        np.testing.assert_array_equal(res[0][2], s)
+        np.testing.assert_array_equal(res[0][3], cp)
+
+
+@pytest.mark.parametrize("smem", [1, 0])
+def test_validation_codes_both_planners(smem):
+    import torch
+
+    from paper_2601_15013_b200 import BoundaryMismatch, NonMonotoneOffsets, _native, build_plan_device
+
+    lib = _native.lib()
+    prev = lib.rdx_plan_debug_smem(smem)
+    try:
+        tok = torch.arange(3000, dtype=torch.int32, device="cuda")
+        for cu, exc in (([0, 3000, 2000], NonMonotoneOffsets), ([0, 1000, 1000, 3000], NonMonotoneOffsets),
+                        ([5, 1000, 3000], BoundaryMismatch), ([0, 1000, 2999], BoundaryMismatch)):
+            cu_t = torch.tensor(cu, dtype=torch.int64, device="cuda")
+            with pytest.raises(exc):
+                build_plan_device(tok, tok, cu_t)
+        # empty sequences are fine when allowed
+        cu_t = torch.tensor([0, 1000, 1000, 3000], dtype=torch.int64, device="cuda")
+        dp = build_plan_device(tok, tok, cu_t, allow_empty=True)
+        assert dp.n_compact == 3000
+    finally:
+        lib.rdx_plan_debug_smem(prev)
