@@ -39,6 +39,17 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 // [4] epilogue busy (tfull seen -> accumulator released), [5] epilogue tiles.
 #ifdef RDX_GEMM_STATS_BUILD
 __device__ unsigned long long g_gemm_stats[8];
+// %globaltimer landmarks of one launch (ns): [0] first CTA entry (min), [1] last CTA entry,
+// [2] last CTA past its prologue, [3] first MMA operand stage ready (min), [4] last MMA
+// commit (max), [5] last epilogue warp done (max), [6] last CTA exit (max)
+__device__ unsigned long long g_gemm_times[8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define GTIME_MIN(k) atomicMin(&g_gemm_times[k], gtimer())
+#define GTIME_MAX(k) atomicMax(&g_gemm_times[k], gtimer())
 #define GST_WAIT(slot, ...)                 \
   do {                                      \
     const long long _t = clock64();         \
@@ -46,6 +57,8 @@ __device__ unsigned long long g_gemm_stats[8];
     slot += clock64() - _t;                 \
   } while (0)
 #else
+#define GTIME_MIN(k) do {} while (0)
+#define GTIME_MAX(k) do {} while (0)
 #define GST_WAIT(slot, ...) __VA_ARGS__
 #endif
 
@@ -210,6 +223,48 @@ __device__ __forceinline__ void emit_f32x32(EpiWarp<NB>& e, const float* v, cons
   epi_issue(e, map, c0, reduce_add);
 }
 
+// packed fp32 pairs (FFMA2 / FMUL2 / FADD2 on sm_100a): IEEE-identical to the scalar ops
+__device__ __forceinline__ uint64_t p2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+constexpr uint64_t kNeg2 = 0x8000000080000000ULL;
+
+// (cos, sin) of pos * inv_freq for two columns at once: the same operations as
+// rope_cs below on packed pairs (identical bits), MUFU sin/cos per element.
+__device__ __forceinline__ void rope_cs2(uint64_t pos2, float4 f, float& c0, float& s0, float& c1, float& s1) {
+  const uint64_t ghi = p2(f.x, f.z), glo = p2(f.y, f.w);
+  const uint64_t t = mul2(pos2, ghi);
+  uint64_t e = fma2(pos2, ghi, t ^ kNeg2);
+  e = fma2(pos2, glo, e);
+  float t0, t1;
+  up2(t, t0, t1);
+  const uint64_t r = mul2(add2(add2(t, p2(-rintf(t0), -rintf(t1))), e), p2(6.283185307179586f, 6.283185307179586f));
+  float r0, r1;
+  up2(r, r0, r1);
+  __sincosf(r0, &s0, &c0);
+  __sincosf(r1, &s1, &c1);
+}
+
 // (cos, sin) of pos * inv_freq for one column.  g = inv_freq / (2*pi) in fp64,
 // kept as an fp32 (hi, lo) pair; the angle in turns is pos*g_hi (exact FMA
 // residual) + pos*g_lo, its integer part drops out exactly, and MUFU sin/cos run
@@ -268,17 +323,26 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
         continue;
       }
       const float* w = kind == 0 ? s_qn : s_kn;
-      float ss = 0.f;
+      float ss;
+      {
+        // sum of squares of the head row: two TMEM loads per wait, packed FFMA2 into
+        // two running sums; (v * rs)^2 = rs^2 * v^2
+        uint64_t ss2 = 0ULL;
 #pragma unroll
-      for (int c = 0; c < HD; c += 32) {
-        float v[32];
-        tmem_ld32p(taddr + h0 + c, v);
-        tmem_wait_ld();
+        for (int c = 0; c < HD; c += 64) {
+          float v[64];
+          tmem_ld32p(taddr + h0 + c, v);
+          tmem_ld32p(taddr + h0 + c + 32, v + 32);
+          tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          v[j] *= rs;
-          ss += v[j] * v[j];
+          for (int j = 0; j < 64; j += 2) {
+            const uint64_t x = p2(v[j], v[j + 1]);
+            ss2 = fma2(x, x, ss2);
+          }
         }
+        float s0, s1;
+        up2(ss2, s0, s1);
+        ss = (s0 + s1) * (rs * rs);
       }
       const float inv = rsqrtf(ss / static_cast<float>(HD) + ep.eps) * rs;  // x1/x2 below are unscaled
 #pragma unroll 1
@@ -289,25 +353,25 @@ __device__ __forceinline__ void qkv_cols(EpiWarp<NB>& e, uint32_t taddr, int64_t
         if (ep.rope_pos) {  // (cos, sin) from the position; the math overlaps the TMEM loads
           float cs[32], sn[32];
           const uint32_t fq = smem_u32(s_qn + 256);
+          const uint64_t pos2 = p2(pos, pos);
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float4 f = ld_shared_f4(fq + 8 * (c + j));
-            rope_cs(pos, f.x, f.y, cs[j], sn[j]);
-            rope_cs(pos, f.z, f.w, cs[j + 1], sn[j + 1]);
-          }
+          for (int j = 0; j < 32; j += 2)
+            rope_cs2(pos2, ld_shared_f4(fq + 8 * (c + j)), cs[j], sn[j], cs[j + 1], sn[j + 1]);
           tmem_wait_ld();
           const uint32_t ws = smem_u32(w);
+          const uint64_t inv2 = p2(inv, inv);
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 w1 = ld_shared_f4(ws + 4 * (c + j));
             const float4 w2 = ld_shared_f4(ws + 4 * (H + c + j));
-            const float wa[4] = {w1.x, w1.y, w1.z, w1.w}, wb[4] = {w2.x, w2.y, w2.z, w2.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float a = x1[j + u] * inv * wa[u];
-              const float b = x2[j + u] * inv * wb[u];
-              x1[j + u] = a * cs[j + u] - b * sn[j + u];
-              x2[j + u] = b * cs[j + u] + a * sn[j + u];
+            for (int u = 0; u < 4; u += 2) {
+              // a = x1 * inv * w1, b = x2 * inv * w2 (same order as the scalar form)
+              const uint64_t a = mul2(mul2(p2(x1[j + u], x1[j + u + 1]), inv2), u ? p2(w1.z, w1.w) : p2(w1.x, w1.y));
+              const uint64_t b = mul2(mul2(p2(x2[j + u], x2[j + u + 1]), inv2), u ? p2(w2.z, w2.w) : p2(w2.x, w2.y));
+              const uint64_t c2 = p2(cs[j + u], cs[j + u + 1]), s2 = p2(sn[j + u], sn[j + u + 1]);
+              up2(fma2(a, c2, mul2(b, s2) ^ kNeg2), x1[j + u], x1[j + u + 1]);  // a*c - b*s
+              up2(fma2(b, c2, mul2(a, s2)), x2[j + u], x2[j + u + 1]);          // b*c + a*s
             }
           }
         } else {
@@ -517,6 +581,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    GTIME_MIN(0);
+    GTIME_MAX(1);
+  }
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const int64_t unit = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
   const int64_t n_units = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
@@ -586,21 +654,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       s_norm[i] = ep.qn[i];
       s_norm[128 + i] = ep.kn[i];
     }
-    if (ep.rope_pos) {
-      // inv_freq_i = theta^(-2i/hd) in fp64 (model.py:165-172), in turns (/ 2 pi), as an fp32 (hi, lo) pair
-      for (int i = threadIdx.x; i < ep.hd / 2; i += blockDim.x) {
-        const double f = pow(ep.rope_theta, -2.0 * i / static_cast<double>(ep.hd)) * 0.15915494309189533577;
-        const float hi = static_cast<float>(f);
-        s_norm[256 + 2 * i] = hi;
-        s_norm[256 + 2 * i + 1] = static_cast<float>(f - static_cast<double>(hi));
-      }
-    }
   }
   tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if (threadIdx.x == 0) GTIME_MAX(2);
   // everything above overlapped the previous kernel's tail (PDL); inputs from here on
   pdl_wait();
   pdl_launch_dependents();
@@ -665,6 +725,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
           GST_WAIT(st_fu, mbar_wait(&full[stage], phase));
+#ifdef RDX_GEMM_STATS_BUILD
+          if (kb == 0 && tile == unit && lane == 0) GTIME_MIN(3);
+#endif
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint64_t da = umma_sdesc_sw128(sa);
@@ -689,6 +752,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       }
 #ifdef RDX_GEMM_STATS_BUILD
       if (lane == 0) {
+        GTIME_MAX(4);
         atomicAdd(&g_gemm_stats[0], static_cast<unsigned long long>(st_te));
         atomicAdd(&g_gemm_stats[1], static_cast<unsigned long long>(st_fu));
         atomicAdd(&g_gemm_stats[2], static_cast<unsigned long long>(clock64() - st_t0));
@@ -702,6 +766,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     const int ew = warp - 2;
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int ch = ew >> 2;  // column half of the tile
+    if constexpr (EPI == RDX_EPI_QKV) {
+      if (ep.rope_pos) {
+        // inv_freq_i = theta^(-2i/hd) in fp64 (model.py:165-172), in turns (/ 2 pi), as an fp32
+        // (hi, lo) pair.  Computed here by the epilogue warps while the first tile's mainloop
+        // runs (fp64 pow costs ~1.2 us; in the prologue it delayed every launch by that much).
+        for (int i = threadIdx.x - 64; i < ep.hd / 2; i += 32 * kEpiWarps) {
+          const double f = pow(ep.rope_theta, -2.0 * i / static_cast<double>(ep.hd)) * 0.15915494309189533577;
+          const float hi = static_cast<float>(f);
+          s_norm[256 + 2 * i] = hi;
+          s_norm[256 + 2 * i + 1] = static_cast<float>(f - static_cast<double>(hi));
+        }
+        named_bar_sync(1, 32 * kEpiWarps);
+      }
+    }
     constexpr int NB = (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32 || EPI == RDX_EPI_RESID_NORM) ? 2 : 4;
     EpiWarp<NB> e;
     e.base = epi_smem + ew * C::EPI_WARP_BYTES;
@@ -760,6 +838,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if (lane == 0) bulk_wait_all();
 #ifdef RDX_GEMM_STATS_BUILD
     if (lane == 0) {
+      GTIME_MAX(5);
       atomicAdd(&g_gemm_stats[3], static_cast<unsigned long long>(st_w));
       atomicAdd(&g_gemm_stats[4], static_cast<unsigned long long>(st_b));
       atomicAdd(&g_gemm_stats[5], static_cast<unsigned long long>(n_t));
@@ -778,6 +857,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     if constexpr (CG == 2) tmem_dealloc_cg2(tmem_base, C::TMEM_COLS);
     else tmem_dealloc(tmem_base, C::TMEM_COLS);
   }
+  if (threadIdx.x == 0) GTIME_MAX(6);
 }
 
 // ---------------------------------------------------------------- host side
@@ -1227,11 +1307,16 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
 // Debug: switch the GEMM tail split on (1) / off (0); returns the previous setting.
 extern "C" int rdx_gemm_debug_stats(unsigned long long* out8, int reset) {
 #ifdef RDX_GEMM_STATS_BUILD
-  if (out8 && cudaMemcpyFromSymbol(out8, rdx::gemm::g_gemm_stats, sizeof(unsigned long long) * 8) != cudaSuccess)
+  // reset >= 2: out8 receives the %globaltimer landmarks (g_gemm_times) instead
+  if (out8 && cudaMemcpyFromSymbol(out8, reset >= 2 ? rdx::gemm::g_gemm_times : rdx::gemm::g_gemm_stats,
+                                   sizeof(unsigned long long) * 8) != cudaSuccess)
     return RDX_ERR_CUDA;
   if (reset) {
     const unsigned long long z[8] = {};
+    unsigned long long zt[8] = {};
+    zt[0] = zt[3] = ~0ULL;  // min slots
     if (cudaMemcpyToSymbol(rdx::gemm::g_gemm_stats, z, sizeof(z)) != cudaSuccess) return RDX_ERR_CUDA;
+    if (cudaMemcpyToSymbol(rdx::gemm::g_gemm_times, zt, sizeof(zt)) != cudaSuccess) return RDX_ERR_CUDA;
   }
   return RDX_OK;
 #else

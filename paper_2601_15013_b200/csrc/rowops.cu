@@ -270,6 +270,10 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   return v;
 }
 
+#ifndef RDX_NORM_BACKOFF_MAX
+#define RDX_NORM_BACKOFF_MAX 2048  // ns: the slab poller's longest nanosleep
+#endif
+
 template <int V>
 __global__ void __launch_bounds__(256)
 rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_rows, const float* __restrict__ w,
@@ -289,7 +293,7 @@ rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_r
         uint32_t spins = 0;
         while (ld_acquire_u32(done_ctr + slab) < target) {
           __nanosleep(ns);
-          ns = ns < 2048 ? 2 * ns : ns;
+          ns = ns < RDX_NORM_BACKOFF_MAX ? 2 * ns : ns;
           if (++spins > (1u << 22)) {  // ~8 s: the producing GEMM never completed this slab
             atomicCAS(&g_device_status, 0, static_cast<int>(RDX_ERR_DEVICE_TIMEOUT));  // reported by rdx_device_status
             break;
