@@ -327,6 +327,12 @@ int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const 
  * sums per-role clock counters (MMA waits on K/V, P, Q, O; softmax waits on S,
  * epilogue; loader waits on free slots; totals); this copies n slots to host
  * and resets them. */
+/* Debug: short units at head_dim 128 run 64-key K/V tiles with two S buffers per
+ * query tile (S two key tiles ahead of the softmax); 0 selects the 128-key
+ * single-buffered kernel for A/B runs, 1 back on.  Same math, same tolerance.
+ * Returns the previous setting. */
+int rdx_attention_debug_bk64(int on);
+
 int rdx_attention_debug_stats(unsigned long long* host, int n);
 /* Debug: event log of CTA 0 of the last launch in the same mode:
  * [count, (clock, code) x min(count, 4096)] as 32-bit words. */

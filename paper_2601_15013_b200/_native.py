@@ -48,6 +48,7 @@ EXPORTS = (
     "rdx_gemm_debug_group_m",
     "rdx_debug_pdl",
     "rdx_attention",
+    "rdx_attention_debug_bk64",
     "rdx_attention_debug_stats",
     "rdx_attention_debug_trace",
     "rdx_attention_debug_cta_times",
@@ -139,6 +140,7 @@ _SIGNATURES = {
     "rdx_gemm_debug_tail_split": (ctypes.c_int, [ctypes.c_int]),
     "rdx_gemm_debug_colpart": (ctypes.c_int, [ctypes.c_int]),
     "rdx_plan_debug_smem": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_attention_debug_bk64": (ctypes.c_int, [ctypes.c_int]),
     "rdx_plan_debug_trace": (ctypes.c_int, [_vp]),
     "rdx_gemm_debug_stats": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rdx_gemm_debug_shape": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),

@@ -72,19 +72,19 @@ constexpr int kSchedWarp = 14;             // walks this CTA's units and publish
 constexpr int kUnitConsumers = 14;         // warps that read each entry: softmax 8, loader, epilogue 4, MMA
 
 // NQB = Q buffers per query tile, NSLOT = K/V ring slots (K and V tiles alternate).
-template <int HDP, int NQB, int NSLOT>
+template <int HDP, int NQB, int NSLOT, int BKT = BK>
 struct Tile {
   static constexpr int HALVES = HDP / 64;
   static constexpr int CH = HDP / 8;               // 16-byte chunks per row
   static constexpr int Q_BYTES = BQ * HDP * 2;     // HALVES x 128 rows x 128 B
-  static constexpr int T_BYTES = BK * HDP * 2;     // one K or V tile
+  static constexpr int T_BYTES = BKT * HDP * 2;    // one K or V tile
   static constexpr int T_OFF = 2 * NQB * Q_BYTES;
   static constexpr int L_OFF = T_OFF + NSLOT * T_BYTES;  // fp32 [2 h][2 slots][128] row sums
   static constexpr int BAR_OFF = L_OFF + 2 * 2 * BQ * 4;
-  static constexpr int RING_OFF = BAR_OFF + 256;               // unit ring (scheduler warp -> roles)
+  static constexpr int RING_OFF = BAR_OFF + 512;               // unit ring (scheduler warp -> roles)
   static constexpr int SMEM = RING_OFF + kRing * kUnitWords * 4 + 2 * kRing * 8;
   static_assert(SMEM <= 232448, "shared memory budget");
-  static constexpr uint32_t IDESC_S = umma_idesc_bf16(BQ, BK);
+  static constexpr uint32_t IDESC_S = umma_idesc_bf16(BQ, BKT);
   static constexpr uint32_t IDESC_PV = umma_idesc_bf16(BQ, HDP) | (1u << 16);  // B (V) MN-major
 };
 
@@ -244,6 +244,7 @@ struct Args {
   int max_pairs;             // query-tile pairs of the longest query range
   int n_units;               // max_pairs * nseq * kv_heads
   int use_tma;               // head_dim % 64 == 0: whole 128-byte column boxes, TMA tile loads
+  int bk;                    // keys per K/V tile of the launched variant (64 or 128)
   float scale_log2;          // softmax scale * log2(e)
   unsigned long long* stats; // debug (RDX_ATTN_STATS_BUILD + RDX_ATTN_STATS=1): summed clocks per role
   uint32_t* trace;           // debug: event log of CTA trace_cta [count, (clock, code) x 4096]
@@ -323,8 +324,8 @@ __device__ __forceinline__ void unit_geometry(const Args& a, int u, int k0, int 
   it.lcp = it.L - it.qlen;
   it.mb0 = 2 * pair;
   const int mb1 = it.mb0 + 1;
-  it.nkt0 = it.mb0 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (it.mb0 + 1) * a.qpt) + BK - 1) / BK : 0;
-  it.nkt1 = mb1 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (mb1 + 1) * a.qpt) + BK - 1) / BK : 0;
+  it.nkt0 = it.mb0 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (it.mb0 + 1) * a.qpt) + a.bk - 1) / a.bk : 0;
+  it.nkt1 = mb1 * a.qpt < it.qlen ? (it.lcp + min(it.qlen, (mb1 + 1) * a.qpt) + a.bk - 1) / a.bk : 0;
 }
 
 // Work distribution.  The valid units (a query-tile pair that exists) are
@@ -416,11 +417,12 @@ __device__ __forceinline__ int ring_unit(const Ring& r, int k, Unit& it, int lan
   return u;
 }
 
-template <int HDP, int NQB, int NSLOT, uint32_t EMU>
+template <int HDP, int NQB, int NSLOT, uint32_t EMU, int BKT>
 __global__ void __launch_bounds__(kThreads, 1)
 attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_constant__ CUtensorMap map_q,
                  const __grid_constant__ CUtensorMap map_g4, const __grid_constant__ CUtensorMap map_r16, Args a) {
-  using T = Tile<HDP, NQB, NSLOT>;
+  using T = Tile<HDP, NQB, NSLOT, BKT>;
+  constexpr bool DB = BKT == 64;  // 64-key S tiles, two S buffers per query tile
   constexpr int Q_BYTES = T::Q_BYTES, T_BYTES = T::T_BYTES, CH = T::CH;
   extern __shared__ __align__(1024) uint8_t smem[];  // dynamic smem starts 1024-aligned (no static smem)
   // the swizzled tiles need a 1024-byte aligned base (no room for slack: T::SMEM is
@@ -438,13 +440,14 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
   uint64_t* q_free = bars + 2 * NQB;             // [2][NQB]
   uint64_t* t_full = bars + 4 * NQB;             // [NSLOT]
   uint64_t* t_free = t_full + NSLOT;             // [NSLOT]
-  uint64_t* s_full = t_free + NSLOT;             // [2]
-  uint64_t* p_full = s_full + 2;                 // [2]
-  uint64_t* o_full = p_full + 2;                 // [2]
+  uint64_t* s_full = t_free + NSLOT;             // [2 h][2 S buffers] ([h][0] when single-buffered)
+  uint64_t* p_full = s_full + 4;                 // [2 h][2] by P parity ([h][0] when single-buffered)
+  uint64_t* o_full = p_full + 4;                 // [2]
   uint64_t* o_free = o_full + 2;                 // [2]
   uint64_t* l_full = o_free + 2;                 // [2 h][2 slots]: one barrier per sL slot, so the
                                                  // softmax can never run two phases ahead of a waiter
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(l_full + 4);
+  uint64_t* pv_done = l_full + 4;                // [2 h]: PV_h(j) done, j < last (DB: O rescale may follow)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(pv_done + 2);
   Ring ring;
   ring.units = reinterpret_cast<int*>(smem + T::RING_OFF);
   ring.full = reinterpret_cast<uint64_t*>(smem + T::RING_OFF + kRing * kUnitWords * 4);
@@ -461,9 +464,12 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       mbar_init(&t_full[i], 32);
       mbar_init(&t_free[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 128);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&pv_done[i], 1);
       mbar_init(&o_full[i], 1);
       mbar_init(&o_free[i], 128);
       mbar_init(&l_full[2 * i], 128);
@@ -546,11 +552,12 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         const int32_t vcol = kcol + a.kv_heads * a.hd;
         const int nkt = max(it.nkt0, it.nkt1);
         // rows of keys 4*lane .. 4*lane+3 of tile j (-1 past the sequence end)
+        const bool ld_lane = 4 * lane < BKT;  // lanes holding keys of the tile (all 32 for 128-key tiles)
         auto key_rows = [&](int j, int (&r)[4]) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int key = j * BK + 4 * lane + i;
-            r[i] = key >= it.L ? -1 : (a.scatter ? __ldg(a.scatter + it.k0 + key) : it.k0 + key);
+            const int key = j * BKT + 4 * lane + i;
+            r[i] = (!ld_lane || key >= it.L) ? -1 : (a.scatter ? __ldg(a.scatter + it.k0 + key) : it.k0 + key);
           }
         };
         int rn[4];
@@ -584,19 +591,20 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
                 if (lane == 0) {
 #pragma unroll
                   for (int half = 0; half < T::HALVES; ++half)
-                    tma_load_2d(&map_kv, dst + half * (BK * 128), bar, col + half * 64, row0);
+                    tma_load_2d(&map_kv, dst + half * (BKT * 128), bar, col + half * 64, row0);
                 }
+              } else if (!ld_lane) {
               } else if (group_run) {
                 // one 16-row box per contiguous 16-key group, issued by the group's first lane
                 if ((lane & 3) == 0) {
 #pragma unroll
                   for (int half = 0; half < T::HALVES; ++half)
-                    tma_load_2d(&map_r16, dst + half * (BK * 128) + 4 * lane * 128, bar, col + half * 64, grow0);
+                    tma_load_2d(&map_r16, dst + half * (BKT * 128) + 4 * lane * 128, bar, col + half * 64, grow0);
                 }
               } else {
 #pragma unroll
                 for (int half = 0; half < T::HALVES; ++half)
-                  tma_gather4(&map_g4, smem_u32(dst + half * (BK * 128) + 4 * lane * 128), bar, col + half * 64,
+                  tma_gather4(&map_g4, smem_u32(dst + half * (BKT * 128) + 4 * lane * 128), bar, col + half * 64,
                               max(r[0], 0), max(r[1], 0), max(r[2], 0), max(r[3], 0));
               }
               if (lane != 0) mbar_arrive(bar);
@@ -604,11 +612,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
             } else {
               const uint32_t st = smem_u32(dst);
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
+              for (int i = 0; i < (ld_lane ? 4 : 0); ++i) {
 #pragma unroll
                 for (int c = 0; c < CH; ++c) {
                   const bool ok = r[i] >= 0 && c * 8 < a.hd;
-                  cp_async16(st + sw_off(4 * lane + i, c, BK),
+                  cp_async16(st + sw_off(4 * lane + i, c, BKT),
                              a.qkv + static_cast<int64_t>(ok ? r[i] : 0) * a.ld + col + c * 8, ok ? 16u : 0u);
                 }
               }
@@ -647,8 +655,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 #pragma unroll
         for (int kk = 0; kk < HDP / 16; ++kk)
           umma_ss_elect(sacc, qd + (((kk >> 2) * (BQ * 128) + (kk & 3) * 32) >> 4),
-                        kd + (((kk >> 2) * (BK * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
-        commit_elect(&s_full[h]);
+                        kd + (((kk >> 2) * (BKT * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
+        commit_elect(&s_full[2 * h]);
         if (lane == 0) RDX_EV(1, 1, h * 16 + j);  // MMA: S_h(j) issued
         if (RDX_STATS_ON) st_iss += clock64() - st_i0;
         if (h) ++s_cnt1; else ++s_cnt0;
@@ -660,17 +668,17 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       auto issue_PV = [&](int h, int nkt_h, int j, uint32_t tile) {
         int& o_cnt = h ? o_cnt1 : o_cnt0;
         const int s_cnt = h ? s_cnt1 : s_cnt0;
-        RDX_TWAIT(&p_full[h], (s_cnt - 1) & 1, st_p);  // P_h(j) published (S_h(j) was the last S of h)
+        RDX_TWAIT(&p_full[2 * h], (s_cnt - 1) & 1, st_p);  // P_h(j) published (S_h(j) was the last S of h)
         if (lane == 0) RDX_EV(1, 2, h * 16 + j);  // MMA: P_h(j) seen
         if (j == 0 && o_cnt > 0) RDX_TWAIT(&o_free[h], (o_cnt - 1) & 1, st_o);
         if (!a.use_tma) fence_proxy_async_smem();
         tc_fence_after();
         const uint32_t va = smem_u32(sT + ((2 * tile + 1) % NSLOT) * T_BYTES);
         const uint32_t o = tmem + O_COL + h * 128, pa = tmem + h * 128;
-        const uint64_t vd = sdesc(va, BK * 128, 1024);
+        const uint64_t vd = sdesc(va, BKT * 128, 1024);
         const long long st_i0 = RDX_STATS_ON ? clock64() : 0;
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk)
+        for (int kk = 0; kk < BKT / 16; ++kk)
           umma_ts_elect(o, pa + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
         if (RDX_STATS_ON) st_iss += clock64() - st_i0;
         if (j == nkt_h - 1) {
@@ -680,53 +688,171 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       };
       auto wait_tile = [&](uint32_t seqno) { RDX_TWAIT(&t_full[seqno % NSLOT], (seqno / NSLOT) & 1, st_t); };
 
-      Unit tmp, pre;
-      int kcur = 0;  // ring entry of the current unit
-      int ucur = ring_unit(ring, 0, tmp, lane);
-      int c0 = tmp.nkt0, c1 = tmp.nkt1, call = max(tmp.nkt0, tmp.nkt1);  // key tiles of the current unit
-      int jcur = 0;
-      int upre = a.n_units;  // the unit after the current one, fetched while S/softmax of this one run
-      if (ucur < a.n_units) {
-        wait_tile(2 * gt);
-        if (c0 > 0) issue_S(0, c0, 0, gt);
-        if (c1 > 0) issue_S(1, c1, 0, gt);
-        commit_elect(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
-        upre = ring_unit(ring, kcur + 1, pre, lane);
-      }
-      while (ucur < a.n_units) {
-        int unxt = ucur, jnxt = jcur + 1, n0 = c0, n1 = c1, nall = call;
-        if (jnxt >= call) {
-          unxt = upre;
-          jnxt = 0;
-          n0 = pre.nkt0;
-          n1 = pre.nkt1;
-          nall = max(pre.nkt0, pre.nkt1);
+      if constexpr (DB) {
+        // 64-key S tiles, two S buffers per query tile: S_h(j+2) goes into the buffer
+        // PV_h(j) has just read, so S runs two key tiles ahead of the softmax and the
+        // softmax never waits for its S behind its own P (the single-buffered chain).
+        int sc[2] = {0, 0};  // S tiles issued per h (buffer sc & 1)
+        int pc[2] = {0, 0};  // P tiles consumed per h (p_full[h][pc & 1], P(k) sits in buffer k & 1)
+        int oc[2] = {0, 0};  // units finished per h
+        int qc[2] = {0, 0};  // Q tiles consumed per h
+        int kread = 0;       // next ring entry
+        struct It {
+          int u, j, n0, n1, nall;
+        };
+        auto fetch = [&](It& x) {
+          Unit tmp;
+          x.u = ring_unit(ring, kread++, tmp, lane);
+          x.j = 0;
+          x.n0 = tmp.nkt0;
+          x.n1 = tmp.nkt1;
+          x.nall = max(tmp.nkt0, tmp.nkt1);
+        };
+        auto advance = [&](const It& x, It& y) {
+          if (x.u >= a.n_units) {
+            y = x;
+          } else if (x.j + 1 < x.nall) {
+            y = x;
+            ++y.j;
+          } else {
+            fetch(y);
+          }
+        };
+        auto issue_S2 = [&](int h, const It& x, uint32_t tile) {
+          const int nkt = h ? x.n1 : x.n0;
+          if (x.j >= nkt) return;
+          const int qb = qc[h] % NQB;
+          if (x.j == 0) RDX_TWAIT(&q_full[h * NQB + qb], (qc[h] / NQB) & 1, st_q);
+          if (!a.use_tma) fence_proxy_async_smem();
+          tc_fence_after();
+          const uint32_t qa = smem_u32(sQ + (h * NQB + qb) * Q_BYTES);
+          const uint32_t ka = smem_u32(sT + ((2 * tile) % NSLOT) * T_BYTES);
+          const int b = sc[h] & 1;
+          const uint32_t sacc = tmem + h * 128 + b * 64;
+          const uint64_t qd = sdesc(qa, 16, 1024), kd = sdesc(ka, 16, 1024);
+          const long long st_i0 = RDX_STATS_ON ? clock64() : 0;
+#pragma unroll
+          for (int kk = 0; kk < HDP / 16; ++kk)
+            umma_ss_elect(sacc, qd + (((kk >> 2) * (BQ * 128) + (kk & 3) * 32) >> 4),
+                          kd + (((kk >> 2) * (BKT * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
+          commit_elect(&s_full[2 * h + b]);
+          if (RDX_STATS_ON) st_iss += clock64() - st_i0;
+          ++sc[h];
+          if (x.j == nkt - 1) {
+            commit_elect(&q_free[h * NQB + qb]);
+            ++qc[h];
+          }
+        };
+        auto issue_PV2 = [&](int h, const It& x, uint32_t tile) {
+          const int nkt = h ? x.n1 : x.n0;
+          if (x.j >= nkt) return;
+          const int b = pc[h] & 1;
+          RDX_TWAIT(&p_full[2 * h + b], (pc[h] >> 1) & 1, st_p);
+          ++pc[h];
+          if (x.j == 0 && oc[h] > 0) RDX_TWAIT(&o_free[h], (oc[h] - 1) & 1, st_o);
+          if (!a.use_tma) fence_proxy_async_smem();
+          tc_fence_after();
+          const uint32_t va = smem_u32(sT + ((2 * tile + 1) % NSLOT) * T_BYTES);
+          const uint32_t o = tmem + O_COL + h * 128, pa = tmem + h * 128 + b * 64;
+          const uint64_t vd = sdesc(va, BKT * 128, 1024);
+          const long long st_i0 = RDX_STATS_ON ? clock64() : 0;
+#pragma unroll
+          for (int kk = 0; kk < BKT / 16; ++kk)
+            umma_ts_elect(o, pa + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, (x.j > 0 || kk > 0) ? 1u : 0u);
+          if (RDX_STATS_ON) st_iss += clock64() - st_i0;
+          if (x.j == nkt - 1) {
+            commit_elect(&o_full[h]);
+            ++oc[h];
+          } else {
+            commit_elect(&pv_done[h]);  // the softmax of tile j + 1 may rescale O after this
+          }
+        };
+        auto wait_tile2 = [&](uint32_t seqno) { RDX_TWAIT(&t_full[seqno % NSLOT], (seqno / NSLOT) & 1, st_t); };
+        It cur, n1, n2;
+        uint32_t gt = 0;  // iteration (key tile) counter: K at ring seq 2gt, V at 2gt + 1
+        fetch(cur);
+        if (cur.u < a.n_units) {
+          wait_tile2(0);
+          issue_S2(0, cur, 0);
+          issue_S2(1, cur, 0);
+          commit_elect(&t_free[0]);
         }
-        const bool has_next = unxt < a.n_units;
-        const uint32_t tnext = gt + 1;
-        wait_tile(2 * gt + 1);  // V(cur)
-        if (jcur < c0) issue_PV(0, c0, jcur, gt);
-        if (has_next) {
-          wait_tile(2 * tnext);  // K(next)
-          if (jnxt < n0) issue_S(0, n0, jnxt, tnext);
+        advance(cur, n1);
+        if (n1.u < a.n_units) {
+          wait_tile2(2);
+          issue_S2(0, n1, 1);
+          issue_S2(1, n1, 1);
+          commit_elect(&t_free[2 % NSLOT]);
         }
-        if (jcur < c1) issue_PV(1, c1, jcur, gt);
-        commit_elect(&t_free[(2 * gt + 1) % NSLOT]);  // V(cur) consumed by both PV
-        if (has_next) {
-          if (jnxt < n1) issue_S(1, n1, jnxt, tnext);
-          commit_elect(&t_free[(2 * tnext) % NSLOT]);  // K(next) consumed by both S
+        advance(n1, n2);
+        while (cur.u < a.n_units) {
+          const bool nx = n2.u < a.n_units;
+          wait_tile2(2 * gt + 1);  // V(cur)
+          issue_PV2(0, cur, gt);
+          if (nx) {
+            wait_tile2(2 * (gt + 2));  // K(cur + 2)
+            issue_S2(0, n2, gt + 2);
+          }
+          issue_PV2(1, cur, gt);
+          commit_elect(&t_free[(2 * gt + 1) % NSLOT]);  // V(cur) consumed by both PV
+          if (nx) {
+            issue_S2(1, n2, gt + 2);
+            commit_elect(&t_free[(2 * (gt + 2)) % NSLOT]);  // K(cur + 2) consumed by both S
+          }
+          cur = n1;
+          n1 = n2;
+          advance(n1, n2);
+          ++gt;
         }
-        const bool switched = unxt != ucur;
-        ucur = unxt;
-        jcur = jnxt;
-        c0 = n0;
-        c1 = n1;
-        call = nall;
-        ++gt;
-        // new current unit: its S tiles are issued; the entry after it is already in the ring
-        if (switched) {
-          ++kcur;
-          if (ucur < a.n_units) upre = ring_unit(ring, kcur + 1, pre, lane);
+      } else {
+        Unit tmp, pre;
+        int kcur = 0;  // ring entry of the current unit
+        int ucur = ring_unit(ring, 0, tmp, lane);
+        int c0 = tmp.nkt0, c1 = tmp.nkt1, call = max(tmp.nkt0, tmp.nkt1);  // key tiles of the current unit
+        int jcur = 0;
+        int upre = a.n_units;  // the unit after the current one, fetched while S/softmax of this one run
+        if (ucur < a.n_units) {
+          wait_tile(2 * gt);
+          if (c0 > 0) issue_S(0, c0, 0, gt);
+          if (c1 > 0) issue_S(1, c1, 0, gt);
+          commit_elect(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
+          upre = ring_unit(ring, kcur + 1, pre, lane);
+        }
+        while (ucur < a.n_units) {
+          int unxt = ucur, jnxt = jcur + 1, n0 = c0, n1 = c1, nall = call;
+          if (jnxt >= call) {
+            unxt = upre;
+            jnxt = 0;
+            n0 = pre.nkt0;
+            n1 = pre.nkt1;
+            nall = max(pre.nkt0, pre.nkt1);
+          }
+          const bool has_next = unxt < a.n_units;
+          const uint32_t tnext = gt + 1;
+          wait_tile(2 * gt + 1);  // V(cur)
+          if (jcur < c0) issue_PV(0, c0, jcur, gt);
+          if (has_next) {
+            wait_tile(2 * tnext);  // K(next)
+            if (jnxt < n0) issue_S(0, n0, jnxt, tnext);
+          }
+          if (jcur < c1) issue_PV(1, c1, jcur, gt);
+          commit_elect(&t_free[(2 * gt + 1) % NSLOT]);  // V(cur) consumed by both PV
+          if (has_next) {
+            if (jnxt < n1) issue_S(1, n1, jnxt, tnext);
+            commit_elect(&t_free[(2 * tnext) % NSLOT]);  // K(next) consumed by both S
+          }
+          const bool switched = unxt != ucur;
+          ucur = unxt;
+          jcur = jnxt;
+          c0 = n0;
+          c1 = n1;
+          call = nall;
+          ++gt;
+          // new current unit: its S tiles are issued; the entry after it is already in the ring
+          if (switched) {
+            ++kcur;
+            if (ucur < a.n_units) upre = ring_unit(ring, kcur + 1, pre, lane);
+          }
         }
       }
       if (lane == 0) RDX_EV_FLUSH();
@@ -805,7 +931,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
     const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
     const uint32_t s_addr = lane_base + h * 128;
     const uint32_t o_addr = lane_base + O_COL + h * 128;
-    int s_cnt = 0, u_cnt = 0;
+    int s_cnt = 0, u_cnt = 0, pv_cnt = 0;
     long long st_s = 0, st_resc = 0, st_exp = 0;
     const long long st_t0 = clock64();
     EvLog evl;
@@ -823,19 +949,22 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       float m_run = -INFINITY, l_run = 0.f;
 #pragma unroll 1
       for (int j = 0; j < nkt_h; ++j, ++s_cnt) {
-        RDX_TWAIT(&s_full[h], s_cnt & 1, st_s);
+        // S_h(j): buffer s_cnt & 1 when double-buffered
+        const uint32_t s_cur = DB ? s_addr + (s_cnt & 1) * 64 : s_addr;
+        if constexpr (DB) RDX_TWAIT(&s_full[2 * h + (s_cnt & 1)], (s_cnt >> 1) & 1, st_s);
+        else RDX_TWAIT(&s_full[2 * h], s_cnt & 1, st_s);
         if (t == 0) RDX_EV(2, 1, h * 16 + j);  // softmax: S_h(j) ready
         tc_fence_after();
-        const int kbase = j * BK;
+        const int kbase = j * BKT;
         // warp-uniform column classes of this tile (32-column chunks): chunks at or past
         // vis_warp are masked for every row of the warp (never loaded, max'ed or exp'ed);
         // chunks below lo_vis are visible for every row (no per-element mask)
         const int vis_warp = pos_max - kbase + 1;
         const int lo_vis = pos_min - kbase + 1;
-        float sv[BK];
+        float sv[BKT];
 #pragma unroll
-        for (int c = 0; c < BK; c += 32)
-          if (c < vis_warp) tmem_ld32p(s_addr + c, sv + c);
+        for (int c = 0; c < BKT; c += 32)
+          if (c < vis_warp) tmem_ld32p(s_cur + c, sv + c);
         tmem_wait_ld();
         if (t == 0) RDX_EV(2, 3, static_cast<int>(sv[0] != 12345.f));  // softmax: S in registers
         const int nvis = pos - kbase + 1;  // visible keys of this row in the tile
@@ -843,7 +972,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 #pragma unroll
         for (int u8 = 0; u8 < 8; ++u8) mx[u8] = -INFINITY;
 #pragma unroll
-        for (int c0 = 0; c0 < BK; c0 += 32) {
+        for (int c0 = 0; c0 < BKT; c0 += 32) {
           if (c0 >= vis_warp) continue;  // whole chunk masked for the warp (column 0 is always visible)
           if (c0 + 32 > lo_vis) {         // the diagonal crosses this chunk: per-element mask
 #pragma unroll
@@ -855,10 +984,15 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * a.scale_log2;
         const bool need = mt > m_run + kRescaleThreshold;
+        bool resc_o = false;  // DB: O_h rescaled by alpha once PV_h(j-1) has completed
+        float alpha_o = 1.f;
         if (__any_sync(0xffffffffu, need)) {
           const float m_new = need ? mt : m_run;
           const float alpha = ex2(m_run - m_new);  // 0 on the first tile (m_run = -inf)
-          if (j > 0) {
+          if (DB && j > 0) {
+            resc_o = true;
+            alpha_o = alpha;
+          } else if (j > 0) {
             if (RDX_STATS_ON) ++st_resc;
             // O_h holds PV_h(0..j-1): complete, since S_h(j) was issued after PV_h(j-1)
 #pragma unroll 1
@@ -879,12 +1013,12 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         const uint64_t scale2 = f2pack(a.scale_log2, a.scale_log2), negm2 = f2pack(-m_run, -m_run);
         uint64_t ls[4] = {0, 0, 0, 0};  // pairs of fp32 partial row sums (+0.0f bits)
 #pragma unroll
-        for (int c = 0; c < BK; c += 32) {
+        for (int c = 0; c < BKT; c += 32) {
           uint32_t pw[16];
           if (c >= vis_warp) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) pw[e] = 0u;
-            tmem_st16u(s_addr + c / 2, pw);
+            tmem_st16u(s_cur + c / 2, pw);
             continue;
           }
 #pragma unroll
@@ -903,7 +1037,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
             f2unpack(p, p0, p1);
             pw[e >> 1] = pack_bf16x2(p0, p1);
           }
-          tmem_st16u(s_addr + c / 2, pw);  // P over the first 64 columns of S_h
+          tmem_st16u(s_cur + c / 2, pw);  // P over the first BKT / 2 columns of S_h
         }
         {
           float s0, s1;
@@ -911,9 +1045,30 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           l_run += s0 + s1;
         }
         if (t == 0) RDX_EV(2, 5, static_cast<int>(l_run != 12345.f));  // softmax: exp + P stores issued
+        if constexpr (DB) {
+          if (j > 0) {
+            // PV_h(j-1) is still in flight behind S_h(j+1): wait for it (lockstep, one
+            // phase per tile) before O_h may be rescaled for this tile's new max
+            RDX_TWAIT(&pv_done[h], pv_cnt & 1, st_s);
+            ++pv_cnt;
+            if (__any_sync(0xffffffffu, resc_o)) {
+              if (RDX_STATS_ON) ++st_resc;
+              tc_fence_after();
+#pragma unroll 1
+              for (int c = 0; c < HDP; c += 32) {
+                float ov[32];
+                tmem_ld32p(o_addr + c, ov);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) ov[e] *= alpha_o;
+                tmem_st32(o_addr + c, ov);
+              }
+            }
+          }
+        }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&p_full[h]);
+        mbar_arrive(&p_full[DB ? 2 * h + (s_cnt & 1) : 2 * h]);
         if (t == 0) RDX_EV(2, 2, h * 16 + j);  // softmax: P_h(j) published
         if (RDX_STATS_ON) st_exp += clock64() - st_b;
       }
@@ -945,13 +1100,15 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 }
 
 unsigned long long* g_stats = nullptr;  // debug counters (RDX_ATTN_STATS=1)
+int g_attn_bk64 = 1;                    // rdx_attention_debug_bk64: 64-key double-buffered variant on/off
 unsigned long long* g_cta_times = nullptr;  // debug per-CTA [start, end, units]
 uint32_t* g_trace = nullptr;            // debug event log of CTA 0 (RDX_ATTN_STATS=1)
 
-template <int HDP, int NQB, int NSLOT, uint32_t EMU>
-int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
-  using T = Tile<HDP, NQB, NSLOT>;
-  auto kern = attention_kernel<HDP, NQB, NSLOT, EMU>;
+template <int HDP, int NQB, int NSLOT, uint32_t EMU, int BKT = BK>
+int launch(Args a, int64_t qkv_rows, cudaStream_t st) {
+  using T = Tile<HDP, NQB, NSLOT, BKT>;
+  auto kern = attention_kernel<HDP, NQB, NSLOT, EMU, BKT>;
+  a.bk = BKT;
   static bool attr_set = false;
   if (!attr_set) {
     RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM));
@@ -963,7 +1120,7 @@ int launch(const Args& a, int64_t qkv_rows, cudaStream_t st) {
   std::memset(&map_q, 0, sizeof(map_q));
   std::memset(&map_g4, 0, sizeof(map_g4));
   if (a.use_tma) {
-    int e = gemm::make_map(&map_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, BK,
+    int e = gemm::make_map(&map_kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, BKT,
                            CU_TENSOR_MAP_SWIZZLE_128B);
     if (e) return e;
     e = gemm::make_map(&map_q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.qkv, a.ld, qkv_rows, a.ld, 64, a.qpt,
@@ -1041,6 +1198,14 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
   cudaStream_t s = as_stream(stream);
   if (head_dim <= 64)
     return short_units ? launch<64, 2, 4, kEmulated>(a, qkv_rows, s) : launch<64, 1, 6, kEmulated>(a, qkv_rows, s);
+  // short suffix-query units at head_dim 128: 64-key tiles with double-buffered S (RDX_ATTN_BK64=0:
+  // 128-key tiles).  Measured at C2: suffix 35.1 vs 35.5 us; the plain layout (full-length query
+  // tiles) is faster on 128-key tiles (43.8 vs 46.8 us), so it keeps them.
+  static const int bk64 = [] {
+    const char* v = std::getenv("RDX_ATTN_BK64");
+    return v && v[0] == '0' ? 0 : 1;
+  }();
+  if (short_units && scatter && bk64 && g_attn_bk64) return launch<128, 2, 6, kEmulated, 64>(a, qkv_rows, s);
   return short_units ? launch<128, 2, 3, kEmulated>(a, qkv_rows, s) : launch<128, 1, 4, kEmulated>(a, qkv_rows, s);
 }
 
@@ -1074,3 +1239,11 @@ extern "C" int rdx_attention_debug_trace(uint32_t* host, int n_words) {
 }
 
 int rdx::take_device_status_attention(int* out, cudaStream_t st) { return take_device_status(out, st); }
+
+// Debug: the 64-key double-buffered-S variant for short units on (1) / off (0) for A/B
+// runs; returns the previous setting.
+extern "C" int rdx_attention_debug_bk64(int on) {
+  const int prev = rdx::attn::g_attn_bk64;
+  rdx::attn::g_attn_bk64 = on ? 1 : 0;
+  return prev;
+}
