@@ -89,7 +89,9 @@ const char* rdx_last_cuda_error(void);
  *                   (compact rows of sequence s are [cu_q[s], cu_q[s+1]))
  *   lcp_out[B]      i32 shared-prefix length of each sequence (may be NULL)
  *   info_out[4]     u32: [0]=N', [1]=status (rdx_status), [2]=hash attempts
- *                   used, [3]=reserved
+ *                   used, [3]=max_q (longest compact suffix, rows).  May be
+ *                   pinned host memory (device-addressable under unified
+ *                   addressing): the kernel writes it directly, no copy.
  * scratch: at least rdx_plan_scratch_bytes(N, B) bytes of device memory.
  * --------------------------------------------------------------------- */
 #define RDX_PLAN_ALLOW_EMPTY 0x1u

@@ -158,6 +158,8 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
     }
   } grid;
   __shared__ uint64_t warp_tot[kPlanWarps];
+  __shared__ uint32_t s_vmax;
+  if (threadIdx.x == 0) s_vmax = 0;
 
   const int64_t n = a.n;
   const int64_t nseq = a.nseq;
@@ -209,6 +211,7 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
         a.info[0] = 0;
         a.info[1] = st;
         a.info[2] = 0;
+        a.info[3] = 0;
       }
       return;  // uniform across the grid
     }
@@ -253,40 +256,87 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
     }
     grid.sync();
 
-    // ---- P2: path hashes into the first-occurrence table ----
+    // ---- P2: path hashes into the first-occurrence table.  Only tokens whose path
+    // differs from the same depth of the previous sequence are inserted (the first
+    // occurrence of a path always is one); long shared prefixes then cost one insert
+    // per node instead of B contending atomics, the other tokens look their key up in P3.
+    auto Pm = [&](int64_t x) -> uint64_t { return x < 0 ? 0ULL : s.P[x]; };
     for (int64_t i = gtid; i < n; i += nthreads) {
       const uint32_t sq = s.seg[i];
       const int64_t st = cu[sq];
-      const uint64_t h = s.P[i] - (st > 0 ? s.P[st - 1] : 0ULL);
-      uint64_t key = fmix64(h ^ seed);
-      if (key == 0) key = 1;
-      uint64_t t = key & tmask;
-      while (true) {
-        const unsigned long long prev =
-            atomicCAS(reinterpret_cast<unsigned long long*>(&s.keys[t]), 0ULL,
-                      static_cast<unsigned long long>(key));
-        if (prev == 0ULL || prev == key) break;
-        t = (t + 1) & tmask;
+      const uint64_t h = s.P[i] - Pm(st - 1);
+      bool insert = true;
+      if (sq > 0) {
+        const int64_t pst = cu[sq - 1];
+        if (i - st < st - pst) insert = (Pm(pst + (i - st)) - Pm(pst - 1)) != h;
       }
-      atomicMin(&s.vals[t], static_cast<uint32_t>(i));
-      s.slot[i] = static_cast<uint32_t>(t);
+      uint32_t slot = 0xFFFFFFFFu;
+      if (insert) {
+        uint64_t key = fmix64(h ^ seed);
+        if (key == 0) key = 1;
+        uint64_t t = key & tmask;
+        while (true) {
+          const unsigned long long prev =
+              atomicCAS(reinterpret_cast<unsigned long long*>(&s.keys[t]), 0ULL,
+                        static_cast<unsigned long long>(key));
+          if (prev == 0ULL || prev == key) break;
+          t = (t + 1) & tmask;
+        }
+        atomicMin(&s.vals[t], static_cast<uint32_t>(i));
+        slot = static_cast<uint32_t>(t);
+      }
+      s.slot[i] = slot;
     }
     grid.sync();
 
-    // ---- P3: representatives + inductive verification + lcp ----
+    // ---- P3: representatives (lookups for non-inserted tokens) + inductive verification
+    // (rep is a function of the key, so rep(i-1) == rep(rep_i - 1) <=> H_{i-1} == H_{rep_i - 1})
+    // + lcp (warp-aggregated atomicMin: one per sequence run of a warp) ----
     {
       uint32_t fail = 0;
-      for (int64_t i = gtid; i < n; i += nthreads) {
-        const uint32_t r = s.vals[s.slot[i]];
-        s.rep[i] = r;
-        const uint32_t si = s.seg[i];
-        const int64_t di = i - cu[si];
-        const uint32_t sr = s.seg[r];
-        const int64_t dr = static_cast<int64_t>(r) - cu[sr];
-        bool ok = (tok[r] == tok[i]) && (pos[r] == pos[i]) && (dr == di);
-        if (ok && di > 0) ok = s.vals[s.slot[i - 1]] == s.vals[s.slot[r - 1]];
-        if (!ok) fail = 1;
-        if (r == static_cast<uint32_t>(i)) atomicMin(&s.lcp[si], static_cast<int32_t>(di));
+      for (int64_t i0 = gtid - (threadIdx.x & 31); i0 < n; i0 += nthreads) {  // warp-uniform trip count
+        const int64_t i = i0 + (threadIdx.x & 31);
+        const bool live = i < n;
+        uint32_t si = 0xFFFFFFFFu;
+        int32_t mine = INT_MAX;
+        if (live) {
+          si = s.seg[i];
+          const int64_t st = cu[si];
+          const int64_t di = i - st;
+          const uint64_t pst1 = Pm(st - 1);
+          uint64_t t = s.slot[i];
+          bool lost = false;
+          if (t == 0xFFFFFFFFu) {
+            uint64_t key = fmix64((s.P[i] - pst1) ^ seed);
+            if (key == 0) key = 1;
+            t = key & tmask;
+            while (true) {
+              const uint64_t k = s.keys[t];
+              if (k == key) break;
+              if (k == 0ULL) {  // unreachable unless hashes collided: new seed
+                lost = true;
+                break;
+              }
+              t = (t + 1) & tmask;
+            }
+          }
+          const uint32_t r = lost ? static_cast<uint32_t>(i) : s.vals[t];
+          s.rep[i] = r;
+          if (lost) fail = 1;
+          if (r == static_cast<uint32_t>(i)) {
+            mine = static_cast<int32_t>(di);
+          } else {
+            const uint32_t sr = s.seg[r];
+            const int64_t sst = cu[sr];
+            bool ok = (tok[r] == tok[i]) && (pos[r] == pos[i]) && (static_cast<int64_t>(r) - sst == di);
+            if (ok && di > 0) ok = (s.P[i - 1] - pst1) == (s.P[r - 1] - Pm(sst - 1));
+            if (!ok) fail = 1;
+          }
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, si);
+        const int32_t mn = __reduce_min_sync(grp, mine);
+        if (live && mn != INT_MAX && static_cast<int>(threadIdx.x & 31) == __ffs(grp) - 1)
+          atomicMin(&s.lcp[si], mn);
       }
       if (__syncthreads_or(fail) && threadIdx.x == 0) atomicOr(&s.flags[attempt], 1u);
     }
@@ -296,9 +346,11 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
     // ---- P4: cu_q (block 0) ----
     if (blockIdx.x == 0) {
       uint64_t carry = 0;
+      uint32_t vmax = 0;  // longest compact suffix (info[3] = max_q)
       for (int64_t base = 0; base < nseq; base += blockDim.x) {
         const int64_t q = base + threadIdx.x;
         const uint64_t v = q < nseq ? static_cast<uint64_t>(cu[q + 1] - cu[q] - s.lcp[q]) : 0;
+        vmax = max(vmax, static_cast<uint32_t>(v));
         uint64_t tile_total;
         const uint64_t ex = block_exclusive_scan_u64(v, warp_tot, tile_total);
         if (q < nseq) {
@@ -307,11 +359,15 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
         }
         carry += tile_total;
       }
+      vmax = __reduce_max_sync(0xffffffffu, vmax);
+      if ((threadIdx.x & 31) == 0) atomicMax(&s_vmax, vmax);
+      __syncthreads();
       if (threadIdx.x == 0) {
         a.cu_q[nseq] = static_cast<int32_t>(carry);
         a.info[0] = static_cast<uint32_t>(carry);
         a.info[1] = RDX_OK;
         a.info[2] = static_cast<uint32_t>(attempt + 1);
+        a.info[3] = s_vmax;
       }
     }
     grid.sync();
@@ -335,6 +391,7 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
     a.info[0] = 0;
     a.info[1] = RDX_ERR_HASH_RETRIES;
     a.info[2] = kMaxAttempts;
+    a.info[3] = 0;
   }
 }
 
@@ -420,6 +477,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
   __shared__ uint64_t s_carry[kSmMaxCtas];
   __shared__ uint64_t s_total;
   __shared__ uint32_t s_flags[kMaxAttempts + 1];  // [0] validation bits, [1 + t] attempt t failed (CTA 0's copy counts)
+  __shared__ uint32_t s_vmax;
 
   const int tid = threadIdx.x;
   auto mark = [&](int k) {
@@ -439,6 +497,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     s_pos[j] = a.pos[lo + j];
   }
   if (tid <= kMaxAttempts) s_flags[tid] = 0;
+  if (tid == 0) s_vmax = 0;
   __syncthreads();
   {
     uint32_t bits = 0;  // bit0 start!=0, bit1 decrease, bit2 empty, bit3 end!=n
@@ -468,6 +527,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
                     : (bits & 6u) ? RDX_ERR_NON_MONOTONE_OFFSETS
                                   : RDX_ERR_BOUNDARY_MISMATCH;
         a.info[2] = 0;
+        a.info[3] = 0;
       }
       cl_sync();  // nobody leaves while another CTA may still read CTA 0's flag
       return;
@@ -659,9 +719,11 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     {
       uint64_t carry = 0;
+      uint32_t vmax = 0;  // longest compact suffix (info[3] = max_q)
       for (int64_t base = 0; base < nseq; base += kSmThreads) {
         const int64_t q = base + tid;
         const uint64_t v = q < nseq ? static_cast<uint64_t>(s_cu[q + 1] - s_cu[q] - s_lcp[q]) : 0;
+        vmax = max(vmax, static_cast<uint32_t>(v));
         uint64_t tile_total;
         const uint64_t ex = block_exclusive_scan_u64_w<kSmWarps>(v, s_wtot, tile_total);
         if (q < nseq) {
@@ -673,6 +735,11 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
         }
         carry += tile_total;
       }
+      if (me == 0) {
+        vmax = __reduce_max_sync(0xffffffffu, vmax);
+        if ((tid & 31) == 0) atomicMax(&s_vmax, vmax);
+        __syncthreads();
+      }
       if (tid == 0) {
         s_cuq[nseq] = static_cast<int32_t>(carry);
         if (me == 0) {
@@ -680,6 +747,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
           a.info[0] = static_cast<uint32_t>(carry);
           a.info[1] = RDX_OK;
           a.info[2] = static_cast<uint32_t>(attempt + 1);
+          a.info[3] = s_vmax;
         }
       }
     }
@@ -709,6 +777,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     a.info[0] = 0;
     a.info[1] = RDX_ERR_HASH_RETRIES;
     a.info[2] = kMaxAttempts;
+    a.info[3] = 0;
   }
   cl_sync();
 }

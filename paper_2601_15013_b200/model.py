@@ -323,7 +323,7 @@ class _Layout:
     max_q: int
     suffix_ok: bool
     dedup: bool
-    cu_q_host: object = None
+    cu_q_host: object = None  # host cu_q (np.ndarray) or the DevicePlan that reads it lazily
 
 
 class _Graph:
@@ -482,7 +482,7 @@ class RadixQwen3:
             if plan.n_original != db.n or plan.scatter.shape[0] != db.n:
                 raise PlanBatchMismatch(f"plan built for {plan.n_original} tokens, batch has {db.n}")
             return _Layout(plan.n_padded, plan.n_compact, plan.gather, plan.scatter, plan.compact_positions,
-                           plan.cu_q, plan.max_q_len, True, True, plan.cu_q_host)
+                           plan.cu_q, plan.max_q_len, True, True, plan)  # cu_q host copy read only if needed
         if isinstance(plan, CompactionPlan):
             if plan.n_original != db.n:
                 raise PlanBatchMismatch(f"plan built for {plan.n_original} tokens, batch has {db.n}")
@@ -542,10 +542,15 @@ class RadixQwen3:
     def _graph_shape(self, db, lay, mode):
         """(m_b, n_b, b_b, max_q_b, max_k_b) of the bucket a batch falls in."""
         r = self._round
+        # the row bucket grows with M (256 below 16K rows, 512 below 32K, ...): at most ~1.6 %
+        # padding, and a distribution of large batches maps onto a few graphs
+        def mq(m):
+            return self.M_BUCKET << max(0, int(m).bit_length() - 14)
+
         if mode == "plain":
-            m_b = n_b = r(db.n, self.M_BUCKET)
+            m_b = n_b = r(db.n, mq(db.n))
         else:
-            m_b, n_b = r(lay.m, self.M_BUCKET), r(db.n, self.N_BUCKET)
+            m_b, n_b = r(lay.m, mq(lay.m)), r(db.n, self.N_BUCKET)
         max_k = r(db.max_len, self.LEN_BUCKET)
         max_q = max_k if mode == "plain" else r(lay.max_q, self.LEN_BUCKET)
         return m_b, n_b, r(db.b, self.B_BUCKET), max_q, max_k
@@ -658,6 +663,8 @@ class RadixQwen3:
         if mode != "suffix":
             return full
         cu_q = getattr(lay, "cu_q_host", None)
+        if cu_q is not None and not isinstance(cu_q, np.ndarray):
+            cu_q = cu_q.cu_q_host  # a DevicePlan: its lazily read host copy
         if cu_q is None:
             return full
         lcp = lens - np.diff(cu_q)

@@ -22,7 +22,7 @@ from fractions import Fraction
 import numpy as np
 
 from . import _native
-from .errors import CapacityExceeded, EmptyPlan, raise_for_status
+from .errors import CapacityExceeded, EmptyPlan, NativeLibraryError, raise_for_status
 from .ragged import RaggedBatch, validate_batch
 
 
@@ -63,7 +63,8 @@ class DevicePlan:
     ``scatter`` has ``n_original``; all int32 views of the u32 maps.
     ``cu_q`` (device, int32 [B+1]) delimits each sequence's compact suffix
     (finding 2 of SURVEY.md: compact rows of sequence s are the contiguous
-    range [cu_q[s], cu_q[s+1]) ); ``cu_q_host`` is its host copy.
+    range [cu_q[s], cu_q[s+1]) ); ``cu_q_host`` is its host copy, read on first
+    use (the planner returns N', the status and max_q without copying cu_q).
     """
 
     gather: "object"
@@ -71,11 +72,18 @@ class DevicePlan:
     compact_positions: "object"
     cu_q: "object"
     lcp: "object"
-    cu_q_host: np.ndarray
     n_original: int
     n_compact: int
     attempts: int = 1
+    max_q: int = -1  # longest compact suffix (rows of one sequence), from the planner
     extras: dict = field(default_factory=dict)
+    _cu_q_host: object = field(default=None, repr=False)
+
+    @property
+    def cu_q_host(self) -> np.ndarray:
+        if self._cu_q_host is None:
+            self._cu_q_host = self.cu_q.cpu().numpy().astype(np.int64)
+        return self._cu_q_host
 
     @property
     def n_padded(self) -> int:
@@ -87,6 +95,8 @@ class DevicePlan:
 
     @property
     def max_q_len(self) -> int:
+        if self.max_q >= 0:
+            return self.max_q
         return int(np.diff(self.cu_q_host).max()) if self.cu_q_host.size > 1 else 0
 
     def to_host(self) -> CompactionPlan:
@@ -124,29 +134,26 @@ _WORKSPACE = _Workspace()
 _PINNED = threading.local()
 
 
-def _read_info(info_cu, stream):
-    """D2H of (N', status, attempts, -, cu_q) through a reused pinned buffer (thread-local,
-    so concurrent planners on different threads do not share it)."""
+def _info_buffer():
+    """Thread-local pinned 4-word buffer the planner kernel writes (N', status, attempts,
+    max_q) into directly: host memory allocated by cudaHostAlloc is device-addressable
+    under unified addressing, so no device-to-host copy is queued after the kernel."""
     import torch
 
-    k = info_cu.numel()
-    buf = getattr(_PINNED, "buf", None)
-    if buf is None or buf.numel() < k:
-        buf = torch.empty(max(k, 1024), dtype=torch.int32, pin_memory=True)
-        _PINNED.buf = buf
-    st = torch.cuda.current_stream(info_cu.device) if stream is None else stream
-    with torch.cuda.stream(st):
-        buf[:k].copy_(info_cu, non_blocking=True)
-    st.synchronize()
-    return buf[:k].numpy().copy()
+    buf = getattr(_PINNED, "info", None)
+    if buf is None:
+        buf = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        _PINNED.info = buf
+    return buf
 
 
 def build_plan_device(tok, pos, cu, *, allow_empty: bool = False, stream=None,
                       n_original: int | None = None) -> DevicePlan:
     """GPU planner on device tensors (tok/pos int32-viewed u32 [N], cu int64 [B+1]).
 
-    One cooperative kernel computes gather/scatter/compact_positions/cu_q;
-    one D2H copy of (N', status, attempts, cu_q) follows.
+    One kernel computes gather/scatter/compact_positions/cu_q and writes
+    (N', status, attempts, max_q) straight into pinned host memory; the call
+    returns after one stream synchronisation.
     """
     import torch
 
@@ -156,36 +163,39 @@ def build_plan_device(tok, pos, cu, *, allow_empty: bool = False, stream=None,
     b = int(cu.shape[0]) - 1
     if n >= (1 << 32) - 1:
         raise CapacityExceeded(f"{n} tokens exceed 32-bit index range")
-    # one allocation for every output: gather | scatter | compact_positions | info+cu_q | lcp
+    # one allocation for every output: gather | scatter | compact_positions | cu_q | lcp
     nn, nb = max(n, 1), max(b, 1)
-    buf = torch.empty(3 * nn + (4 + b + 1) + nb, dtype=torch.int32, device=dev)
-    gather, scatter, cpos = buf[:nn], buf[nn:2 * nn], buf[2 * nn:3 * nn]
-    info_cu = buf[3 * nn:3 * nn + 4 + b + 1]
-    lcp = buf[3 * nn + 4 + b + 1:]
-    scratch_bytes = int(lib.rdx_plan_scratch_bytes(n, b))
-    scratch = _WORKSPACE.get(dev, scratch_bytes)
+    buf = torch.empty(3 * nn + (b + 1) + nb, dtype=torch.int32, device=dev)
+    o = 3 * nn
+    cu_q, lcp = buf[o:o + b + 1], buf[o + b + 1:]
+    scratch = _WORKSPACE.get(dev, int(lib.rdx_plan_scratch_bytes(n, b)))
     flags = _native.RDX_PLAN_ALLOW_EMPTY if allow_empty else 0
-    st = _native.stream_handle(stream)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    info = _info_buffer()
+    iv = info.numpy()
+    iv[1] = -1  # status sentinel: a kernel that never ran cannot leave a stale RDX_OK behind
+    p0 = buf.data_ptr()
     code = lib.rdx_plan_build(
         tok.data_ptr(), pos.data_ptr(), cu.data_ptr(), b, n, flags,
-        gather.data_ptr(), scatter.data_ptr(), cpos.data_ptr(),
-        info_cu.data_ptr() + 16, lcp.data_ptr(), info_cu.data_ptr(),
-        scratch.data_ptr(), ctypes.c_size_t(scratch.numel()), st,
+        p0, p0 + 4 * nn, p0 + 8 * nn, cu_q.data_ptr(), lcp.data_ptr(), info.data_ptr(),
+        scratch.data_ptr(), ctypes.c_size_t(scratch.numel()), st.cuda_stream,
     )
     _native.check(code, "rdx_plan_build")
-    host = _read_info(info_cu, stream)  # the one synchronising read
-    n_compact, status, attempts = int(host[0]), int(host[1]), int(host[2])
+    st.synchronize()  # the one host wait: the kernel's (N', status, attempts, max_q) are in `info`
+    n_compact, status, attempts, max_q = (int(x) for x in iv)
+    if status == -1:
+        raise NativeLibraryError("rdx_plan_build: the planner kernel did not report a status")
     raise_for_status(status, "rdx_plan_build")
     return DevicePlan(
-        gather=gather[:n_compact],
-        scatter=scatter[:n],
-        compact_positions=cpos[:n_compact],
-        cu_q=info_cu[4:],
+        gather=buf[:n_compact],
+        scatter=buf[nn:nn + n],
+        compact_positions=buf[2 * nn:2 * nn + n_compact],
+        cu_q=cu_q,
         lcp=lcp[:b],
-        cu_q_host=host[4:].astype(np.int64),
         n_original=n,
         n_compact=n_compact,
         attempts=attempts,
+        max_q=max_q,
     )
 
 
