@@ -510,6 +510,32 @@ def _event_time(fn, iters=10, warm=2, flush=None):
     return statistics.median(ts)
 
 
+def _graph_time(fn, reps=10):
+    """Device time (ms) per call of a launch-only fn: `reps` calls captured in one CUDA graph and
+    replayed, so host submission latency is not in the number (median of 5 replays)."""
+    import torch
+
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) / reps)
+    return sorted(ts)[2]
+
+
 def run_micro(args):
     """BASELINE configs[4]: index build and gather/scatter over ragged batches of
     1K-1M tokens (prefix-sharing ratios 0..1, multi-level tries): GPU planner
@@ -547,16 +573,16 @@ def run_micro(args):
         info = torch.empty(4 + b + 1, dtype=torch.int32, device="cuda")
         lcp = torch.empty(max(b, 1), dtype=torch.int32, device="cuda")
         scratch = _WORKSPACE.get(tok.device, int(lib.rdx_plan_scratch_bytes(nn, b)))
-        st = _native.stream_handle()
-
         def kernel_only():
             _native.check(lib.rdx_plan_build(tok.data_ptr(), pos.data_ptr(), cu.data_ptr(), b, nn, 0,
                                              gather.data_ptr(), scatter.data_ptr(), cpos.data_ptr(),
                                              info.data_ptr() + 16, lcp.data_ptr(), info.data_ptr(),
-                                             scratch.data_ptr(), ctypes.c_size_t(scratch.numel()), st),
+                                             scratch.data_ptr(), ctypes.c_size_t(scratch.numel()),
+                                             _native.stream_handle()),
                           "rdx_plan_build")
 
-        ms_kernel = _event_time(kernel_only, flush=flush)
+        ms_launch = _event_time(kernel_only, flush=flush)  # host-submitted launch, L2 flushed before it
+        ms_kernel = _graph_time(kernel_only)                # device time per launch (CUDA graph of 10)
         ms_api = _event_time(lambda: build_plan_device(tok, pos, cu), flush=flush)
         plan = build_plan_device(tok, pos, cu)
         g, sc, cp, m = orc.build_plan_oracle(batch.token_ids, batch.position_ids, batch.cu_seqlens)
@@ -564,6 +590,7 @@ def run_micro(args):
                                                              batch.cu_seqlens), reps=5) * 1e3
         rec = {"case": name, "N": nn, "B": b, "N_compact": plan.n_compact,
                "gamma": round(plan.n_compact / max(nn, 1), 4), "gpu_kernel_us": round(ms_kernel * 1e3, 1),
+               "gpu_launch_us": round(ms_launch * 1e3, 1),
                "gpu_api_us": round(ms_api * 1e3, 1), "cpu_port_us": round(port_ms * 1e3, 1)}
         if ref is not None:
             rb = ref.RaggedBatch(batch.token_ids, batch.position_ids, batch.cu_seqlens)
