@@ -65,9 +65,10 @@ typedef enum rdx_status {
   RDX_ERR_CUDA = 100
 } rdx_status;
 
-/* Library version (major*10000 + minor*100 + patch): 200 = 0.2.0, whose
- * rdx_gemm_args ends at done_ctr.  Check it against RDX_VERSION before use. */
-#define RDX_VERSION 200
+/* Library version (major*10000 + minor*100 + patch): 300 = 0.3.0, whose
+ * rdx_gemm_args ends at a_ready_use and whose rdx_rmsnorm_rows_after takes
+ * ready_ctr.  Check it against RDX_VERSION before use. */
+#define RDX_VERSION 300
 int rdx_version(void);
 /* Stable name of a status code ("RDX_OK", "IndexOutOfRange", …). */
 const char* rdx_status_name(int status);
@@ -168,6 +169,10 @@ int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t
                      int64_t d, const float* w, float eps, void* out_bf16, int64_t ld_out,
                      void* stream);
 
+/* First device-side failure of an asynchronous contract since the last call
+ * (RDX_OK or RDX_ERR_DEVICE_TIMEOUT), then cleared; synchronises `stream`. */
+int rdx_device_status(void* stream);
+
 /* rdx_rmsnorm_rows on rows 0..n_rows-1 that may still be in flight from a
  * preceding rdx_gemm (RDX_EPI_RESID_F32 with done_ctr) on the same stream: the
  * kernel is launched as a programmatic dependent of that GEMM (it can start on
@@ -175,14 +180,14 @@ int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t
  * done_ctr[r / 32] >= target (a slab still incomplete after ~8 s stops the wait,
  * the rows are normalised as found and rdx_device_status reports
  * RDX_ERR_DEVICE_TIMEOUT: the counters and targets did not match).  d must be 128 * V for V in {2, 4, 8, 16, 20, 32}
- * (else RDX_ERR_UNSUPPORTED: use rdx_rmsnorm_rows after a stream-ordered GEMM). */
-/* First device-side failure of an asynchronous contract since the last call
- * (RDX_OK or RDX_ERR_DEVICE_TIMEOUT), then cleared; synchronises `stream`. */
-int rdx_device_status(void* stream);
-
+ * (else RDX_ERR_UNSUPPORTED: use rdx_rmsnorm_rows after a stream-ordered GEMM).
+ * ready_ctr (may be NULL): ceil(n_rows / 32) counters; every finished row adds 1 to
+ * ready_ctr[row / 32] (release) and the grid becomes one small block per SM whose
+ * registers fit beside a GEMM CTA, so a chained consumer rdx_gemm (a_ready =
+ * ready_ctr) runs concurrently with the norm's last rows. */
 int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_rows, int64_t d, const float* w, float eps,
                            void* out_bf16, int64_t ld_out, const uint32_t* done_ctr, uint32_t target,
-                           void* stream);
+                           uint32_t* ready_ctr, void* stream);
 
 /* RoPE table for compact rows: table[j][i] = (cos, sin)(pos[j] * theta^(-2i/hd))
  * for i < hd/2, computed in fp64 and rounded to fp32 (model.py:165-172). */
@@ -267,6 +272,13 @@ typedef struct rdx_gemm_args {
    * when its counter has grown by N); done_ctr holds ceil(M / 32) counters.
    * Feeds rdx_rmsnorm_rows_after. */
   uint32_t* done_ctr;
+  /* Chained A (any epilogue): when a_ready != NULL the A rows of 32-row slab s are
+   * read only once a_ready[s] >= a_ready_use * rows_in_slab(s) (the ready_ctr of a
+   * preceding rdx_rmsnorm_rows_after that wrote A).  The launch is then that norm's
+   * programmatic dependent and does not wait for its grid: the GEMM's first tiles
+   * overlap the norm's last rows.  Tiles run in row-block-major order (< 64 row blocks). */
+  const uint32_t* a_ready;
+  uint32_t a_ready_use;
 } rdx_gemm_args;
 
 int rdx_gemm(const rdx_gemm_args* args, void* stream);

@@ -110,6 +110,8 @@ class GemmArgs(ctypes.Structure):
         ("rope_pos", _vp),
         ("rope_theta", _f64),
         ("done_ctr", _vp),
+        ("a_ready", _vp),
+        ("a_ready_use", _u32),
     ]
 
 
@@ -133,7 +135,7 @@ _SIGNATURES = {
     "rdx_embed_rows": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "rdx_rmsnorm_rows": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _i64, _vp]),
     "rdx_device_status": (ctypes.c_int, [_vp]),
-    "rdx_rmsnorm_rows_after": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _f32, _vp, _i64, _vp, _u32, _vp]),
+    "rdx_rmsnorm_rows_after": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _f32, _vp, _i64, _vp, _u32, _vp, _vp]),
     "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_rope_table_blocked": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmArgs), _vp]),

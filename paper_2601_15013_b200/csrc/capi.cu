@@ -39,7 +39,7 @@ bool pdl_enabled() {
 
 }  // namespace rdx
 
-extern "C" int rdx_version(void) { return 200; }  // 0.2.0: rdx_gemm_args grew (rope_blocked, rope_pos, rope_theta, done_ctr)
+extern "C" int rdx_version(void) { return 300; }  // 0.3.0: rdx_gemm_args grew (a_ready, a_ready_use); rdx_rmsnorm_rows_after took ready_ctr
 
 extern "C" const char* rdx_status_name(int status) {
   switch (status) {
@@ -70,8 +70,10 @@ extern "C" int rdx_device_status(void* stream) {
   int a = 0, r = 0;
   if (int rc = rdx::take_device_status_attention(&a, st)) return rc;
   if (int rc = rdx::take_device_status_rowops(&r, st)) return rc;
+  int g = 0;
+  if (int rc = rdx::take_device_status_gemm(&g, st)) return rc;
   RDX_CUDA_TRY(cudaStreamSynchronize(st));
-  return a ? a : r;
+  return a ? a : (r ? r : g);
 }
 
 extern "C" int rdx_num_sms(void) { return rdx::num_sms(); }

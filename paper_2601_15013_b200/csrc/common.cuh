@@ -24,6 +24,12 @@ int set_cuda_error(cudaError_t e);  // records the string, returns RDX_ERR_CUDA
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // First device-side failure of an asynchronous contract in this translation unit
 // (a slab wait that timed out, a misaligned smem base): one copy per .cu file
 // (no relocatable device code), read and cleared by take_device_status_<tu>() for
@@ -39,6 +45,7 @@ inline int take_device_status(int* out, cudaStream_t st) {
 }  // namespace
 int take_device_status_attention(int* out, cudaStream_t st);
 int take_device_status_rowops(int* out, cudaStream_t st);
+int take_device_status_gemm(int* out, cudaStream_t st);
 
 int num_sms();
 

@@ -91,6 +91,11 @@ struct EpiParams {
   // persistent grid, so the rounds stay balanced (see choose_colpart).
   int cp_ncol, cp_wide, cp_narrow;
   uint32_t cp_mask;
+  // chained A (rdx_rmsnorm_rows_after with ready_ctr): A rows of 32-row slab s are ready
+  // once a_ready[s] >= a_ready_use * rows(s); the producer waits per tile instead of the
+  // launch waiting for the whole norm grid (programmatic dependent without griddepcontrol.wait)
+  const uint32_t* a_ready;
+  uint32_t a_ready_use;
   // RDX_EPI_RESID_F32 with a completion counter: tiles in row-block-major order, and
   // per 32-row slab the number of columns whose stores have completed
   uint32_t* done_ctr;
@@ -661,8 +666,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   if (threadIdx.x == 0) GTIME_MAX(2);
-  // everything above overlapped the previous kernel's tail (PDL); inputs from here on
-  pdl_wait();
+  // everything above overlapped the previous kernel's tail (PDL); inputs from here on.
+  // A chained consumer does not wait for its predecessor grid: it waits per tile on the
+  // norm's ready counters (producer below); weights and outputs have no other producer.
+  if (!ep.a_ready) pdl_wait();
   pdl_launch_dependents();
 
   if (warp == 0) {
@@ -678,6 +685,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const int32_t m0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM);
         const int32_t nb0 = static_cast<int32_t>(n0 + rank * b_rows);
         const uint32_t bytes = C::A_BYTES + static_cast<uint32_t>(b_rows) * (BK * 2);
+        if (ep.a_ready && m0 < M) {
+          const int64_t r_hi = (m0 + BM < M ? m0 + BM : M) - 1;
+          for (int64_t slab = m0 >> 5; slab <= (r_hi >> 5); ++slab) {
+            const uint32_t rows = static_cast<uint32_t>(M - slab * 32 < 32 ? M - slab * 32 : 32);
+            const uint32_t want = ep.a_ready_use * rows;
+            unsigned ns = 64;
+            uint32_t spins = 0;
+            while (ld_acquire_u32(ep.a_ready + slab) < want) {
+              __nanosleep(ns);
+              ns = ns < 1024 ? 2 * ns : ns;
+              if (++spins > (1u << 23)) {  // ~8 s: the norm never published these rows
+                atomicCAS(&g_device_status, 0, static_cast<int>(RDX_ERR_DEVICE_TIMEOUT));
+                break;
+              }
+            }
+          }
+          // the rows were written by generic-proxy stores of another grid: order this
+          // thread's acquire before its async-proxy (TMA) reads of them
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         const CUtensorMap* mapb;
         if (ep.cp_ncol > 0) {
           mapb = width == ep.cp_wide ? &tmB2 : &tmB4;  // boxes of cp_wide / cp_narrow rows (host)
@@ -1106,6 +1133,8 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   ep.ss_out = a.ss_out;
   ep.ss_out_parts = static_cast<int>(a.n / kNormGroup);
   ep.done_ctr = EPI == RDX_EPI_RESID_F32 ? a.done_ctr : nullptr;
+  ep.a_ready = a.a_ready;
+  ep.a_ready_use = a.a_ready_use;
   {
     const int64_t m_tiles = (a.m + BM * CG - 1) / (BM * CG);
     // Default raster: with many row blocks (C3/C4 scale: A = M x K no longer fits L2)
@@ -1116,7 +1145,7 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
     // completion counter is attached).
     int gm = group_m_setting();
     if (gm <= 0) gm = m_tiles >= 64 ? (a.k >= 8192 ? group_m_bigk_setting() : 16)
-                                     : (ep.done_ctr ? 1 : static_cast<int>(m_tiles));
+                                     : ((ep.done_ctr || ep.a_ready) ? 1 : static_cast<int>(m_tiles));
     ep.group_m = static_cast<int>(gm < m_tiles ? gm : m_tiles);
   }
   const int64_t tiles = ((a.m + BM * CG - 1) / (BM * CG)) * ((a.n + BN - 1) / BN);
@@ -1177,7 +1206,7 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[1].val.programmaticStreamSerializationAllowed = (pdl_enabled() || ep.a_ready) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mb2, mb4, mc, md, a.m, a.n, a.k, tail_start, split, ep));
@@ -1362,3 +1391,5 @@ extern "C" int rdx_gemm_debug_tail_split(int on) {
   rdx::gemm::g_tail_split = on ? 1 : 0;
   return prev;
 }
+
+int rdx::take_device_status_gemm(int* out, cudaStream_t st) { return take_device_status(out, st); }

@@ -264,30 +264,32 @@ rmsnorm_rows_pipe_kernel(const float* __restrict__ x, int64_t ld_x, const uint32
 // 32-row slab counter reaches `target` (acquire), in row order, so the blocks that
 // land on SMs the GEMM's last round leaves idle work on the row blocks it has
 // already finished.
-__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 #ifndef RDX_NORM_BACKOFF_MAX
 #define RDX_NORM_BACKOFF_MAX 2048  // ns: the slab poller's longest nanosleep
 #endif
 
-template <int V>
-__global__ void __launch_bounds__(256)
+// W warps per block, one row per warp per step.  ready_ctr != NULL (the chained mode):
+// after each step the block publishes its W finished rows on ready_ctr[slab] (release),
+// so a consumer GEMM launched as this kernel's programmatic dependent can stream A rows
+// as they become ready; the launch trigger fires at entry so that consumer can launch
+// (its CTAs start as the producing GEMM's CTAs exit).  The chained grid is one small
+// block per SM whose registers fit beside a GEMM CTA (see rdx_rmsnorm_rows_after).
+template <int V, int W>
+__global__ void __launch_bounds__(W * 32)
 rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_rows, const float* __restrict__ w,
                           float eps, __nv_bfloat16* __restrict__ out, int64_t ld_out,
-                          const uint32_t* __restrict__ done_ctr, uint32_t target) {
+                          const uint32_t* __restrict__ done_ctr, uint32_t target, uint32_t* ready_ctr) {
   constexpr int D = 128 * V;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // A block takes 8 consecutive rows (one per warp) per step.  One thread polls
+  if (ready_ctr) pdl_launch_dependents();
+  // A block takes W consecutive rows (one per warp) per step.  One thread polls
   // their slab counters (acquire, backing off) so waiting blocks add almost no L2
   // traffic.  No cross-step prefetch: a block must not wait on a later, unfinished
   // row block while it holds rows that are ready.
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * 8; base < n_rows; base += static_cast<int64_t>(gridDim.x) * 8) {
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * W; base < n_rows; base += static_cast<int64_t>(gridDim.x) * W) {
     if (threadIdx.x == 0) {
-      const int64_t last = base + 7 < n_rows ? base + 7 : n_rows - 1;
+      const int64_t last = base + W - 1 < n_rows ? base + W - 1 : n_rows - 1;
       for (int64_t slab = base >> 5; slab <= (last >> 5); ++slab) {
         unsigned ns = 128;
         uint32_t spins = 0;
@@ -320,6 +322,14 @@ rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_r
         const float4 g = __ldg(reinterpret_cast<const float4*>(w) + lane + 32 * i);
         orow[lane + 32 * i] = make_uint2(pack_bf16x2(v[i].x * inv * g.x, v[i].y * inv * g.y),
                                          pack_bf16x2(v[i].z * inv * g.z, v[i].w * inv * g.w));
+      }
+    }
+    if (ready_ctr) {
+      __threadfence();  // this thread's row stores, visible at gpu scope before the publication
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int64_t rows = n_rows - base < W ? n_rows - base : W;
+        atomicAdd(ready_ctr + (base >> 5), static_cast<uint32_t>(rows));
       }
     }
   }
@@ -486,9 +496,22 @@ extern "C" int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* ro
   return RDX_OK;
 }
 
+namespace rdx {
+namespace {
+template <int V, int W>
+cudaError_t launch_norm_after(cudaLaunchConfig_t& cfg, const float* x, int64_t ld_x, int64_t n_rows, const float* w,
+                              float eps, __nv_bfloat16* o, int64_t ld_out, const uint32_t* done_ctr, uint32_t target,
+                              uint32_t* ready_ctr) {
+  cfg.blockDim = dim3(W * 32);
+  return cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<V, W>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr,
+                            target, ready_ctr);
+}
+}  // namespace
+}  // namespace rdx
+
 extern "C" int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_rows, int64_t d, const float* w,
                                       float eps, void* out_bf16, int64_t ld_out, const uint32_t* done_ctr,
-                                      uint32_t target, void* stream) {
+                                      uint32_t target, uint32_t* ready_ctr, void* stream) {
   using namespace rdx;
   if (n_rows < 0 || d <= 0 || (d % 8) != 0 || (ld_x % 4) != 0 || (ld_out % 8) != 0) return RDX_ERR_SHAPE_MISMATCH;
   if (n_rows == 0) return RDX_OK;
@@ -496,8 +519,15 @@ extern "C" int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_ro
   if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) != 0) return RDX_ERR_UNSUPPORTED;
   __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out_bf16);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid_for_rows(n_rows, 8)));
-  cfg.blockDim = dim3(256);
+  // chained: one block per SM, 2-8 warps so its registers fit beside a GEMM CTA (168 x 320);
+  // plain: 8 warps, one block per 8 rows (capped)
+  static const int chain_grid = [] {  // RDX_NORM_CHAIN_GRID=1: the one-block-per-SM chained grid
+    const char* v = std::getenv("RDX_NORM_CHAIN_GRID");
+    return v && v[0] == '1' ? 1 : 0;
+  }();
+  const bool small = ready_ctr && chain_grid;
+  cfg.gridDim = dim3(static_cast<unsigned>(small ? (n_rows < num_sms() ? n_rows : num_sms())
+                                                 : grid_for_rows(n_rows, 8)));
   cfg.stream = as_stream(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // always: it overlaps the GEMM's tail
@@ -509,15 +539,18 @@ extern "C" int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_ro
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaError_t e;
+#define RDX_NA(V, WCH) (small ? launch_norm_after<V, WCH>(cfg, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target, ready_ctr) \
+                              : launch_norm_after<V, 8>(cfg, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target, ready_ctr))
   switch (d) {
-    case 256: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<2>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
-    case 512: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<4>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
-    case 1024: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<8>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
-    case 2048: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<16>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
-    case 2560: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<20>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
-    case 4096: e = cudaLaunchKernelEx(&cfg, rmsnorm_rows_after_kernel<32>, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target); break;
+    case 256: e = RDX_NA(2, 8); break;
+    case 512: e = RDX_NA(4, 8); break;
+    case 1024: e = RDX_NA(8, 4); break;
+    case 2048: e = RDX_NA(16, 4); break;
+    case 2560: e = RDX_NA(20, 2); break;
+    case 4096: e = RDX_NA(32, 1); break;  // 197 registers: one warp fits beside a 168 x 320 GEMM CTA
     default: return RDX_ERR_UNSUPPORTED;
   }
+#undef RDX_NA
   if (e != cudaSuccess) return set_cuda_error(e);
   RDX_LAUNCH_CHECK();
   return RDX_OK;

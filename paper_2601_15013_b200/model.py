@@ -365,6 +365,9 @@ class RadixQwen3:
         self.fused_norm = False if fused_norm is None else fused_norm
         # rmsnorm passes overlap the residual GEMM's last round (RDX_NORM_OVERLAP=0: stream-ordered)
         self.norm_overlap = os.environ.get("RDX_NORM_OVERLAP", "1") != "0"
+        # chained norm -> next GEMM on ready counters: correct (tests) but measured slower
+        # (C2 -6.7 %, C3 -4.5 %), so off unless RDX_NORM_CHAIN=1
+        self.norm_chain = os.environ.get("RDX_NORM_CHAIN", "0") == "1"
         if self.fused_norm:
             if config.hidden_size % 64:
                 raise ShapeMismatch("fused_norm needs hidden_size % 64 == 0")
@@ -382,7 +385,7 @@ class RadixQwen3:
         return fn()
 
     def _gemm(self, name, a, w, epi, out, *, m, stream, qkv=False, rope=None, layer=None, row_ss=None,
-              hb=None, ss_out=None, done=None):
+              hb=None, ss_out=None, done=None, ready=None):
         cfg = self.config
         args = _native.GemmArgs()
         args.a = a.data_ptr()
@@ -411,6 +414,9 @@ class RadixQwen3:
             args.eps = cfg.norm_eps
         if done is not None:  # per-32-row-slab completion counter for rdx_rmsnorm_rows_after
             args.done_ctr = done.data_ptr()
+        if ready is not None:  # chained A: (the norm's ready counters, use number)
+            args.a_ready = ready[0].data_ptr()
+            args.a_ready_use = ready[1]
         if row_ss is not None:  # RMSNorm of the A rows fused in (weight folded into w)
             args.row_ss = row_ss.data_ptr()
             args.ss_parts = row_ss.shape[1]
@@ -439,14 +445,15 @@ class RadixQwen3:
 
         self._op("rmsnorm", launch)
 
-    def _rmsnorm_after(self, x, w, out, ctr, target, stream=None):
-        """rmsnorm overlapping the tail of the residual GEMM that feeds it (slab counters)."""
+    def _rmsnorm_after(self, x, w, out, ctr, target, stream=None, ready=None):
+        """rmsnorm overlapping the tail of the residual GEMM that feeds it (slab counters);
+        with ``ready`` it publishes finished rows for a chained consumer GEMM."""
         lib = _native.lib()
 
         def launch():
             code = lib.rdx_rmsnorm_rows_after(x.data_ptr(), x.stride(0), x.shape[0], x.shape[1], w.data_ptr(),
                                               self.config.norm_eps, out.data_ptr(), out.stride(0), ctr.data_ptr(),
-                                              target, stream)
+                                              target, None if ready is None else ready.data_ptr(), stream)
             _native.check(code, "rdx_rmsnorm_rows_after")
 
         self._op("rmsnorm", launch)
@@ -728,21 +735,30 @@ class RadixQwen3:
         # ln2 / next ln1 start on the row blocks the residual GEMM has finished (its last
         # round leaves SMs idle): 32-row slab counters, one target step of d per use
         overlap = self.norm_overlap and not fused and d in (256, 512, 1024, 2048, 2560, 4096)
-        ctr = torch.zeros(-(-m // 32), dtype=torch.int32, device=dev) if overlap else None
+        # chained (RDX_NORM_CHAIN=1): that norm also publishes finished rows and the next GEMM
+        # (gate_up / the next layer's QKV) starts on them as its programmatic dependent
+        chain = overlap and self.norm_chain
+        slabs = -(-m // 32)
+        ctrs = torch.zeros(2 * slabs if chain else slabs, dtype=torch.int32, device=dev) if overlap else None
+        ctr = ctrs[:slabs] if overlap else None
+        rdy = ctrs[slabs:] if chain else None
         uses = 0
 
         def norm_after(wt):
             nonlocal uses
             if overlap:
                 uses += 1
-                self._rmsnorm_after(h, wt, hn, ctr, uses * d, stream=st)
+                self._rmsnorm_after(h, wt, hn, ctr, uses * d, stream=st, ready=rdy)
             else:
                 self._rmsnorm(h, wt, hn, stream=st)
+
+        def ready_arg():  # the consumer of the norm just launched (None before the first one)
+            return (rdy, uses) if chain and uses > 0 else None
 
         for i in range(cfg.num_layers):
             pre = f"layers.{i}."
             self._gemm("qkv", hn, T[pre + "w_qkv" + sfx], _native.EPI_QKV, qkv, m=m, stream=st, qkv=True,
-                       rope=rope, layer=pre, row_ss=ss)
+                       rope=rope, layer=pre, row_ss=ss, ready=ready_arg())
             if mode == "plain":
                 a = self._attn(qkv, None, cu32, cu32, b, max_k, max_k, attn_out, att_flops, st)
             elif mode == "suffix":
@@ -757,7 +773,8 @@ class RadixQwen3:
                        ss_out=ss, done=ctr)
             if not fused:
                 norm_after(T[pre + "ln2"])
-            self._gemm("gate_up", hn, T[pre + "w_gu" + sfx], _native.EPI_SWIGLU, act, m=m, stream=st, row_ss=ss)
+            self._gemm("gate_up", hn, T[pre + "w_gu" + sfx], _native.EPI_SWIGLU, act, m=m, stream=st, row_ss=ss,
+                       ready=ready_arg())
             last = i + 1 == cfg.num_layers
             self._gemm("down", act, T[pre + "w_down"], resid_epi, h, m=m, stream=st, hb=hn if fused else None,
                        ss_out=ss, done=None if last else ctr)

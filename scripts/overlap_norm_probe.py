@@ -50,7 +50,7 @@ for K in (2048, 3072):
     def rms_after():
         use[0] += 1
         _native.check(lib.rdx_rmsnorm_rows_after(h.data_ptr(), d, M, d, ln.data_ptr(), 1e-6, hn.data_ptr(), d,
-                                                 ctr.data_ptr(), use[0] * d, st), "ra")
+                                                 ctr.data_ptr(), use[0] * d, None, st), "ra")
 
     r = {
         "gemm": t(lambda: gemm(False)),
@@ -83,7 +83,7 @@ for K in (2048,):
             _native.check(lib.rdx_gemm(args, s_), "gemm")
             if overlap:
                 _native.check(lib.rdx_rmsnorm_rows_after(h.data_ptr(), d, M, d, ln.data_ptr(), 1e-6, hn.data_ptr(), d,
-                                                         ctr.data_ptr(), u * d, s_), "ra")
+                                                         ctr.data_ptr(), u * d, None, s_), "ra")
             else:
                 _native.check(lib.rdx_rmsnorm_rows(h.data_ptr(), d, None, M, d, ln.data_ptr(), 1e-6, hn.data_ptr(), d,
                                                    s_), "r")

@@ -32,7 +32,7 @@ def test_library_exports_every_symbol(native_lib):
 
 
 def test_status_names(native_lib):
-    assert native_lib.rdx_version() == 200
+    assert native_lib.rdx_version() == 300
     assert native_lib.rdx_status_name(0) == b"RDX_OK"
     assert native_lib.rdx_status_name(7) == b"IndexOutOfRange"
     assert native_lib.rdx_status_name(2) == b"NonMonotoneOffsets"

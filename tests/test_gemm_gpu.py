@@ -260,11 +260,11 @@ def test_gemm_error_codes():
     o = torch.empty(64, 384, dtype=torch.bfloat16, device="cuda")
     ctr = torch.zeros(2, dtype=torch.int32, device="cuda")
     assert lib.rdx_rmsnorm_rows_after(x.data_ptr(), 384, 64, 384, wn.data_ptr(), 1e-6, o.data_ptr(), 384,
-                                      ctr.data_ptr(), 384, st) == 13  # RDX_ERR_UNSUPPORTED
+                                      ctr.data_ptr(), 384, None, st) == 13  # RDX_ERR_UNSUPPORTED
     assert lib.rdx_rmsnorm_rows_after(x.data_ptr(), 384, 64, 384, wn.data_ptr(), 1e-6, o.data_ptr(), 384,
-                                      None, 384, st) == 12  # RDX_ERR_INVALID_ARGUMENT
+                                      None, 384, None, st) == 12  # RDX_ERR_INVALID_ARGUMENT
     assert lib.rdx_rmsnorm_rows_after(x.data_ptr(), 384, 0, 384, wn.data_ptr(), 1e-6, o.data_ptr(), 384,
-                                      None, 0, st) == 0  # no rows: nothing to do
+                                      None, 0, None, st) == 0  # no rows: nothing to do
     aq = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
     wq = torch.zeros(6 * 32, 64, dtype=torch.bfloat16, device="cuda")
     oq = torch.zeros(8, 6 * 32, dtype=torch.bfloat16, device="cuda")
@@ -304,7 +304,7 @@ def test_rmsnorm_after_timeout_reports_status():
     o = torch.empty(32, 256, dtype=torch.bfloat16, device="cuda")
     ctr = torch.zeros(1, dtype=torch.int32, device="cuda")  # never incremented
     _native.check(lib.rdx_rmsnorm_rows_after(x.data_ptr(), 256, 32, 256, wn.data_ptr(), 1e-6, o.data_ptr(), 256,
-                                             ctr.data_ptr(), 256, st), "rmsnorm_after")
+                                             ctr.data_ptr(), 256, None, st), "rmsnorm_after")
     with pytest.raises(NativeLibraryError):
         _native.check_device_status()
     assert lib.rdx_device_status(st) == 0  # cleared by the read
@@ -525,7 +525,7 @@ def test_resid_done_counter_and_rmsnorm_after(m, d, k):
         args.done_ctr = ctr.data_ptr()
         _native.check(lib.rdx_gemm(args, st), "gemm")
         _native.check(lib.rdx_rmsnorm_rows_after(h.data_ptr(), d, m, d, ln.data_ptr(), 1e-6, out.data_ptr(), d,
-                                                 ctr.data_ptr(), use * d, st), "rms_after")
+                                                 ctr.data_ptr(), use * d, None, st), "rms_after")
         if use == 1:
             torch.cuda.synchronize()
             assert torch.equal(h, h_ref)

@@ -182,16 +182,47 @@ def test_norm_overlap_bit_identical():
     plan = build_plan_device(db.tok, db.pos, db.cu)
     outs = {}
     for graphs in (False, True):
-        for overlap in (True, False):
+        for overlap, chain in ((True, True), (True, False), (False, False)):
             m = RadixQwen3(cfg, w, use_graphs=graphs)
-            m.norm_overlap = overlap
+            m.norm_overlap, m.norm_chain = overlap, chain
             for p in (plan, None):
                 o = m.prefill(db, p, logits="last")
                 o = m.prefill(db, p, logits="last").clone()  # second call: graph replay
                 torch.cuda.synchronize()
-                outs[(graphs, overlap, p is None)] = o
+                outs[(graphs, overlap, chain, p is None)] = o
     for key, o in outs.items():
-        assert torch.equal(o, outs[(False, False, key[2])]), key
+        assert torch.equal(o, outs[(False, False, False, key[3])]), key
+    from paper_2601_15013_b200 import _native
+
+    _native.check_device_status()  # no slab wait timed out on the way
+
+
+@pytest.mark.parametrize("preset,layers", [("qwen3-0.6b", 4), ("qwen3-4b", 2), ("qwen3-8b", 2)])
+def test_norm_chain_bit_identical_widths(preset, layers):
+    """The chained norm -> GEMM pipeline (the GEMM streams rows the norm publishes on
+    ready counters) at every model width (d = 1024 / 2560 / 4096: 4, 2 and 1 warps per
+    norm block beside the GEMM CTA) equals the stream-ordered passes bit for bit."""
+    import torch
+
+    from paper_2601_15013_b200 import DeviceWeights, RadixQwen3, _native
+    from paper_2601_15013_b200.model import QWEN3_PRESETS, DeviceBatch, Qwen3Config
+    from paper_2601_15013_b200.plan import build_plan_device
+    from paper_2601_15013_b200.workloads import RerankSpec, msmarco_rerank_batch
+
+    base = QWEN3_PRESETS[preset]
+    cfg = Qwen3Config(layers, base.hidden_size, base.intermediate_size, base.num_heads, base.num_kv_heads,
+                      base.head_dim, base.vocab_size, base.rope_theta, base.norm_eps)
+    w = DeviceWeights.random(cfg, seed=5)
+    db = DeviceBatch.from_batch(msmarco_rerank_batch(RerankSpec(queries=2, passages_per_query=32)))
+    plan = build_plan_device(db.tok, db.pos, db.cu)
+    outs = []
+    for overlap, chain in ((True, True), (False, False)):
+        m = RadixQwen3(cfg, w, use_graphs=False)
+        m.norm_overlap, m.norm_chain = overlap, chain
+        outs.append(m.prefill(db, plan, logits="last").clone())
+    torch.cuda.synchronize()
+    _native.check_device_status()
+    assert torch.equal(outs[0], outs[1])
 
 
 def test_graph_buckets_distinct_batches():
