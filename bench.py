@@ -627,6 +627,25 @@ def run_micro(args):
                          "scatter_dram_gbs": round(uniq_s / (ms_s * 1e-3) / 1e9, 1),
                          "gather_us": round(ms_g * 1e3, 1), "gather_gbs": round(alg_g / (ms_g * 1e-3) / 1e9, 1)})
             del x, full, comp
+    # the reference's own CPU row ops beside them (radix_compact.ops, numpy; f32 rows since numpy
+    # has no bf16), 1 thread and all host threads, _median_time methodology (bench.py:243-250)
+    cpu_rows = []
+    if ref is not None:
+        import radix_compact.ops as rops
+
+        for rec in plans:
+            if rec["case"] != "ratio0.50" or rec["N"] != (1 << 17):
+                continue
+            pb = prefix_ratio_batch(rec["N"], 0.5)
+            hplan = ref.trie.build_plan(ref.RaggedBatch(pb.token_ids, pb.position_ids, pb.cu_seqlens))
+            for d in (1024, 4096):
+                xc = np.random.default_rng(0).standard_normal((hplan.n_compact, d), dtype=np.float32)
+                for th in (1, os.cpu_count() or 1):
+                    t = _median_time(lambda: rops.gather_rows(xc, hplan.scatter_indices, num_threads=th), reps=3)
+                    nb = rec["N"] * (2 * 4 * d + 4)
+                    cpu_rows.append({"op": "scatter (gather_rows with the scatter map, N' -> N)", "N": rec["N"],
+                                     "d": d, "dtype": "f32", "threads": th, "ms": round(t * 1e3, 2),
+                                     "gbs": round(nb / t / 1e9, 2)})
     gather = gather_microbench(hbm)
     best = max(r["gather_gbs"] for r in rows) if rows else gather["gbs"]
     line = {"metric": "C5 index build + row gather/scatter microbenchmark", "value": round(best, 1),
@@ -636,6 +655,7 @@ def run_micro(args):
             "hbm_peak_gbs": hbm, "peak_source": peaks_src,
             "bytes_convention": "gather/scatter: 2*rows_out*row_bytes + 4*rows_out; index: 12N + 8N' + 8(B+1)",
             "index_build": plans, "row_ops": rows, "gather_table6": gather, "host": host_info(),
+            "cpu_row_ops_reference": cpu_rows,
             "cpu_baseline": {"kind": "reference" if ref is not None else "port", "cores": 1,
                              "sample": ("radix_compact.trie.build_plan (numba, 1 thread) and the C restatement"
                                         if ref is not None else "oracle/trie_oracle.c") + ", full batch"}}
