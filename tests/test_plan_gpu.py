@@ -219,3 +219,42 @@ def test_validation_codes_both_planners(smem):
         assert dp.n_compact == 3000
     finally:
         lib.rdx_plan_debug_smem(prev)
+
+
+def test_planner_fuzz_both_kernels(oracle):
+    """Seeded random batches across the cluster-planner's whole range (1 CTA .. 16 CTAs, chunks
+    ending mid-sequence, sequence starts on chunk boundaries, duplicated and empty-suffix
+    sequences, tiny alphabets = deep shared structure) and beyond it (grid planner): both
+    kernels bit-exact vs the oracle."""
+    from paper_2601_15013_b200 import RaggedBatch, _native
+
+    lib = _native.lib()
+    rng = np.random.default_rng(2026)
+    for trial in range(40):
+        n_target = int(rng.choice([1, 7, 300, 1024, 1025, 4096, 9000, 16383, 33000, 65536, 70000]))
+        nseq = int(rng.integers(1, max(2, min(n_target, 3000))))
+        lens = rng.multinomial(n_target - nseq, np.ones(nseq) / nseq) + 1 if n_target >= nseq else np.ones(nseq, int)
+        cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        n = int(cu[-1])
+        alphabet = int(rng.choice([2, 3, 50, 151936]))
+        tok = rng.integers(0, alphabet, size=n).astype(np.uint32)
+        # copy whole earlier sequences / prefixes into later ones (shared trunks, exact duplicates)
+        for s in range(1, nseq):
+            if rng.random() < 0.5:
+                src = int(rng.integers(0, s))
+                k = int(min(lens[s], lens[src], rng.integers(0, lens[src] + 1)))
+                tok[cu[s]:cu[s] + k] = tok[cu[src]:cu[src] + k]
+        pos = (np.arange(n) - np.repeat(cu[:-1], lens)).astype(np.uint32)
+        b = RaggedBatch(tok, pos, cu)
+        g, s_, cp, m = oracle.build_plan_oracle(tok, pos, cu)
+        for on in (1, 0):
+            prev = lib.rdx_plan_debug_smem(on)
+            try:
+                res = _device_plan_arrays(b)
+            finally:
+                lib.rdx_plan_debug_smem(prev)
+            assert res[0] == m, (trial, on, n, nseq)
+            np.testing.assert_array_equal(res[1], g)
+            np.testing.assert_array_equal(res[2], s_)
+            np.testing.assert_array_equal(res[3], cp)
+            assert int(np.diff(res[4]).max()) == int(np.max(np.diff(cu) - res[5]))
