@@ -304,9 +304,11 @@ def ncu_traffic(path):
 
 
 def roofline(by, steps, ms_per_step, peaks, peaks_src, config_name):
-    """Dominant kernel = the gate|up SwiGLU GEMM (largest single GEMM, the top
-    launch of the step in every ncu launch list)."""
-    name = "gemm.gate_up"
+    """Dominant kernel = the MLP launch: gate|up SwiGLU GEMM and down GEMM in one
+    persistent kernel (rdx_gemm_pair), else the gate|up GEMM alone (the top launch of
+    the step in every ncu launch list)."""
+    pair = "gemm.mlp" in by
+    name = "gemm.mlp" if pair else "gemm.gate_up"
     f, ms, n = by[name]
     achieved = f / (ms * 1e-3) / 1e12
     long_step = ms_per_step >= 50.0
@@ -315,16 +317,19 @@ def roofline(by, steps, ms_per_step, peaks, peaks_src, config_name):
     gf, gms, gn = sum(x[0] for x in gemm), sum(x[1] for x in gemm), sum(x[2] for x in gemm)
     roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "gemm_kernel (tcgen05 2-CTA, EPI_SWIGLU): gate|up projection + SiLU*mul",
+            "kernel": ("gemm_kernel<256, SWIGLU, 2, RESID_F32> (tcgen05 2-CTA, rdx_gemm_pair): gate|up + SiLU*mul, "
+                       "then down + residual reduce-add in the same launch" if pair else
+                       "gemm_kernel (tcgen05 2-CTA, EPI_SWIGLU): gate|up projection + SiLU*mul"),
             "flops_per_launch": round(f / n), "avg_launch_us": round(ms * 1e3 / n, 2),
             "peak_kind": ("sustained (step >= 50 ms: clocks settle under the power cap)" if long_step
                           else "burst (short step, kernels run at boost clocks)") + f"; {peaks_src}",
             "all_gemms": {"achieved": round(gf / (gms * 1e-3) / 1e12, 1), "frac": round(gf / (gms * 1e-3) / 1e12 / peak, 4),
                           "launches_per_step": gn // steps, "share_of_step": round(gms / steps / ms_per_step, 3)}}
-    for rnd in ("r2", "r1"):
-        path = os.path.join(ROOT, "profiles", f"{rnd}_ncu_gemm_gateup_{config_name}.txt")
+    stems = ["ncu_gemm_mlp"] if pair else ["ncu_gemm_gateup", "ncu_gateup"]
+    for path in [os.path.join(ROOT, "profiles", f"{rnd}_{stem}_{config_name}.txt") for rnd in ("r2", "r1")
+                 for stem in stems]:
         tr = ncu_traffic(path)
-        if tr is not None:  # DRAM bytes of one gate_up launch from the committed ncu --set full capture
+        if tr is not None:  # DRAM bytes of one launch from the committed ncu --set full capture
             roof["traffic"] = tr[0]
             roof["traffic_source"] = f"{os.path.relpath(path, ROOT)} (dram read+write, 1 launch)"
             roof["algorithmic_bytes"] = None

@@ -283,6 +283,21 @@ typedef struct rdx_gemm_args {
 
 int rdx_gemm(const rdx_gemm_args* args, void* stream);
 
+/* The MLP's two GEMMs in ONE persistent launch: first = gate|up (RDX_EPI_SWIGLU,
+ * output act), second = down (RDX_EPI_RESID_F32 with second->a == first->out,
+ * second->k == first->n / 2, same m).  Job 1's tiles follow job 0's in every CTA's
+ * static schedule; a down tile's TMA producer waits until every act column of its
+ * rows is written (dep_ctr: ceil(m / 32) zeroed u32 counters, one per 32-row slab,
+ * release/acquire), so the down GEMM starts while the gate|up GEMM drains and the
+ * second launch's prologue disappears.  Same bits as the two rdx_gemm calls; falls
+ * back to them when the two GEMMs want different tile shapes or M spans >= 64 pair
+ * row blocks (large M: measured neutral). */
+int rdx_gemm_pair(const rdx_gemm_args* first, const rdx_gemm_args* second, uint32_t* dep_ctr, void* stream);
+
+/* Debug: rdx_gemm_pair as one launch (1) or two stream-ordered launches (0) for
+ * A/B runs; returns the previous setting. */
+int rdx_gemm_debug_pair(int on);
+
 /* Debug: the GEMM splits the tiles of a last partial round into 2 or 4
  * narrower tiles (same per-element K reduction, same bits); 0 turns that off
  * for A/B runs, 1 back on.  Returns the previous setting. */

@@ -41,6 +41,8 @@ EXPORTS = (
     "rdx_rope_table",
     "rdx_rope_table_blocked",
     "rdx_gemm",
+    "rdx_gemm_pair",
+    "rdx_gemm_debug_pair",
     "rdx_gemm_debug_tail_split",
     "rdx_gemm_debug_colpart",
     "rdx_gemm_debug_stats",
@@ -139,8 +141,10 @@ _SIGNATURES = {
     "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_rope_table_blocked": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_gemm": (ctypes.c_int, [ctypes.POINTER(GemmArgs), _vp]),
+    "rdx_gemm_pair": (ctypes.c_int, [ctypes.POINTER(GemmArgs), ctypes.POINTER(GemmArgs), _vp, _vp]),
     "rdx_gemm_debug_tail_split": (ctypes.c_int, [ctypes.c_int]),
     "rdx_gemm_debug_colpart": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_gemm_debug_pair": (ctypes.c_int, [ctypes.c_int]),
     "rdx_plan_debug_smem": (ctypes.c_int, [ctypes.c_int]),
     "rdx_attention_debug_bk64": (ctypes.c_int, [ctypes.c_int]),
     "rdx_plan_debug_trace": (ctypes.c_int, [_vp]),

@@ -736,6 +736,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
             umma_ss_elect(sacc, qd + (((kk >> 2) * (BQ * 128) + (kk & 3) * 32) >> 4),
                           kd + (((kk >> 2) * (BKT * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
           commit_elect(&s_full[2 * h + b]);
+          if (lane == 0) RDX_EV(1, 1, h * 16 + (x.j & 15));  // MMA: S_h(j) issued
           if (RDX_STATS_ON) st_iss += clock64() - st_i0;
           ++sc[h];
           if (x.j == nkt - 1) {
@@ -748,6 +749,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           if (x.j >= nkt) return;
           const int b = pc[h] & 1;
           RDX_TWAIT(&p_full[2 * h + b], (pc[h] >> 1) & 1, st_p);
+          if (lane == 0) RDX_EV(1, 2, h * 16 + (x.j & 15));  // MMA: P_h(j) seen
           ++pc[h];
           if (x.j == 0 && oc[h] > 0) RDX_TWAIT(&o_free[h], (oc[h] - 1) & 1, st_o);
           if (!a.use_tma) fence_proxy_async_smem();
@@ -788,9 +790,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         while (cur.u < a.n_units) {
           const bool nx = n2.u < a.n_units;
           wait_tile2(2 * gt + 1);  // V(cur)
+          if (lane == 0) RDX_EV(1, 4, cur.j & 15);  // MMA: V(cur) resident
           issue_PV2(0, cur, gt);
           if (nx) {
             wait_tile2(2 * (gt + 2));  // K(cur + 2)
+            if (lane == 0) RDX_EV(1, 3, n2.j & 15);  // MMA: K(cur + 2) resident
             issue_S2(0, n2, gt + 2);
           }
           issue_PV2(1, cur, gt);

@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -563,14 +564,107 @@ __device__ __forceinline__ void epilogue_tile(EpiWarp<NB>& e, uint32_t taddr, in
   }
 }
 
+// Tensor maps and scalar arguments of one GEMM ("job") of a launch.
+struct alignas(64) JobMaps {
+  CUtensorMap a, b, b2, b4, c, d;  // A, B (full / half or wide / quarter or narrow boxes), output, RESID_NORM bf16 out
+};
+struct JobArgs {
+  int64_t N, K, tail_start;
+  int split;
+  EpiParams ep;
+};
+// staging boxes per epilogue warp: four 2 KB bf16 boxes or two 4 KB fp32 boxes
+__host__ __device__ constexpr int nb_of(int epi) {
+  return (epi == RDX_EPI_STORE_F32 || epi == RDX_EPI_RESID_F32 || epi == RDX_EPI_RESID_NORM) ? 2 : 4;
+}
+
 // ------------------------------------------------------------------ the kernel
-template <int BN, int EPI, int CG>
+// Per-warp epilogue state carried across tiles (and across the two jobs of a pair).
+struct EpiCtx {
+  uint32_t tmem_base, tempty_leader0;
+  uint64_t *tfull, *tempty;
+  const float* s_norm;
+  uint32_t rank;
+  int q, ch, lane;
+  int acc;
+  uint32_t acc_phase;
+  long long st_w, st_b;
+  long long n_t;
+};
+
+// One output tile of one job in this epilogue warp: wait for the accumulator, the fused
+// epilogue (EP), release the accumulator, publish slab counters (done_ctr of a residual
+// GEMM; `dep` = job 0 of a pair: the output columns job 1 waits for).
+template <int BN, int CG, int EP, int NB>
+__device__ __forceinline__ void epi_job_tile(EpiWarp<NB>& e, EpiCtx& x, const JobArgs& J, const JobMaps& MP,
+                                             uint32_t* dep, int64_t M, int64_t m_blk, int64_t n0, int width) {
+  const EpiParams& ej = J.ep;
+  const int64_t N = J.N;
+  const int lane = x.lane, ch = x.ch;
+  e.row0 = static_cast<int32_t>(m_blk * (BM * CG) + x.rank * BM + x.q * 32);
+  // row scale of the fused RMSNorm: its loads overlap the wait for the accumulator
+  const int64_t gm = e.row0 + lane;
+  const float rs = ej.row_ss ? row_rstd(ej, gm < M ? gm : (M > 0 ? M - 1 : 0)) : 1.f;
+  if constexpr (EP == RDX_EPI_RESID_NORM) resid_norm_prefetch(e, &MP.c, n0 + ch * (width / 2), N);
+  GST_WAIT(x.st_w, mbar_wait(&x.tfull[x.acc], x.acc_phase));
+  const long long st_tb = clock64();
+  tc_fence_after();
+  const uint32_t taddr = x.tmem_base + x.acc * BN + (static_cast<uint32_t>(x.q * 32) << 16);
+  // this warp's columns: halves of the tile, or in a column partition (widths in
+  // 32-column boxes, possibly odd) the first ceil(boxes/2) boxes and the rest
+  int c_lo = ch * (width / 2), hw = width / 2;
+  if (ej.cp_ncol > 0) {
+    const int w0 = ((width / 32 + 1) / 2) * 32;
+    c_lo = ch ? w0 : 0;
+    hw = ch ? width - w0 : w0;
+  }
+  epilogue_tile<BN, EP, NB>(e, taddr, ch, c_lo, hw, gm, M, n0, N, ej, x.s_norm, x.s_norm + 128, &MP.c, &MP.d, rs);
+  tc_fence_before();
+  __syncwarp();
+  if (lane == 0) {
+    if constexpr (CG == 2) mbar_arrive_cluster(x.tempty_leader0 + x.acc * 8);
+    else mbar_arrive(&x.tempty[x.acc]);
+  }
+  x.acc ^= 1;
+  if (x.acc == 0) x.acc_phase ^= 1;
+  if constexpr (EP == RDX_EPI_RESID_F32) {
+    if (ej.done_ctr && lane == 0 && e.row0 < M) {  // slabs past M do not exist
+      // this warp's reduce-adds are complete and visible: publish its columns of the slab
+      const int64_t c0 = n0 + c_lo;
+      const int64_t cols = N - c0 < hw ? (N - c0 > 0 ? N - c0 : 0) : hw;
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      atomicAdd(ej.done_ctr + (e.row0 >> 5), static_cast<uint32_t>(cols));
+    }
+  }
+  if (dep && lane == 0 && e.row0 < M) {
+    // job 1 of the pair reads these rows: publish this warp's output columns once its stores landed
+    const int64_t nout = EP == RDX_EPI_SWIGLU ? N / 2 : N;
+    const int64_t c0 = EP == RDX_EPI_SWIGLU ? (n0 + c_lo) / 2 : n0 + c_lo;
+    const int64_t w_out = EP == RDX_EPI_SWIGLU ? hw / 2 : hw;
+    const int64_t cols = nout - c0 < w_out ? (nout - c0 > 0 ? nout - c0 : 0) : w_out;
+    bulk_wait_all();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence();
+    atomicAdd(dep + (e.row0 >> 5), static_cast<uint32_t>(cols));
+  }
+  x.st_b += clock64() - st_tb;
+  ++x.n_t;
+}
+
+// One launch runs one GEMM (EPI2 < 0) or two dependent GEMMs sharing M, BN and CG
+// (EPI2 >= 0, rdx_gemm_pair: the MLP's gate|up -> down).  Job 1's tiles follow job 0's
+// in every CTA's static schedule; a job-1 tile's producer waits until job 0 has written
+// all dep_cols output columns of its A rows (per-32-row-slab counters in `dep`), so job
+// 1's first tiles overlap job 0's last epilogues and one launch prologue is saved.
+template <int BN, int EPI, int CG, int EPI2>
 __global__ void __launch_bounds__(kThreads, 1)
-gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-            const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmB4,
-            const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int64_t M, int64_t N,
-            int64_t K, int64_t tail_start, int split, EpiParams ep) {
+gemm_kernel(const __grid_constant__ JobMaps mp0, const __grid_constant__ JobMaps mp1, int64_t M,
+            const __grid_constant__ JobArgs j0, const __grid_constant__ JobArgs j1, uint32_t* dep, uint32_t dep_cols) {
   using C = Cfg<BN, CG, EPI>;
+  static_assert(EPI2 < 0 || Cfg<BN, CG, EPI2 < 0 ? EPI : EPI2>::SMEM == C::SMEM, "paired jobs share one smem layout");
+  const EpiParams& ep = j0.ep;  // job 0's epilogue parameters (prologue uses)
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -594,46 +688,68 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   const int64_t unit = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;
   const int64_t n_units = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
   const int64_t m_tiles = (M + BM * CG - 1) / (BM * CG);
-  const int64_t n_tiles = ep.cp_ncol > 0 ? ep.cp_ncol : (N + BN - 1) / BN;
-  const int64_t full_tiles = m_tiles * n_tiles;
+  auto n_tiles_of = [&](const JobArgs& J) -> int64_t {
+    return J.ep.cp_ncol > 0 ? J.ep.cp_ncol : (J.N + BN - 1) / BN;
+  };
   // Tail split: the tiles of the last partial round (from tail_start on) run as
   // `split` narrower tiles each (width BN/split), so r leftover tiles occupy
   // ceil(split*r/units)/split of a round instead of a whole one.  No split-K:
   // every output element is still one CTA's full K reduction -> same bits.
-  const int64_t num_tiles = tail_start + split * (full_tiles - tail_start);
-  auto decode = [&](int64_t t, int64_t& m_blk, int64_t& n0, int& width) {
+  auto num_tiles_of = [&](const JobArgs& J) -> int64_t {
+    return J.tail_start + J.split * (m_tiles * n_tiles_of(J) - J.tail_start);
+  };
+  const int64_t nt0 = num_tiles_of(j0);
+  const int64_t num_tiles = nt0 + (EPI2 >= 0 ? num_tiles_of(j1) : 0);
+  // job of a schedule index and the tile index inside that job
+  auto job_of = [&](int64_t tile, int64_t& t) -> int {
+    if (EPI2 >= 0 && tile >= nt0) {
+      t = tile - nt0;
+      return 1;
+    }
+    t = tile;
+    return 0;
+  };
+  auto decode = [&](const JobArgs& J, int64_t t, int64_t& m_blk, int64_t& n0, int& width) {
+    const EpiParams& ej = J.ep;
+    const int64_t n_tiles = n_tiles_of(J);
     int64_t f = t;
     int part = 0;
     width = BN;
-    if (t >= tail_start) {
-      f = tail_start + (t - tail_start) / split;
-      part = static_cast<int>((t - tail_start) % split);
-      width = BN / split;
+    if (t >= J.tail_start) {
+      f = J.tail_start + (t - J.tail_start) / J.split;
+      part = static_cast<int>((t - J.tail_start) % J.split);
+      width = BN / J.split;
     }
     // grouped raster: the tiles running at once cover ~group_m row blocks x a few column
     // blocks, so both A rows and B columns are re-read from L2 rather than HBM
-    const int64_t gsz = static_cast<int64_t>(ep.group_m) * n_tiles;
+    const int64_t gsz = static_cast<int64_t>(ej.group_m) * n_tiles;
     const int64_t g = f / gsz, r = f - g * gsz;
-    const int64_t g_rows = m_tiles - g * ep.group_m < ep.group_m ? m_tiles - g * ep.group_m : ep.group_m;
-    m_blk = g * ep.group_m + r % g_rows;
+    const int64_t g_rows = m_tiles - g * ej.group_m < ej.group_m ? m_tiles - g * ej.group_m : ej.group_m;
+    m_blk = g * ej.group_m + r % g_rows;
     const int cblk = static_cast<int>(r / g_rows);
-    if (ep.cp_ncol > 0) {
-      const bool wide = (ep.cp_mask >> cblk) & 1u;
-      width = wide ? ep.cp_wide : ep.cp_narrow;
-      n0 = static_cast<int64_t>(cblk) * ep.cp_narrow +
-           static_cast<int64_t>(__popc(ep.cp_mask & ((1u << cblk) - 1u))) * (ep.cp_wide - ep.cp_narrow);
+    if (ej.cp_ncol > 0) {
+      const bool wide = (ej.cp_mask >> cblk) & 1u;
+      width = wide ? ej.cp_wide : ej.cp_narrow;
+      n0 = static_cast<int64_t>(cblk) * ej.cp_narrow +
+           static_cast<int64_t>(__popc(ej.cp_mask & ((1u << cblk) - 1u))) * (ej.cp_wide - ej.cp_narrow);
     } else {
       n0 = static_cast<int64_t>(cblk) * BN + part * width;
     }
   };
-  const int kblocks = static_cast<int>((K + BK - 1) / BK);
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    tma_prefetch_desc(&tmB2);
-    tma_prefetch_desc(&tmB4);
-    tma_prefetch_desc(&tmC);
+    tma_prefetch_desc(&mp0.a);
+    tma_prefetch_desc(&mp0.b);
+    tma_prefetch_desc(&mp0.b2);
+    tma_prefetch_desc(&mp0.b4);
+    tma_prefetch_desc(&mp0.c);
+    if constexpr (EPI2 >= 0) {
+      tma_prefetch_desc(&mp1.a);
+      tma_prefetch_desc(&mp1.b);
+      tma_prefetch_desc(&mp1.b2);
+      tma_prefetch_desc(&mp1.b4);
+      tma_prefetch_desc(&mp1.c);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -677,15 +793,43 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
-        int64_t m_blk, n0;
+        int64_t m_blk, n0, lt;
         int width;
-        decode(tile, m_blk, n0, width);
+        const int job = job_of(tile, lt);
+        const JobArgs& J = job ? j1 : j0;
+        const JobMaps& MP = job ? mp1 : mp0;
+        decode(J, lt, m_blk, n0, width);
+        const int kblocks = static_cast<int>((J.K + BK - 1) / BK);
         // B rows this CTA stages: width / CG (1, 1/2 or 1/4 of B_ROWS, or a column-partition width)
         const int b_rows = width / CG;
         const int32_t m0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM);
         const int32_t nb0 = static_cast<int32_t>(n0 + rank * b_rows);
         const uint32_t bytes = C::A_BYTES + static_cast<uint32_t>(b_rows) * (BK * 2);
-        if (ep.a_ready && m0 < M) {
+        if (job == 1 && m0 < M) {
+          // job 1's A rows are job 0's output: wait until every column of them is written
+#ifdef RDX_GEMM_STATS_BUILD
+          const long long dw0 = clock64();
+#endif
+          const int64_t r_hi = (m0 + BM < M ? m0 + BM : M) - 1;
+          for (int64_t slab = m0 >> 5; slab <= (r_hi >> 5); ++slab) {
+            unsigned ns = 32;
+            uint32_t spins = 0;
+            while (ld_acquire_u32(dep + slab) < dep_cols) {
+              __nanosleep(ns);
+              ns = ns < 512 ? 2 * ns : ns;
+              if (++spins > (1u << 24)) {  // ~8 s: job 0 never completed these rows
+                atomicCAS(&g_device_status, 0, static_cast<int>(RDX_ERR_DEVICE_TIMEOUT));
+                break;
+              }
+            }
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA-written rows -> TMA reads
+#ifdef RDX_GEMM_STATS_BUILD
+          atomicAdd(&g_gemm_stats[6], static_cast<unsigned long long>(clock64() - dw0));
+          atomicAdd(&g_gemm_stats[7], 1ull);
+#endif
+        }
+        if (job == 0 && ep.a_ready && m0 < M) {
           const int64_t r_hi = (m0 + BM < M ? m0 + BM : M) - 1;
           for (int64_t slab = m0 >> 5; slab <= (r_hi >> 5); ++slab) {
             const uint32_t rows = static_cast<uint32_t>(M - slab * 32 < 32 ? M - slab * 32 : 32);
@@ -706,11 +850,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         const CUtensorMap* mapb;
-        if (ep.cp_ncol > 0) {
-          mapb = width == ep.cp_wide ? &tmB2 : &tmB4;  // boxes of cp_wide / cp_narrow rows (host)
+        if (J.ep.cp_ncol > 0) {
+          mapb = width == J.ep.cp_wide ? &MP.b2 : &MP.b4;  // boxes of cp_wide / cp_narrow rows (host)
         } else {
           const int div = BN / width;  // 1, 2 or 4
-          mapb = div == 1 ? &tmB : (div == 2 ? &tmB2 : &tmB4);
+          mapb = div == 1 ? &MP.b : (div == 2 ? &MP.b2 : &MP.b4);
         }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -719,11 +863,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
           if constexpr (CG == 2) {
             const uint32_t bar = mapa_shared(smem_u32(&full[stage]), 0);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
-            tma_load_2d_cg2(&tmA, sa, bar, kb * BK, m0);
+            tma_load_2d_cg2(&MP.a, sa, bar, kb * BK, m0);
             tma_load_2d_cg2(mapb, sb, bar, kb * BK, nb0);
           } else {
             mbar_arrive_expect_tx(&full[stage], bytes);
-            tma_load_2d(&tmA, sa, &full[stage], kb * BK, m0);
+            tma_load_2d(&MP.a, sa, &full[stage], kb * BK, m0);
             tma_load_2d(mapb, sb, &full[stage], kb * BK, nb0);
           }
           if (++stage == STAGES) {
@@ -742,10 +886,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       long long st_te = 0, st_fu = 0;
       const long long st_t0 = clock64();
       for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
-        int64_t m_blk, n0;
+        int64_t m_blk, n0, lt;
         int width;
-        decode(tile, m_blk, n0, width);
-        const uint32_t idesc = ep.cp_ncol > 0 ? umma_idesc_bf16(BM * CG, width)
+        const int job = job_of(tile, lt);
+        const JobArgs& J = job ? j1 : j0;
+        decode(J, lt, m_blk, n0, width);
+        const int kblocks = static_cast<int>((J.K + BK - 1) / BK);
+        const uint32_t idesc = J.ep.cp_ncol > 0 ? umma_idesc_bf16(BM * CG, width)
                                : (width == BN ? C::IDESC : (width == BN / 2 ? C::IDESC_HALF : C::IDESC_QUARTER));
         GST_WAIT(st_te, mbar_wait(&tempty[acc], acc_phase ^ 1));
         tc_fence_after();
@@ -807,61 +954,41 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         named_bar_sync(1, 32 * kEpiWarps);
       }
     }
-    constexpr int NB = (EPI == RDX_EPI_STORE_F32 || EPI == RDX_EPI_RESID_F32 || EPI == RDX_EPI_RESID_NORM) ? 2 : 4;
-    EpiWarp<NB> e;
+    constexpr int E2 = EPI2 < 0 ? EPI : EPI2;
+    EpiWarp<nb_of(EPI)> e;
     e.base = epi_smem + ew * C::EPI_WARP_BYTES;
     e.lbar = eload + 2 * ew;
     e.lphase = 0;
     e.cur = 0;
     e.lane = lane;
     const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    long long st_w = 0, st_b = 0, n_t = 0;
-    for (int64_t tile = unit; tile < num_tiles; tile += n_units) {
+    EpiCtx x{tmem_base, tempty_leader0, tfull, tempty, s_norm, rank, q, ch, lane, 0, 0u, 0, 0};
+    // job 0's tiles, then (paired launch) job 1's: in every CTA's static schedule all job-0
+    // tiles come first, so two loops with concrete epilogue types (no job-generic code)
+    int64_t tile = unit;
+    for (; tile < nt0; tile += n_units) {
       int64_t m_blk, n0;
       int width;
-      decode(tile, m_blk, n0, width);
-      e.row0 = static_cast<int32_t>(m_blk * (BM * CG) + rank * BM + q * 32);
-      // row scale of the fused RMSNorm: its loads overlap the wait for the accumulator
-      const int64_t gm = e.row0 + lane;
-      const float rs = ep.row_ss ? row_rstd(ep, gm < M ? gm : (M > 0 ? M - 1 : 0)) : 1.f;
-      if constexpr (EPI == RDX_EPI_RESID_NORM) resid_norm_prefetch(e, &tmC, n0 + ch * (width / 2), N);
-      GST_WAIT(st_w, mbar_wait(&tfull[acc], acc_phase));
-      const long long st_tb = clock64();
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      // this warp's columns: halves of the tile, or in a column partition (widths in
-      // 32-column boxes, possibly odd) the first ceil(boxes/2) boxes and the rest
-      int c_lo = ch * (width / 2), hw = width / 2;
-      if (ep.cp_ncol > 0) {
-        const int w0 = ((width / 32 + 1) / 2) * 32;
-        c_lo = ch ? w0 : 0;
-        hw = ch ? width - w0 : w0;
-      }
-      epilogue_tile<BN, EPI, NB>(e, taddr, ch, c_lo, hw, gm, M, n0, N, ep, s_norm, s_norm + 128, &tmC, &tmD, rs);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
-        else mbar_arrive(&tempty[acc]);
-      }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
-      if constexpr (EPI == RDX_EPI_RESID_F32) {
-        if (ep.done_ctr && lane == 0 && e.row0 < M) {  // slabs past M do not exist
-          // this warp's reduce-adds are complete and visible: publish its columns of the slab
-          const int64_t c0 = n0 + c_lo;
-          const int64_t cols = N - c0 < hw ? (N - c0 > 0 ? N - c0 : 0) : hw;
-          bulk_wait_all();
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          __threadfence();
-          atomicAdd(ep.done_ctr + (e.row0 >> 5), static_cast<uint32_t>(cols));
-        }
-      }
-      st_b += clock64() - st_tb;
-      ++n_t;
+      decode(j0, tile, m_blk, n0, width);
+      epi_job_tile<BN, CG, EPI>(e, x, j0, mp0, EPI2 >= 0 ? dep : nullptr, M, m_blk, n0, width);
     }
+    if constexpr (EPI2 >= 0) {
+      if (lane == 0) bulk_wait_all();  // the staging ring changes box layout: drain job 0's stores
+      __syncwarp();
+      EpiWarp<nb_of(E2)> e2;  // job 1's staging ring (same smem, its own box layout)
+      e2.base = e.base;
+      e2.lbar = e.lbar;
+      e2.lphase = 0;
+      e2.cur = 0;
+      e2.lane = lane;
+      for (; tile < num_tiles; tile += n_units) {
+        int64_t m_blk, n0;
+        int width;
+        decode(j1, tile - nt0, m_blk, n0, width);
+        epi_job_tile<BN, CG, E2>(e2, x, j1, mp1, nullptr, M, m_blk, n0, width);
+      }
+    }
+    long long st_w = x.st_w, st_b = x.st_b, n_t = x.n_t;
     if (lane == 0) bulk_wait_all();
 #ifdef RDX_GEMM_STATS_BUILD
     if (lane == 0) {
@@ -974,6 +1101,14 @@ bool tail_split_enabled() {
 
 // RDX_GEMM_COLPART=0 (env) or rdx_gemm_debug_colpart(0) disables the column partition (A/B runs).
 int g_colpart = -1;
+int g_pair = -1;  // RDX_GEMM_PAIR / rdx_gemm_debug_pair
+bool pair_enabled() {
+  if (g_pair < 0) {
+    const char* e = getenv("RDX_GEMM_PAIR");
+    g_pair = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_pair == 1;
+}
 int g_last_cp_ncol = 0;  // debug query (rdx_gemm_debug_colpart(-1))
 bool colpart_enabled() {
   if (g_colpart < 0) {
@@ -998,16 +1133,18 @@ struct ColPart {
   uint32_t mask;
 };
 
-double sched_makespan(int64_t m_tiles, int ncol, const int* widths, int group_m, int64_t units) {
+double sched_makespan(int64_t m_tiles, int ncol, const int* widths, int group_m, int64_t units, int64_t offset = 0,
+                      double head = 0.0) {
   double load[1024];
   if (units > 1024) return 1e30;
-  for (int64_t u = 0; u < units; ++u) load[u] = 0.0;
+  // a preceding job of `offset` (mod units) leftover tiles of cost `head` on units [0, offset)
+  for (int64_t u = 0; u < units; ++u) load[u] = u < offset ? head : 0.0;
   const int64_t tiles = m_tiles * ncol;
   for (int64_t t = 0; t < tiles; ++t) {
     const int64_t gsz = static_cast<int64_t>(group_m) * ncol;
     const int64_t g = t / gsz, r = t - g * gsz;
     const int64_t g_rows = m_tiles - g * group_m < group_m ? m_tiles - g * group_m : group_m;
-    load[t % units] += widths[r / g_rows] + kTileFixed;
+    load[(t + offset) % units] += widths[r / g_rows] + kTileFixed;
   }
   double mx = 0.0;
   for (int64_t u = 0; u < units; ++u) mx = load[u] > mx ? load[u] : mx;
@@ -1015,7 +1152,7 @@ double sched_makespan(int64_t m_tiles, int ncol, const int* widths, int group_m,
 }
 
 bool choose_colpart(int64_t m_tiles, int64_t n, int bn, int group_m, int64_t units, int64_t tail_rem,
-                    int tail_split, ColPart* out) {
+                    int tail_split, ColPart* out, int64_t offset = 0, double head = 0.0) {
   if (n % 32 || n > 32 * 256) return false;
   const int64_t tiles = m_tiles * ((n + bn - 1) / bn);
   if (tiles > 6 * units || tiles <= units / 2) return false;
@@ -1025,15 +1162,15 @@ bool choose_colpart(int64_t m_tiles, int64_t n, int bn, int group_m, int64_t uni
   {
     int w[64];
     for (int c = 0; c < n_tiles; ++c) w[c] = bn;
-    base = sched_makespan(m_tiles, n_tiles, w, group_m, units);
-    if (tail_split > 1 && tail_rem > 0) {  // full rounds + the split tail's rounds
+    base = sched_makespan(m_tiles, n_tiles, w, group_m, units, offset, head);
+    if (tail_split > 1 && tail_rem > 0 && offset == 0) {  // full rounds + the split tail's rounds
       const double full = static_cast<double>(tiles / units) * (bn + kTileFixed);
       const int64_t narrow = tail_split * tail_rem;
       base = full + static_cast<double>((narrow + units - 1) / units) * (bn / tail_split + kTileFixed);
     }
   }
   struct Key {
-    int64_t m_tiles, n, units;
+    int64_t m_tiles, n, units, offset;
     int bn, group_m;
     ColPart cp;
     bool ok;
@@ -1044,7 +1181,8 @@ bool choose_colpart(int64_t m_tiles, int64_t n, int bn, int group_m, int64_t uni
   std::lock_guard<std::mutex> lock(mu);
   for (int i = 0; i < cache_n; ++i) {
     const Key& k = cache[i];
-    if (k.m_tiles == m_tiles && k.n == n && k.units == units && k.bn == bn && k.group_m == group_m) {
+    if (k.m_tiles == m_tiles && k.n == n && k.units == units && k.bn == bn && k.group_m == group_m &&
+        k.offset == offset) {
       *out = k.cp;
       return k.ok;
     }
@@ -1061,7 +1199,7 @@ bool choose_colpart(int64_t m_tiles, int64_t n, int bn, int group_m, int64_t uni
       if (__builtin_popcount(mask) != wide) continue;
       int w[32];
       for (int c = 0; c < ncol; ++c) w[c] = 32 * (nar + ((mask >> c) & 1u));
-      const double ms = sched_makespan(m_tiles, ncol, w, group_m, units);
+      const double ms = sched_makespan(m_tiles, ncol, w, group_m, units, offset, head);
       if (ms < best - 1e-9) {
         best = ms;
         bestcp = ColPart{ncol, 32 * (nar + 1), 32 * nar, mask};
@@ -1069,25 +1207,24 @@ bool choose_colpart(int64_t m_tiles, int64_t n, int bn, int group_m, int64_t uni
     }
   }
   const bool ok = bestcp.ncol > 0;
-  Key k{m_tiles, n, units, bn, group_m, bestcp, ok};
+  Key k{m_tiles, n, units, offset, bn, group_m, bestcp, ok};
   if (cache_n < 16) cache[cache_n++] = k;
   else cache[(m_tiles + n) & 15] = k;
   *out = bestcp;
   return ok;
 }
 
+// Tensor maps, epilogue parameters and static schedule (raster, tail split or column
+// partition) of one GEMM; *grid_units = CTA units (pairs when CG = 2) it wants.
+// pair_role: 0 = a stand-alone launch; 1 = job 0 of a pair (row-block-major raster so its
+// early row blocks finish first, no tail split: job 1's tiles fill its last round);
+// 2 = job 1 of a pair, whose tiles continue job 0's round-robin from unit `offset`.
 template <int BN, int EPI, int CG>
-int launch(const rdx_gemm_args& a, cudaStream_t stream) {
+int prepare_job(const rdx_gemm_args& a, JobMaps* maps, JobArgs* job, int64_t* grid_units, int pair_role = 0,
+                int64_t offset = 0) {
   using C = Cfg<BN, CG, EPI>;
-  auto kern = gemm_kernel<BN, EPI, CG>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    if (CG == 2) RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
-    attr_set = true;
-  }
-  CUtensorMap ma, mb, mb2, mb4, mc, md;
-  std::memset(&md, 0, sizeof(md));
+  std::memset(maps, 0, sizeof(*maps));
+  CUtensorMap &ma = maps->a, &mb = maps->b, &mb2 = maps->b2, &mb4 = maps->b4, &mc = maps->c, &md = maps->d;
   int st = make_map(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.a, a.k, a.m, a.lda, BK, BM);
   if (st) return st;
   st = make_map(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.b, a.k, a.n, a.ldb, BK, C::B_ROWS);
@@ -1111,7 +1248,8 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
     st = make_map(&md, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.out_bf16, a.n, a.m, a.ldo_bf16, 64, 32);
     if (st) return st;
   }
-  EpiParams ep;
+  EpiParams& ep = job->ep;
+  std::memset(&ep, 0, sizeof(ep));
   ep.qn = a.q_norm_w;
   ep.kn = a.k_norm_w;
   ep.rope = reinterpret_cast<const float2*>(a.rope_table);
@@ -1145,7 +1283,7 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
     // completion counter is attached).
     int gm = group_m_setting();
     if (gm <= 0) gm = m_tiles >= 64 ? (a.k >= 8192 ? group_m_bigk_setting() : 16)
-                                     : ((ep.done_ctr || ep.a_ready) ? 1 : static_cast<int>(m_tiles));
+                                     : ((ep.done_ctr || ep.a_ready || pair_role == 1) ? 1 : static_cast<int>(m_tiles));
     ep.group_m = static_cast<int>(gm < m_tiles ? gm : m_tiles);
   }
   const int64_t tiles = ((a.m + BM * CG - 1) / (BM * CG)) * ((a.n + BN - 1) / BN);
@@ -1157,7 +1295,7 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   // norm groups, 32-column boxes)
   const int64_t rem = tiles % units;
   int split = 1;
-  if (BN == 256 && rem > 0 && tail_split_enabled()) {
+  if (BN == 256 && rem > 0 && tail_split_enabled() && pair_role == 0) {
     double best = 1.0;
     for (int sf : {2}) {  // quarters measured slower: a narrow tile still streams the full A tile
       const int w = BN / sf;
@@ -1179,7 +1317,9 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   if constexpr (EPI == RDX_EPI_RESID_F32 || EPI == RDX_EPI_STORE_BF16 || EPI == RDX_EPI_STORE_F32) {
     ColPart cp;
     const int64_t m_tiles = (a.m + BM * CG - 1) / (BM * CG);
-    if (colpart_enabled() && choose_colpart(m_tiles, a.n, BN, ep.group_m, units_max, rem, split, &cp)) {
+    if (colpart_enabled() && choose_colpart(m_tiles, a.n, BN, ep.group_m, units_max, rem, split, &cp,
+                                            pair_role == 2 ? offset % units_max : 0,
+                                            pair_role == 2 ? static_cast<double>(BN + kTileFixed) : 0.0)) {
       ep.cp_ncol = cp.ncol;
       ep.cp_wide = cp.wide_w;
       ep.cp_narrow = cp.narrow_w;
@@ -1193,10 +1333,28 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
       if (st2) return st2;
     }
   }
-  const int64_t grid_units = ep.cp_ncol > 0 ? units_max : units;
+  *grid_units = ep.cp_ncol > 0 ? units_max : units;
   g_last_cp_ncol = ep.cp_ncol;
+  job->N = a.n;
+  job->K = a.k;
+  job->tail_start = tail_start;
+  job->split = split;
+  return RDX_OK;
+}
+
+template <int BN, int EPI, int CG, int EPI2>
+int launch_jobs(const JobMaps& mp0, const JobMaps& mp1, int64_t m, const JobArgs& j0, const JobArgs& j1,
+                uint32_t* dep, uint32_t dep_cols, int64_t grid_units, cudaStream_t stream) {
+  using C = Cfg<BN, CG, EPI>;
+  auto kern = gemm_kernel<BN, EPI, CG, EPI2>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    if (CG == 2) RDX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    attr_set = true;
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid_units * CG));
+  cfg.gridDim = dim3(static_cast<unsigned>(grid_units * CG));  // persistent: at most one CTA per SM
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
@@ -1206,11 +1364,22 @@ int launch(const rdx_gemm_args& a, cudaStream_t stream) {
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = (pdl_enabled() || ep.a_ready) ? 1 : 0;
+  attr[1].val.programmaticStreamSerializationAllowed = (pdl_enabled() || j0.ep.a_ready) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mb2, mb4, mc, md, a.m, a.n, a.k, tail_start, split, ep));
+  RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, mp0, mp1, m, j0, j1, dep, dep_cols));
   return RDX_OK;
+}
+
+template <int BN, int EPI, int CG>
+int launch(const rdx_gemm_args& a, cudaStream_t stream) {
+  JobMaps mp0, mp1;
+  JobArgs j0, j1;
+  int64_t units = 0;
+  if (int st = prepare_job<BN, EPI, CG>(a, &mp0, &j0, &units)) return st;
+  std::memset(&mp1, 0, sizeof(mp1));
+  std::memset(&j1, 0, sizeof(j1));
+  return launch_jobs<BN, EPI, CG, -1>(mp0, mp1, a.m, j0, j1, nullptr, 0, units, stream);
 }
 
 template <int EPI>
@@ -1221,6 +1390,23 @@ int dispatch(const rdx_gemm_args& a, int bn, int cg, cudaStream_t s) {
   } else {
     return bn == 256 ? launch<256, EPI, 1>(a, s) : launch<128, EPI, 1>(a, s);
   }
+}
+
+template <int BN, int CG>
+int launch_mlp_pair(const rdx_gemm_args& g, const rdx_gemm_args& d, uint32_t* dep, cudaStream_t stream) {
+  JobMaps mp0, mp1;
+  JobArgs j0, j1;
+  int64_t u0 = 0, u1 = 0;
+  if (int st = prepare_job<BN, RDX_EPI_SWIGLU, CG>(g, &mp0, &j0, &u0, 1)) return st;
+  const int64_t nt0 = j0.tail_start + j0.split * (((g.m + BM * CG - 1) / (BM * CG)) *
+                                                  (j0.ep.cp_ncol > 0 ? j0.ep.cp_ncol : (g.n + BN - 1) / BN) -
+                                                  j0.tail_start);
+  if (int st = prepare_job<BN, RDX_EPI_RESID_F32, CG>(d, &mp1, &j1, &u1, 2, nt0)) return st;
+  const int64_t units_max = num_sms() / CG;
+  int64_t units = u0 > u1 ? u0 : u1;
+  units = units < units_max ? units : units_max;
+  return launch_jobs<BN, RDX_EPI_SWIGLU, CG, RDX_EPI_RESID_F32>(mp0, mp1, g.m, j0, j1, dep,
+                                                                  static_cast<uint32_t>(g.n / 2), units, stream);
 }
 
 // Pick (CG, BN) minimising tile rounds x per-tile cost.  A 1-CTA tile streams
@@ -1331,6 +1517,61 @@ extern "C" int rdx_gemm(const rdx_gemm_args* args, void* stream) {
     default:
       return RDX_ERR_INVALID_ARGUMENT;
   }
+}
+
+// Checks of rdx_gemm shared by rdx_gemm_pair (RDX_OK or the status rdx_gemm returns).
+namespace rdx {
+namespace gemm {
+int validate_common(const rdx_gemm_args& a) {
+  if (a.m < 0 || a.n <= 0 || a.k <= 0) return RDX_ERR_SHAPE_MISMATCH;
+  if ((a.k % 8) || (a.lda % 8) || (a.ldb % 8) || a.lda < a.k || a.ldb < a.k) return RDX_ERR_SHAPE_MISMATCH;
+  if (a.m >= (int64_t(1) << 31) || a.n >= (int64_t(1) << 31)) return RDX_ERR_CAPACITY_EXCEEDED;
+  if (!a.a || !a.b || !a.out) return RDX_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(a.a) | reinterpret_cast<uintptr_t>(a.b) | reinterpret_cast<uintptr_t>(a.out)) & 15)
+    return RDX_ERR_INVALID_ARGUMENT;
+  if (a.block_n != 0 && a.block_n != 128 && a.block_n != 256) return RDX_ERR_INVALID_ARGUMENT;
+  if (a.row_ss && (a.ss_parts <= 0 || a.norm_dim <= 0)) return RDX_ERR_INVALID_ARGUMENT;
+  if (a.done_ctr && a.epi != RDX_EPI_RESID_F32) return RDX_ERR_INVALID_ARGUMENT;
+  return RDX_OK;
+}
+}  // namespace gemm
+}  // namespace rdx
+
+extern "C" int rdx_gemm_pair(const rdx_gemm_args* first, const rdx_gemm_args* second, uint32_t* dep_ctr,
+                             void* stream) {
+  using namespace rdx;
+  using namespace rdx::gemm;
+  if (!first || !second) return RDX_ERR_INVALID_ARGUMENT;
+  const rdx_gemm_args &g = *first, &d = *second;
+  if (int st = validate_common(g)) return st;
+  if (int st = validate_common(d)) return st;
+  if (g.epi != RDX_EPI_SWIGLU || d.epi != RDX_EPI_RESID_F32) return RDX_ERR_UNSUPPORTED;
+  if (g.m != d.m || d.a != g.out || d.lda != g.ldo || d.k != g.n / 2 || d.a_ready) return RDX_ERR_SHAPE_MISMATCH;
+  if (g.n % (2 * kSwigluUnit) || g.ldo % 8 || g.ldo < g.n / 2) return RDX_ERR_SHAPE_MISMATCH;
+  if (d.ldo % 4 || d.ldo < d.n) return RDX_ERR_SHAPE_MISMATCH;
+  if (!dep_ctr) return RDX_ERR_INVALID_ARGUMENT;
+  if (g.m == 0) return RDX_OK;
+  int bn0 = 256, cg0 = 1, bn1 = 256, cg1 = 1;
+  choose_shape(g, &bn0, &cg0);
+  choose_shape(d, &bn1, &cg1);
+  cudaStream_t s = as_stream(stream);
+  // One launch pays off when the MLP is a few rounds of tiles (C2: +3.9 % per step); at C3/C4
+  // scale (>= 64 pair row blocks, grouped raster) a launch boundary is noise and measured
+  // neutral / -2 %, so those shapes (and pairs that want different tile shapes) run as two
+  // stream-ordered launches (dep_ctr unused).
+  const bool few_rounds = (g.m + 2 * BM - 1) / (2 * BM) < 64;
+  if (!pair_enabled() || !few_rounds || bn0 != bn1 || cg0 != cg1 || bn0 != 256 || cg0 != 2) {
+    if (int st = rdx_gemm(first, stream)) return st;
+    return rdx_gemm(second, stream);
+  }
+  return launch_mlp_pair<256, 2>(g, d, dep_ctr, s);
+}
+
+// RDX_GEMM_PAIR=0 (env) or rdx_gemm_debug_pair(0): rdx_gemm_pair runs two launches (A/B).
+extern "C" int rdx_gemm_debug_pair(int on) {
+  const int prev = rdx::gemm::pair_enabled() ? 1 : 0;
+  rdx::gemm::g_pair = on ? 1 : 0;
+  return prev;
 }
 
 // Debug: switch the GEMM tail split on (1) / off (0); returns the previous setting.

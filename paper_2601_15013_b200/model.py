@@ -368,6 +368,8 @@ class RadixQwen3:
         # chained norm -> next GEMM on ready counters: correct (tests) but measured slower
         # (C2 -6.7 %, C3 -4.5 %), so off unless RDX_NORM_CHAIN=1
         self.norm_chain = os.environ.get("RDX_NORM_CHAIN", "0") == "1"
+        # gate|up -> down as one persistent launch (rdx_gemm_pair); RDX_GEMM_PAIR=0: two launches
+        self.mlp_pair = os.environ.get("RDX_GEMM_PAIR", "1") != "0"
         if self.fused_norm:
             if config.hidden_size % 64:
                 raise ShapeMismatch("fused_norm needs hidden_size % 64 == 0")
@@ -385,7 +387,7 @@ class RadixQwen3:
         return fn()
 
     def _gemm(self, name, a, w, epi, out, *, m, stream, qkv=False, rope=None, layer=None, row_ss=None,
-              hb=None, ss_out=None, done=None, ready=None):
+              hb=None, ss_out=None, done=None, ready=None, build_only=False):
         cfg = self.config
         args = _native.GemmArgs()
         args.a = a.data_ptr()
@@ -426,12 +428,23 @@ class RadixQwen3:
             args.out_bf16 = hb.data_ptr()
             args.ldo_bf16 = hb.stride(0)
             args.ss_out = ss_out.data_ptr()
+        if build_only:  # the caller launches it (rdx_gemm_pair)
+            return args
         lib = _native.lib()
 
         def launch():
             _native.check(lib.rdx_gemm(args, stream), f"rdx_gemm[{name}]")
 
         self._op("gemm." + name, launch, 2.0 * m * args.n * args.k)
+
+    def _gemm_pair(self, first, second, dep, stream):
+        """gate|up and down in one persistent launch (rdx_gemm_pair, dep: zeroed slab counters)."""
+        lib = _native.lib()
+
+        def launch():
+            _native.check(lib.rdx_gemm_pair(first, second, dep.data_ptr(), stream), "rdx_gemm_pair")
+
+        self._op("gemm.mlp", launch, 2.0 * first.m * first.n * first.k + 2.0 * second.m * second.n * second.k)
 
     def _rmsnorm(self, x, w, out, rows=None, n_rows=None, stream=None):
         lib = _native.lib()
@@ -739,9 +752,13 @@ class RadixQwen3:
         # (gate_up / the next layer's QKV) starts on them as its programmatic dependent
         chain = overlap and self.norm_chain
         slabs = -(-m // 32)
-        ctrs = torch.zeros(2 * slabs if chain else slabs, dtype=torch.int32, device=dev) if overlap else None
+        pair = self.mlp_pair and not fused
+        n_dep = cfg.num_layers * slabs if pair else 0
+        n_ctr = (2 * slabs if chain else slabs) if overlap else 0
+        ctrs = torch.zeros(n_ctr + n_dep, dtype=torch.int32, device=dev) if n_ctr + n_dep else None  # one memset
         ctr = ctrs[:slabs] if overlap else None
-        rdy = ctrs[slabs:] if chain else None
+        rdy = ctrs[slabs:2 * slabs] if chain else None
+        deps = ctrs[n_ctr:] if pair else None
         uses = 0
 
         def norm_after(wt):
@@ -773,11 +790,18 @@ class RadixQwen3:
                        ss_out=ss, done=ctr)
             if not fused:
                 norm_after(T[pre + "ln2"])
-            self._gemm("gate_up", hn, T[pre + "w_gu" + sfx], _native.EPI_SWIGLU, act, m=m, stream=st, row_ss=ss,
-                       ready=ready_arg())
             last = i + 1 == cfg.num_layers
-            self._gemm("down", act, T[pre + "w_down"], resid_epi, h, m=m, stream=st, hb=hn if fused else None,
-                       ss_out=ss, done=None if last else ctr)
+            if pair:
+                g_args = self._gemm("gate_up", hn, T[pre + "w_gu"], _native.EPI_SWIGLU, act, m=m, stream=st,
+                                    ready=ready_arg(), build_only=True)
+                d_args = self._gemm("down", act, T[pre + "w_down"], resid_epi, h, m=m, stream=st,
+                                    done=None if last else ctr, build_only=True)
+                self._gemm_pair(g_args, d_args, deps[i * slabs:(i + 1) * slabs], st)
+            else:
+                self._gemm("gate_up", hn, T[pre + "w_gu" + sfx], _native.EPI_SWIGLU, act, m=m, stream=st,
+                           row_ss=ss, ready=ready_arg())
+                self._gemm("down", act, T[pre + "w_down"], resid_epi, h, m=m, stream=st,
+                           hb=hn if fused else None, ss_out=ss, done=None if last else ctr)
             if not fused and not last:
                 norm_after(T[f"layers.{i + 1}.ln1"])
 

@@ -22,6 +22,8 @@ elif what == "groupk":  # raster group of the K >= 8192 GEMMs only (C4 down): G_
 elif what == "norm":  # model-level switch: rmsnorm overlapping the residual GEMM's tail
     def setter(on):
         os.environ["RDX_NORM_OVERLAP"] = str(on)
+elif what == "pair":  # gate|up + down as one launch (rdx_gemm_pair) vs two launches
+    setter = lib.rdx_gemm_debug_pair
 elif what == "chain":  # model-level switch: norm -> next GEMM chained on ready counters
     def setter(on):
         os.environ["RDX_NORM_CHAIN"] = str(on)

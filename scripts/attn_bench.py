@@ -125,7 +125,8 @@ if os.environ.get("RDX_ATTN_TRACE") == "1":
     ev = sorted((buf[2 + 2 * i], buf[3 + 2 * i]) for i in range(n))
     t0 = ev[0][0] if ev else 0
     roles = {0: "LOAD", 1: "MMA ", 2: "SOFT", 3: "EPI "}
-    names = {(0, 1): "K tile", (0, 2): "V tile", (1, 1): "issue S", (1, 2): "got P", (2, 1): "got S",
+    names = {(0, 1): "K tile", (0, 2): "V tile", (1, 1): "issue S", (1, 2): "got P", (1, 3): "K ready",
+             (1, 4): "V ready", (2, 1): "got S",
              (2, 2): "pub P", (2, 3): "S in regs", (2, 4): "max done", (2, 5): "exp done", (3, 1): "O ready",
              (3, 2): "O stored"}
     for tt, code in ev[:int(os.environ.get("TRACE_N", "160"))]:

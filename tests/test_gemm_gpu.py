@@ -601,3 +601,63 @@ def test_gemm_shape_fuzz():
         assert (out - ref).abs().max().item() <= tol, (m, n, k, shape, group)
         assert (h - (h0 + ref)).abs().max().item() <= tol, (m, n, k, shape, group)
         assert (ctr == n).all(), (m, n, k, shape, group)
+
+
+def _unweave(gu):
+    """[m, 2 di] gate|up output interleaved in 64-column units -> (gate, up), each [m, di]."""
+    m, n = gu.shape
+    v = gu.view(m, n // 128, 2, 64)
+    return v[:, :, 0, :].reshape(m, n // 2), v[:, :, 1, :].reshape(m, n // 2)
+
+
+@pytest.mark.parametrize("m,d,di", [(7024, 1024, 3072), (5000, 1024, 3072), (300, 512, 1536), (20000, 2560, 9728)])
+def test_gemm_pair_bit_identical(m, d, di):
+    """rdx_gemm_pair (gate|up SwiGLU then down residual in one persistent launch, down tiles
+    gated on per-slab counters of act) == the two rdx_gemm launches, bit for bit; the slab
+    counters of the down GEMM's own done_ctr still reach N."""
+    import torch
+
+    from paper_2601_15013_b200 import _native
+
+    lib = _native.lib()
+    st = _native.stream_handle()
+    x = _rand(m, d, 51)
+    wgu = _rand(2 * di, d, 52, 0.05)
+    wd = _rand(d, di, 53, 0.05)
+    h0 = torch.randn(m, d, device="cuda")
+    slabs = -(-m // 32)
+
+    def args(a, w, epi, out, done=None):
+        g = _native.GemmArgs()
+        g.a, g.b, g.m, g.n, g.k = a.data_ptr(), w.data_ptr(), m, w.shape[0], w.shape[1]
+        g.lda, g.ldb, g.epi, g.out, g.ldo = a.stride(0), w.stride(0), epi, out.data_ptr(), out.stride(0)
+        if done is not None:
+            g.done_ctr = done.data_ptr()
+        return g
+
+    outs = []
+    for pair in (1, 0):
+        prev = lib.rdx_gemm_debug_pair(pair)
+        try:
+            act = torch.full((m, di), float("nan"), device="cuda").to(torch.bfloat16)
+            h = h0.clone()
+            done = torch.zeros(slabs, dtype=torch.int32, device="cuda")
+            dep = torch.zeros(slabs, dtype=torch.int32, device="cuda")
+            g = args(x, wgu, _native.EPI_SWIGLU, act)
+            dn = args(act, wd, _native.EPI_RESID_F32, h, done)
+            _native.check(lib.rdx_gemm_pair(g, dn, dep.data_ptr(), st), "rdx_gemm_pair")
+            torch.cuda.synchronize()
+        finally:
+            lib.rdx_gemm_debug_pair(prev)
+        assert (done == d).all()
+        if pair and bool(dep.any()):  # the one-launch path ran (not the two-launch fallback)
+            assert (dep == di).all()  # every act column of every slab was published
+        outs.append((act, h))
+    _native.check_device_status()
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    # and against torch (fp32 reference of the SwiGLU MLP on the bf16 act)
+    gu = x.float() @ wgu.float().T
+    gate, up = _unweave(gu)
+    ref_act = (torch.nn.functional.silu(gate) * up)
+    assert (outs[0][0].float() - ref_act).abs().max().item() <= 2e-2 * ref_act.abs().max().item()

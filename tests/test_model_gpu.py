@@ -197,6 +197,36 @@ def test_norm_overlap_bit_identical():
     _native.check_device_status()  # no slab wait timed out on the way
 
 
+@pytest.mark.parametrize("graphs", [False, True])
+def test_mlp_pair_bit_identical(graphs):
+    """gate|up and down in one persistent launch (rdx_gemm_pair) == two launches, bit for
+    bit, with the overlapped norms on, eager and under CUDA graphs, dedup on and off."""
+    import torch
+
+    from paper_2601_15013_b200 import DeviceWeights, RadixQwen3, _native
+    from paper_2601_15013_b200.model import QWEN3_PRESETS, DeviceBatch, Qwen3Config
+    from paper_2601_15013_b200.plan import build_plan_device
+    from paper_2601_15013_b200.workloads import RerankSpec, msmarco_rerank_batch
+
+    base = QWEN3_PRESETS["qwen3-0.6b"]
+    cfg = Qwen3Config(4, base.hidden_size, base.intermediate_size, base.num_heads, base.num_kv_heads, base.head_dim,
+                      base.vocab_size, base.rope_theta, base.norm_eps)
+    w = DeviceWeights.random(cfg, seed=7)
+    db = DeviceBatch.from_batch(msmarco_rerank_batch(RerankSpec(passages_per_query=64)))
+    plan = build_plan_device(db.tok, db.pos, db.cu)
+    outs = {}
+    for pair in (True, False):
+        m = RadixQwen3(cfg, w, use_graphs=graphs)
+        m.mlp_pair = pair
+        for p in (plan, None):
+            m.prefill(db, p, logits="last")
+            outs[(pair, p is None)] = m.prefill(db, p, logits="last").clone()
+    torch.cuda.synchronize()
+    _native.check_device_status()
+    for nd in (False, True):
+        assert torch.equal(outs[(True, nd)], outs[(False, nd)])
+
+
 @pytest.mark.parametrize("preset,layers", [("qwen3-0.6b", 4), ("qwen3-4b", 2), ("qwen3-8b", 2)])
 def test_norm_chain_bit_identical_widths(preset, layers):
     """The chained norm -> GEMM pipeline (the GEMM streams rows the norm publishes on
