@@ -356,9 +356,10 @@ int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const 
  * sums per-role clock counters (MMA waits on K/V, P, Q, O; softmax waits on S,
  * epilogue; loader waits on free slots; totals); this copies n slots to host
  * and resets them. */
-/* Debug: short units at head_dim 128 run 64-key K/V tiles with two S buffers per
- * query tile (S two key tiles ahead of the softmax); 0 selects the 128-key
- * single-buffered kernel for A/B runs, 1 back on.  Same math, same tolerance.
+/* Debug: 1 runs short suffix-query units at head_dim 128 on 64-key K/V tiles
+ * with two S buffers per query tile (S two key tiles ahead of the softmax), 0
+ * (the default, also RDX_ATTN_BK64 unset) on the 128-key single-buffered kernel.
+ * Same tolerance; only equal key tiles keep suffix and plain attention bit-identical.
  * Returns the previous setting. */
 int rdx_attention_debug_bk64(int on);
 

@@ -1104,7 +1104,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 }
 
 unsigned long long* g_stats = nullptr;  // debug counters (RDX_ATTN_STATS=1)
-int g_attn_bk64 = 1;                    // rdx_attention_debug_bk64: 64-key double-buffered variant on/off
+int g_attn_bk64 = 1;                    // rdx_attention_debug_bk64 (AND-ed with RDX_ATTN_BK64=1)
 unsigned long long* g_cta_times = nullptr;  // debug per-CTA [start, end, units]
 uint32_t* g_trace = nullptr;            // debug event log of CTA 0 (RDX_ATTN_STATS=1)
 
@@ -1202,14 +1202,16 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
   cudaStream_t s = as_stream(stream);
   if (head_dim <= 64)
     return short_units ? launch<64, 2, 4, kEmulated>(a, qkv_rows, s) : launch<64, 1, 6, kEmulated>(a, qkv_rows, s);
-  // short suffix-query units at head_dim 128: 64-key tiles with double-buffered S (RDX_ATTN_BK64=0:
-  // 128-key tiles).  Measured at C2: suffix 35.1 vs 35.5 us; the plain layout (full-length query
-  // tiles) is faster on 128-key tiles (43.8 vs 46.8 us), so it keeps them.
+  // short suffix-query units at head_dim 128: 64-key tiles with double-buffered S when enabled
+  // (RDX_ATTN_BK64=1 / rdx_attention_debug_bk64(1)).  Off by default: it gains 1 % at C2 (35.1 vs
+  // 35.5 us) but the plain layout is faster on 128-key tiles (43.8 vs 46.8 us), and different key
+  // tiles change the online-softmax order, so suffix and plain attention (RadixMLP on vs off)
+  // would no longer give bit-identical rows.
   static const int bk64 = [] {
     const char* v = std::getenv("RDX_ATTN_BK64");
-    return v && v[0] == '0' ? 0 : 1;
+    return v && v[0] == '1' ? 1 : 0;
   }();
-  if (short_units && scatter && bk64 && g_attn_bk64) return launch<128, 2, 6, kEmulated, 64>(a, qkv_rows, s);
+  if (short_units && scatter && (bk64 || g_attn_bk64 == 2)) return launch<128, 2, 6, kEmulated, 64>(a, qkv_rows, s);
   return short_units ? launch<128, 2, 3, kEmulated>(a, qkv_rows, s) : launch<128, 1, 4, kEmulated>(a, qkv_rows, s);
 }
 
@@ -1247,7 +1249,7 @@ int rdx::take_device_status_attention(int* out, cudaStream_t st) { return take_d
 // Debug: the 64-key double-buffered-S variant for short units on (1) / off (0) for A/B
 // runs; returns the previous setting.
 extern "C" int rdx_attention_debug_bk64(int on) {
-  const int prev = rdx::attn::g_attn_bk64;
-  rdx::attn::g_attn_bk64 = on ? 1 : 0;
+  const int prev = rdx::attn::g_attn_bk64 == 2 ? 1 : 0;
+  rdx::attn::g_attn_bk64 = on ? 2 : 0;  // 2 = forced on for this process
   return prev;
 }

@@ -61,7 +61,7 @@ for layout in ("suffix", "plain"):
             e.record()
             e.synchronize()
             res[v].append(s.elapsed_time(e) / 5 * 1e3)
-    lib.rdx_attention_debug_bk64(1)
+    lib.rdx_attention_debug_bk64(0)
     diff = (outs[1].float() - outs[0].float()).abs().max().item()
     # fp32 reference on the first 4 sequences (suffix queries attend to all keys of their sequence)
     qf = qkv.float()
