@@ -752,7 +752,9 @@ class RadixQwen3:
         # (gate_up / the next layer's QKV) starts on them as its programmatic dependent
         chain = overlap and self.norm_chain
         slabs = -(-m // 32)
-        pair = self.mlp_pair and not fused
+        # (rdx_gemm_pair runs two launches itself at >= 64 pair row blocks; decided here too so
+        # launch counts and the per-op breakdown name what runs)
+        pair = self.mlp_pair and not fused and -(-m // 256) < 64
         n_dep = cfg.num_layers * slabs if pair else 0
         n_ctr = (2 * slabs if chain else slabs) if overlap else 0
         ctrs = torch.zeros(n_ctr + n_dep, dtype=torch.int32, device=dev) if n_ctr + n_dep else None  # one memset
