@@ -363,6 +363,12 @@ int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_rows, const 
  * Returns the previous setting. */
 int rdx_attention_debug_bk64(int on);
 
+/* Debug: a short last round of attention units (rem units, 2 rem <= CTAs) is dealt
+ * as single-query-tile half units, one per CTA (1; also RDX_ATTN_SPLIT=1), or as
+ * whole units (0, the default: the half units measured slower).  Returns the
+ * previous setting. */
+int rdx_attention_debug_split(int on);
+
 int rdx_attention_debug_stats(unsigned long long* host, int n);
 /* Debug: event log of CTA 0 of the last launch in the same mode:
  * [count, (clock, code) x min(count, 4096)] as 32-bit words. */

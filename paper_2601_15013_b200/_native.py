@@ -51,6 +51,7 @@ EXPORTS = (
     "rdx_debug_pdl",
     "rdx_attention",
     "rdx_attention_debug_bk64",
+    "rdx_attention_debug_split",
     "rdx_attention_debug_stats",
     "rdx_attention_debug_trace",
     "rdx_attention_debug_cta_times",
@@ -147,6 +148,7 @@ _SIGNATURES = {
     "rdx_gemm_debug_pair": (ctypes.c_int, [ctypes.c_int]),
     "rdx_plan_debug_smem": (ctypes.c_int, [ctypes.c_int]),
     "rdx_attention_debug_bk64": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_attention_debug_split": (ctypes.c_int, [ctypes.c_int]),
     "rdx_plan_debug_trace": (ctypes.c_int, [_vp]),
     "rdx_gemm_debug_stats": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rdx_gemm_debug_shape": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),

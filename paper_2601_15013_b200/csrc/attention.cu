@@ -245,6 +245,7 @@ struct Args {
   int n_units;               // max_pairs * nseq * kv_heads
   int use_tma;               // head_dim % 64 == 0: whole 128-byte column boxes, TMA tile loads
   int bk;                    // keys per K/V tile of the launched variant (64 or 128)
+  int split_tail;            // deal a short last round as single-query-tile half units
   float scale_log2;          // softmax scale * log2(e)
   unsigned long long* stats; // debug (RDX_ATTN_STATS_BUILD + RDX_ATTN_STATS=1): summed clocks per role
   uint32_t* trace;           // debug: event log of CTA trace_cta [count, (clock, code) x 4096]
@@ -359,6 +360,24 @@ __device__ __forceinline__ void sched_units(const Args& a, const Ring& r, int la
     __syncwarp();
     ++k;
   };
+  // Tail split: when the last partial round holds rem units and 2 rem <= G, those units
+  // (the shortest: dense order is longest first) are dealt as 2 rem single-query-tile
+  // half units, one per CTA, so the slowest CTAs run n/G + 1/2 units instead of n/G + 1
+  // (C2: 512 units on 148 CTAs = 3 rounds + 68 -> 136 halves).  Needs the valid-unit
+  // count first: one pass of ballots over the (pair level, sequence) grid.
+  int64_t base = INT64_MAX;
+  if (a.split_tail) {
+    int64_t n_full = 0;
+    for (int pair = a.max_pairs - 1; pair >= 0; --pair)
+      for (int s0 = 0; s0 < a.nseq; s0 += 32) {
+        const int sq = s0 + lane;
+        bool ok = false;
+        if (sq < a.nseq) ok = 2 * pair * a.qpt < __ldg(a.cu_q + sq + 1) - __ldg(a.cu_q + sq);
+        n_full += static_cast<int64_t>(__popc(__ballot_sync(0xffffffffu, ok))) * a.kv_heads;
+      }
+    const int64_t rem = n_full % G;
+    if (rem > 0 && 2 * rem <= G) base = n_full - rem;
+  }
   int64_t dense = 0;  // dense index of the first unit of the current chunk
   for (int pair = a.max_pairs - 1; pair >= 0; --pair) {
     for (int s0 = 0; s0 < a.nseq; s0 += 32) {
@@ -376,10 +395,8 @@ __device__ __forceinline__ void sched_units(const Args& a, const Ring& r, int la
       }
       const uint32_t bits = __ballot_sync(0xffffffffu, ok);
       const int64_t cnt = static_cast<int64_t>(__popc(bits)) * a.kv_heads;
-      // this CTA's dense indices in [dense, dense + cnt): one candidate per snake round
-      for (int64_t rd = dense / G; rd * G < dense + cnt; ++rd) {
-        const int64_t d = rd * G + ((rd & 1) ? (G - 1 - c) : c);
-        if (d < dense || d >= dense + cnt) continue;
+      // one unit (or half unit) of dense index d in this chunk: geometry + publish
+      auto emit = [&](int64_t d, int half) {
         const int e = static_cast<int>(d - dense);
         const int nth = e / a.kv_heads;  // nth valid sequence of the chunk
         int l = 0;
@@ -392,7 +409,27 @@ __device__ __forceinline__ void sched_units(const Args& a, const Ring& r, int la
         const int g = e - nth * a.kv_heads;
         const int u = (a.max_pairs - 1 - pair) * (a.nseq * a.kv_heads) + (s0 + l) * a.kv_heads + g;
         unit_geometry(a, u, ka, kb, qa, qb, it);
+        if (half == 0) {  // the pair's first query tile alone
+          it.nkt1 = 0;
+        } else if (half == 1) {  // its second query tile alone, as tile h = 0
+          if (it.nkt1 == 0) return;  // the pair has no second tile: nothing to run
+          it.mb0 += 1;
+          it.nkt0 = it.nkt1;
+          it.nkt1 = 0;
+        }
         publish(u, it);
+      };
+      // this CTA's dense indices in [dense, min(dense + cnt, base)): one candidate per snake round
+      for (int64_t rd = dense / G; rd * G < dense + cnt; ++rd) {
+        const int64_t d = rd * G + ((rd & 1) ? (G - 1 - c) : c);
+        if (d < dense || d >= dense + cnt || d >= base) continue;
+        emit(d, -1);
+      }
+      // the tail's half units: half k = 2 (d - base) + h goes to CTA k mod G
+      for (int64_t d = dense > base ? dense : base; d < dense + cnt; ++d) {
+        const int64_t k0 = 2 * (d - base);
+        if (k0 % G == c) emit(d, 0);
+        if ((k0 + 1) % G == c) emit(d, 1);
       }
       dense += cnt;
     }
@@ -1105,6 +1142,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 
 unsigned long long* g_stats = nullptr;  // debug counters (RDX_ATTN_STATS=1)
 int g_attn_bk64 = 1;                    // rdx_attention_debug_bk64 (AND-ed with RDX_ATTN_BK64=1)
+int g_attn_split = 0;                   // rdx_attention_debug_split: 2 = half units forced on
 unsigned long long* g_cta_times = nullptr;  // debug per-CTA [start, end, units]
 uint32_t* g_trace = nullptr;            // debug event log of CTA 0 (RDX_ATTN_STATS=1)
 
@@ -1181,6 +1219,14 @@ extern "C" int rdx_attention(const void* qkv_bf16, int64_t ld_qkv, int64_t qkv_r
   a.stats = nullptr;
   a.trace = nullptr;
   a.trace_cta = 0;
+  // off by default: measured slower at C2 (35.5 vs 34.8 us suffix, 38.8 vs 32.5 us on the
+  // literal configs[1] shape): the counting pass delays every CTA's first unit and a lone
+  // query tile loses the two-tile ping-pong that hides its softmax
+  static const int split_env = [] {
+    const char* v = std::getenv("RDX_ATTN_SPLIT");
+    return v && v[0] == '1' ? 1 : 0;
+  }();
+  a.split_tail = split_env || g_attn_split == 2;
   a.cta_times = nullptr;
   if (const char* e = std::getenv("RDX_ATTN_STATS")) {
     if (e[0] == '1') {
@@ -1251,5 +1297,13 @@ int rdx::take_device_status_attention(int* out, cudaStream_t st) { return take_d
 extern "C" int rdx_attention_debug_bk64(int on) {
   const int prev = rdx::attn::g_attn_bk64 == 2 ? 1 : 0;
   rdx::attn::g_attn_bk64 = on ? 2 : 0;  // 2 = forced on for this process
+  return prev;
+}
+
+// Debug: deal a short last round of attention units as single-query-tile half units
+// (1) or not (0, the default); returns the previous setting.
+extern "C" int rdx_attention_debug_split(int on) {
+  const int prev = rdx::attn::g_attn_split == 2 ? 1 : 0;
+  rdx::attn::g_attn_split = on ? 2 : 0;
   return prev;
 }

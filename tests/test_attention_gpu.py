@@ -70,7 +70,7 @@ def test_plain_layout(hd, H, KV):
     assert err <= 2e-2 * ref.abs().max().item() + 1e-3, err
 
 
-@pytest.mark.parametrize("pipeline", ["auto", "long", "bk64"])
+@pytest.mark.parametrize("pipeline", ["auto", "long", "bk64", "split"])
 @pytest.mark.parametrize("hd,H,KV", [(128, 16, 8), (128, 32, 8), (64, 4, 2), (16, 4, 2)])
 def test_suffix_queries_through_scatter(hd, H, KV, pipeline):
     """Compact Q rows + K/V gathered through the plan's scatter map == full-layout attention."""
@@ -90,11 +90,14 @@ def test_suffix_queries_through_scatter(hd, H, KV, pipeline):
     scatter = torch.from_numpy(np.array(plan.scatter_indices).view(np.int32)).cuda()
     from paper_2601_15013_b200 import _native
 
-    prev = _native.lib().rdx_attention_debug_bk64(1 if pipeline == "bk64" else 0)  # 64-key double-buffered S
+    lib = _native.lib()
+    prev = lib.rdx_attention_debug_bk64(1 if pipeline == "bk64" else 0)  # 64-key double-buffered S
+    prev_s = lib.rdx_attention_debug_split(1 if pipeline == "split" else 0)  # half units in the last round
     try:
         out = _run(qkv, scatter, b.cu_seqlens, cu_q, H, KV, hd, m, max_k=0 if pipeline == "long" else None)
     finally:
-        _native.lib().rdx_attention_debug_bk64(prev)
+        lib.rdx_attention_debug_bk64(prev)
+        lib.rdx_attention_debug_split(prev_s)
     ref_full = _reference(qkv, scatter, b.cu_seqlens, H, KV, hd)
     gather = torch.from_numpy(np.array(plan.gather_indices).astype(np.int64)).cuda()
     ref = ref_full[gather]
