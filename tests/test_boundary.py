@@ -153,6 +153,21 @@ def test_swap_reference_binding_contract_gpu():
             assert np.array_equal(got["gather"], ref.gather_indices)
             assert np.array_equal(got["scatter"], ref.scatter_indices)
             assert np.array_equal(got["compact_positions"], ref.compact_positions)
+        # acceptance criterion 12 (test_acceptance.py:302-339): the reference CLI `plan --binary`
+        # (CPU numba planner) and the binding's save_plan of the GPU plan write identical bytes
+        from radix_compact import save_batch
+        from radix_compact.cli import main as cli_main
+        with tempfile.TemporaryDirectory() as d:
+            for i in range(100):
+                b = int(rng.integers(1, 7))
+                cu = np.concatenate([[0], np.cumsum(rng.integers(1, 12, size=b))]).astype(np.int64)
+                tokens = rng.integers(0, 4, size=int(cu[-1])).astype(np.uint32)
+                batch = radix_compact.RaggedBatch(tokens, default_positions(cu), cu)
+                bfile, pfile, qfile = (os.path.join(d, n) for n in ("b.json", "p.rdxp", "q.rdxp"))
+                save_batch(batch, bfile)
+                assert cli_main(["plan", bfile, "-o", pfile, "--binary"]) == 0
+                rb.save_plan(rb.compute_plan(batch.token_ids, batch.position_ids, batch.cu_seqlens), qfile)
+                assert open(pfile, "rb").read() == open(qfile, "rb").read(), i
         print("PASS")
     """)
     out = _run(code)
