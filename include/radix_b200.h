@@ -169,6 +169,10 @@ int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* rows, int64_t
                      int64_t d, const float* w, float eps, void* out_bf16, int64_t ld_out,
                      void* stream);
 
+/* cudaStreamSynchronize(stream) (a C-ABI caller's one host wait, e.g. after
+ * rdx_plan_build wrote its info into pinned memory). */
+int rdx_stream_synchronize(void* stream);
+
 /* First device-side failure of an asynchronous contract since the last call
  * (RDX_OK or RDX_ERR_DEVICE_TIMEOUT), then cleared; synchronises `stream`. */
 int rdx_device_status(void* stream);

@@ -38,6 +38,7 @@ EXPORTS = (
     "rdx_rmsnorm_rows",
     "rdx_rmsnorm_rows_after",
     "rdx_device_status",
+    "rdx_stream_synchronize",
     "rdx_rope_table",
     "rdx_rope_table_blocked",
     "rdx_gemm",
@@ -138,6 +139,7 @@ _SIGNATURES = {
     "rdx_embed_rows": (ctypes.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "rdx_rmsnorm_rows": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i64, _vp, _f32, _vp, _i64, _vp]),
     "rdx_device_status": (ctypes.c_int, [_vp]),
+    "rdx_stream_synchronize": (ctypes.c_int, [_vp]),
     "rdx_rmsnorm_rows_after": (ctypes.c_int, [_vp, _i64, _i64, _i64, _vp, _f32, _vp, _i64, _vp, _u32, _vp, _vp]),
     "rdx_rope_table": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
     "rdx_rope_table_blocked": (ctypes.c_int, [_vp, _i64, _i32, _f64, _vp, _vp]),
@@ -233,5 +235,7 @@ def ptr(t) -> int | None:
 def stream_handle(stream=None) -> int:
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    # the current stream's raw handle without building a torch.cuda.Stream object (~4 us less)
+    return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())

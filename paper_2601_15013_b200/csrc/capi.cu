@@ -65,6 +65,11 @@ extern "C" const char* rdx_status_name(int status) {
 
 extern "C" const char* rdx_last_cuda_error(void) { return rdx::g_last_error; }
 
+extern "C" int rdx_stream_synchronize(void* stream) {
+  RDX_CUDA_TRY(cudaStreamSynchronize(rdx::as_stream(stream)));
+  return RDX_OK;
+}
+
 extern "C" int rdx_device_status(void* stream) {
   cudaStream_t st = rdx::as_stream(stream);
   int a = 0, r = 0;

@@ -134,15 +134,19 @@ _WORKSPACE = _Workspace()
 _PINNED = threading.local()
 
 
+_SCRATCH_BYTES: dict = {}
+
+
 def _info_buffer():
-    """Thread-local pinned 4-word buffer the planner kernel writes (N', status, attempts,
-    max_q) into directly: host memory allocated by cudaHostAlloc is device-addressable
-    under unified addressing, so no device-to-host copy is queued after the kernel."""
+    """Thread-local pinned 4-word buffer (tensor, numpy view) the planner kernel writes
+    (N', status, attempts, max_q) into directly: host memory allocated by cudaHostAlloc is
+    device-addressable under unified addressing, so no device-to-host copy is queued."""
     import torch
 
     buf = getattr(_PINNED, "info", None)
     if buf is None:
-        buf = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        t = torch.zeros(4, dtype=torch.int32, pin_memory=True)
+        buf = (t, t.numpy())
         _PINNED.info = buf
     return buf
 
@@ -167,22 +171,27 @@ def build_plan_device(tok, pos, cu, *, allow_empty: bool = False, stream=None,
     nn, nb = max(n, 1), max(b, 1)
     buf = torch.empty(3 * nn + (b + 1) + nb, dtype=torch.int32, device=dev)
     o = 3 * nn
-    cu_q, lcp = buf[o:o + b + 1], buf[o + b + 1:]
-    scratch = _WORKSPACE.get(dev, int(lib.rdx_plan_scratch_bytes(n, b)))
+    key = (n, b)
+    sb = _SCRATCH_BYTES.get(key)
+    if sb is None:
+        sb = _SCRATCH_BYTES[key] = int(lib.rdx_plan_scratch_bytes(n, b))
+    scratch = _WORKSPACE.get(dev, sb)
     flags = _native.RDX_PLAN_ALLOW_EMPTY if allow_empty else 0
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
-    info = _info_buffer()
-    iv = info.numpy()
+    sh = (stream.cuda_stream if stream is not None else
+          torch._C._cuda_getCurrentRawStream(dev.index if dev.index is not None else torch.cuda.current_device()))
+    info, iv = _info_buffer()
     iv[1] = -1  # status sentinel: a kernel that never ran cannot leave a stale RDX_OK behind
     p0 = buf.data_ptr()
     code = lib.rdx_plan_build(
         tok.data_ptr(), pos.data_ptr(), cu.data_ptr(), b, n, flags,
-        p0, p0 + 4 * nn, p0 + 8 * nn, cu_q.data_ptr(), lcp.data_ptr(), info.data_ptr(),
-        scratch.data_ptr(), ctypes.c_size_t(scratch.numel()), st.cuda_stream,
+        p0, p0 + 4 * nn, p0 + 8 * nn, p0 + 4 * o, p0 + 4 * (o + b + 1), info.data_ptr(),
+        scratch.data_ptr(), ctypes.c_size_t(scratch.numel()), sh,
     )
     _native.check(code, "rdx_plan_build")
-    st.synchronize()  # the one host wait: the kernel's (N', status, attempts, max_q) are in `info`
+    # the one host wait (GIL released in the ctypes call): (N', status, attempts, max_q) are in `info`
+    _native.check(lib.rdx_stream_synchronize(sh), "rdx_stream_synchronize")
     n_compact, status, attempts, max_q = (int(x) for x in iv)
+    cu_q, lcp = buf[o:o + b + 1], buf[o + b + 1:]
     if status == -1:
         raise NativeLibraryError("rdx_plan_build: the planner kernel did not report a status")
     raise_for_status(status, "rdx_plan_build")

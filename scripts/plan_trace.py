@@ -13,8 +13,11 @@ from paper_2601_15013_b200.plan import build_plan_device, upload_batch  # noqa: 
 lib = _native.lib()
 buf = torch.zeros(64, dtype=torch.int64, device="cuda")
 names = ["start", "staged", "B1", "P0", "B2", "P2", "B3", "P3", "B4", "P4", "P5", "end"]
-for name in ("c2", "c3"):
-    b = bench.workload(name, 1, "weak")[2]
+from paper_2601_15013_b200.workloads import prefix_ratio_batch  # noqa: E402
+
+cases = [(name, bench.workload(name, 1, "weak")[2]) for name in ("c2", "c3")]
+cases += [(f"{n // 1024}K", prefix_ratio_batch(n, 0.5)) for n in (1024, 4096)]
+for name, b in cases:
     tok, pos, cu = upload_batch(b)
     for _ in range(5):
         build_plan_device(tok, pos, cu)
