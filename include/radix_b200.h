@@ -314,6 +314,10 @@ int rdx_gemm_debug_tail_split(int on);
  * the number of column tiles the last launch used (0 = no partition). */
 int rdx_gemm_debug_colpart(int on);
 
+/* Debug (stats builds, -DRDX_NORM_STATS_BUILD): per-block [entry, exit]
+ * %globaltimer of the last rdx_rmsnorm_rows_after launch (n_blocks <= 4096). */
+int rdx_norm_debug_times(unsigned long long* host, int n_blocks);
+
 /* Debug: pin the GEMM tile shape (cg = 1 or 2 CTAs, block_n = 128 or 256) for
  * later launches, or cg = 0 for the automatic choice (A/B experiments; the
  * RDX_GEMM_SHAPE="cg,bn" environment variable sets the same override). */

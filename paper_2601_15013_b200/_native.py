@@ -46,6 +46,7 @@ EXPORTS = (
     "rdx_gemm_debug_pair",
     "rdx_gemm_debug_tail_split",
     "rdx_gemm_debug_colpart",
+    "rdx_norm_debug_times",
     "rdx_gemm_debug_stats",
     "rdx_gemm_debug_shape",
     "rdx_gemm_debug_group_m",
@@ -147,6 +148,7 @@ _SIGNATURES = {
     "rdx_gemm_pair": (ctypes.c_int, [ctypes.POINTER(GemmArgs), ctypes.POINTER(GemmArgs), _vp, _vp]),
     "rdx_gemm_debug_tail_split": (ctypes.c_int, [ctypes.c_int]),
     "rdx_gemm_debug_colpart": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_norm_debug_times": (ctypes.c_int, [_vp, ctypes.c_int]),
     "rdx_gemm_debug_pair": (ctypes.c_int, [ctypes.c_int]),
     "rdx_plan_debug_smem": (ctypes.c_int, [ctypes.c_int]),
     "rdx_attention_debug_bk64": (ctypes.c_int, [ctypes.c_int]),

@@ -275,6 +275,10 @@ rmsnorm_rows_pipe_kernel(const float* __restrict__ x, int64_t ld_x, const uint32
 // as they become ready; the launch trigger fires at entry so that consumer can launch
 // (its CTAs start as the producing GEMM's CTAs exit).  The chained grid is one small
 // block per SM whose registers fit beside a GEMM CTA (see rdx_rmsnorm_rows_after).
+#ifdef RDX_NORM_STATS_BUILD
+__device__ unsigned long long g_norm_times[2 * 4096];  // per block: %globaltimer at entry / exit
+#endif
+
 template <int V, int W>
 __global__ void __launch_bounds__(W * 32)
 rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_rows, const float* __restrict__ w,
@@ -283,6 +287,11 @@ rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_r
   constexpr int D = 128 * V;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (ready_ctr) pdl_launch_dependents();
+#ifdef RDX_NORM_STATS_BUILD
+  unsigned long long t_in;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_in));
+  if (threadIdx.x == 0 && blockIdx.x < 4096) g_norm_times[2 * blockIdx.x] = t_in;
+#endif
   // A block takes W consecutive rows (one per warp) per step.  One thread polls
   // their slab counters (acquire, backing off) so waiting blocks add almost no L2
   // traffic.  No cross-step prefetch: a block must not wait on a later, unfinished
@@ -333,6 +342,14 @@ rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_r
       }
     }
   }
+#ifdef RDX_NORM_STATS_BUILD
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned long long t_out;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_out));
+    g_norm_times[2 * blockIdx.x + 1] = t_out;
+  }
+#endif
 }
 
 // blocked = 0: table[j][i]; blocked = 1: the QKV epilogue's lane-coalesced layout
@@ -604,3 +621,17 @@ extern "C" int rdx_rerank_scores(const float* logits, int64_t n_rows, int64_t ld
 }
 
 int rdx::take_device_status_rowops(int* out, cudaStream_t st) { return take_device_status(out, st); }
+
+// Debug (-DRDX_NORM_STATS_BUILD): per-block [entry, exit] %globaltimer of the last
+// rdx_rmsnorm_rows_after launch, n_blocks <= 4096 entries.
+extern "C" int rdx_norm_debug_times(unsigned long long* host, int n_blocks) {
+#ifdef RDX_NORM_STATS_BUILD
+  if (!host || n_blocks <= 0 || n_blocks > 4096) return RDX_ERR_INVALID_ARGUMENT;
+  RDX_CUDA_TRY(cudaMemcpyFromSymbol(host, rdx::g_norm_times, 2 * n_blocks * sizeof(unsigned long long)));
+  return RDX_OK;
+#else
+  (void)host;
+  (void)n_blocks;
+  return RDX_ERR_UNSUPPORTED;
+#endif
+}
