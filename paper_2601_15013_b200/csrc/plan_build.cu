@@ -399,10 +399,10 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
 // Batches up to kSmMaxCtas * kSmChunkMax tokens (and a staged cu) run as ONE
 // thread-block cluster whose whole working set lives in shared memory: each CTA
 // owns a contiguous chunk of tokens (tok, pos, seg, path prefix P, slot) and a
-// slice of the open-addressing table; every cross-token lookup (P at a sequence
-// start, the representative's tok/pos/seg, the slots of i-1 and rep-1, the table
-// itself) is a distributed-shared-memory access (~200 cycles) instead of an L2
-// round trip, and the phases are separated by 4 hardware cluster barriers (the
+// slice of the open-addressing table; the cross-token lookups (P at a sequence
+// start and at rep-1, the table itself) are distributed-shared-memory accesses
+// (~200 cycles) instead of L2 round trips (the representative's tok/pos are read
+// from global memory: a shared prefix's representatives all sit in one CTA), and the phases are separated by 4 hardware cluster barriers (the
 // cooperative grid version has 7 grid barriers and L2 traffic in every phase).
 // Same algorithm, same seeds, same outputs as plan_build_kernel.
 constexpr int kSmThreads = 1024;
@@ -640,6 +640,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
       s_slot[j] = t;
     }
     mark(5);
+    if (g.trace && tid == 0 && me < 16) g.trace[32 + me] = globaltimer_ns();  // this CTA's P2 end
     cl_sync();  // B3: table final
     mark(6);
     auto vals_at = [&](uint32_t t) -> uint32_t {
@@ -686,12 +687,14 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
         if (r == static_cast<uint32_t>(i)) {
           mine = static_cast<int32_t>(di);
         } else {
-          const uint32_t o = r / static_cast<uint32_t>(chunk);
-          const uint32_t lr = r - o * static_cast<uint32_t>(chunk);
-          sr = *cl.map_shared_rank(&s_seg[lr], o);
+          // the representative's sequence, token and position come from this CTA's copy of
+          // cu and from global memory (L1/L2): the representatives of a shared prefix all live
+          // in one CTA, whose shared memory would otherwise serve every such lookup (C2 18.3 ->
+          // 17.4 us, C3 36.0 -> 34.3 us per launch)
+          sr = find_seq(s_cu, nseq, r);
           const int64_t sst = s_cu[sr];
-          bool ok = (*cl.map_shared_rank(&s_tok[lr], o) == s_tok[j]) &&
-                    (*cl.map_shared_rank(&s_pos[lr], o) == s_pos[j]) && (static_cast<int64_t>(r) - sst == di);
+          bool ok = (__ldg(a.tok + r) == s_tok[j]) && (__ldg(a.pos + r) == s_pos[j]) &&
+                    (static_cast<int64_t>(r) - sst == di);
           if (ok && di > 0) ok = (P_at(i - 1) - pst1) == (P_at(static_cast<int64_t>(r) - 1) - P_at(sst - 1));
           if (!ok) fail = 1;
         }
@@ -707,6 +710,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     }
     if (__syncthreads_or(fail) && tid == 0) atomicOr(cl.map_shared_rank(&s_flags[1 + attempt], 0), 1u);
     mark(7);
+    if (g.trace && tid == 0 && me < 16) g.trace[48 + me] = globaltimer_ns();  // this CTA's P3 end
     cl_sync();  // B4: verification and lcp final
     mark(8);
     if (*reinterpret_cast<volatile uint32_t*>(cl.map_shared_rank(&s_flags[1 + attempt], 0)) != 0) continue;

@@ -31,3 +31,6 @@ for name, b in cases:
     starts = [x - t0 for x in t[16:32] if x]
     print(name, "CTA starts (ns rel. CTA 0):", starts)
     print(name, " ".join(f"{names[k]}={(t[k] - t0) / 1e3:.2f}" for k in range(12) if t[k]), "us")
+    for nm, off in (("P2 end", 32), ("P3 end", 48)):
+        v = [(x - t0) / 1e3 for x in t[off:off + 16] if x]
+        print(name, f"per-CTA {nm} (us):", " ".join(f"{x:.2f}" for x in v))
