@@ -500,26 +500,45 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
   if (tid == 0) s_vmax = 0;
   __syncthreads();
   {
+    // every CTA validates the whole staged cu itself (<= 8192 entries): no shared-memory
+    // traffic between CTAs before the first cluster barrier
     uint32_t bits = 0;  // bit0 start!=0, bit1 decrease, bit2 empty, bit3 end!=n
-    if (me == 0 && tid == 0) {
+    if (tid == 0) {
       if (s_cu[0] != 0) bits |= 1u;
       if (s_cu[nseq] != n) bits |= 8u;
     }
-    for (int64_t q = static_cast<int64_t>(me) * kSmThreads + tid; q < nseq; q += static_cast<int64_t>(C) * kSmThreads) {
+    for (int64_t q = tid; q < nseq; q += kSmThreads) {
       const int64_t d = s_cu[q + 1] - s_cu[q];
       if (d < 0) bits |= 2u;
       if (d == 0 && !(a.flags & RDX_PLAN_ALLOW_EMPTY)) bits |= 4u;
     }
     bits = __reduce_or_sync(0xffffffffu, bits);
-    if (bits && (tid & 31) == 0) atomicOr(cl.map_shared_rank(&s_flags[0], 0), bits);
+    if (bits && (tid & 31) == 0) atomicOr(&s_flags[0], bits);
   }
   if (me == 0)
     for (int64_t q = tid; q < nseq; q += kSmThreads) s_lcp[q] = static_cast<int32_t>(s_cu[q + 1] - s_cu[q]);
+  // independent of the other CTAs, so done before B1: the first attempt's table clear and
+  // the sequence of each own token (a contiguous run per thread, found once; garbage
+  // but bounded when cu is invalid, in which case the kernel leaves after B1)
+  for (int64_t t = tid; t < g.tslots; t += kSmThreads) {
+    s_keys[t] = 0ULL;
+    s_vals[t] = 0xFFFFFFFFu;
+  }
+  const int per = static_cast<int>((cnt + kSmThreads - 1) / kSmThreads);
+  const int64_t j0 = static_cast<int64_t>(tid) * per;
+  if (j0 < cnt) {
+    uint32_t sq = find_seq(s_cu, nseq, lo + j0);
+    for (int u = 0; u < per && j0 + u < cnt; ++u) {
+      const int64_t i = lo + j0 + u;
+      while (sq + 1 < nseq && s_cu[sq + 1] <= i) ++sq;
+      s_seg[j0 + u] = sq;
+    }
+  }
   mark(1);
   cl_sync();  // B1
   mark(2);
   {
-    const uint32_t bits = *reinterpret_cast<volatile uint32_t*>(cl.map_shared_rank(&s_flags[0], 0));
+    const uint32_t bits = s_flags[0];  // this CTA's own verdict on the whole cu
     if (bits) {
       if (me == 0 && tid == 0) {
         a.info[0] = 0;
@@ -533,25 +552,14 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
       return;
     }
   }
-  // seq of each own token: contiguous run per thread, found once
-  const int per = static_cast<int>((cnt + kSmThreads - 1) / kSmThreads);
-  const int64_t j0 = static_cast<int64_t>(tid) * per;
-  if (j0 < cnt) {
-    uint32_t sq = find_seq(s_cu, nseq, lo + j0);
-    for (int u = 0; u < per && j0 + u < cnt; ++u) {
-      const int64_t i = lo + j0 + u;
-      while (sq + 1 < nseq && s_cu[sq + 1] <= i) ++sq;
-      s_seg[j0 + u] = sq;
-    }
-  }
-
   for (int attempt = 0; attempt < kMaxAttempts; ++attempt) {
     const uint64_t seed = 0x243F6A8885A308D3ULL * static_cast<uint64_t>(2 * attempt + 1) + 0x13198A2E03707344ULL;
-    // ---- P0: clear the table slice; per-token elements; chunk-local inclusive scan ----
-    for (int64_t t = tid; t < g.tslots; t += kSmThreads) {
-      s_keys[t] = 0ULL;
-      s_vals[t] = 0xFFFFFFFFu;
-    }
+    // ---- P0: clear the table slice (retries); per-token elements; chunk-local inclusive scan ----
+    if (attempt > 0)
+      for (int64_t t = tid; t < g.tslots; t += kSmThreads) {
+        s_keys[t] = 0ULL;
+        s_vals[t] = 0xFFFFFFFFu;
+      }
     if (me == 0 && attempt > 0)
       for (int64_t q = tid; q < nseq; q += kSmThreads) s_lcp[q] = static_cast<int32_t>(s_cu[q + 1] - s_cu[q]);
     {
