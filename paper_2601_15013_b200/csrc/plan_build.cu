@@ -416,7 +416,7 @@ struct SmGeom {
   int64_t chunk;   // tokens per CTA
   int64_t tslots;  // hash slots per CTA
   int64_t tsize;   // tslots * cluster size
-  uint32_t off_P, off_slot, off_seg, off_tok, off_pos, off_keys, off_vals, off_lcp, off_cuq;
+  uint32_t off_P, off_slot, off_seg, off_tok, off_pos, off_keys, off_lcp, off_cuq;
   uint32_t bytes;
   unsigned long long* trace;  // debug (rdx_plan_debug_trace): phase timestamps of CTA 0, start of every CTA
 };
@@ -470,7 +470,6 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
   uint32_t* s_tok = reinterpret_cast<uint32_t*>(sm + g.off_tok);
   uint32_t* s_pos = reinterpret_cast<uint32_t*>(sm + g.off_pos);
   unsigned long long* s_keys = reinterpret_cast<unsigned long long*>(sm + g.off_keys);
-  uint32_t* s_vals = reinterpret_cast<uint32_t*>(sm + g.off_vals);
   int32_t* s_lcp = reinterpret_cast<int32_t*>(sm + g.off_lcp);
   int32_t* s_cuq = reinterpret_cast<int32_t*>(sm + g.off_cuq);
   __shared__ uint64_t s_wtot[kSmWarps];
@@ -520,10 +519,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
   // independent of the other CTAs, so done before B1: the first attempt's table clear and
   // the sequence of each own token (a contiguous run per thread, found once; garbage
   // but bounded when cu is invalid, in which case the kernel leaves after B1)
-  for (int64_t t = tid; t < g.tslots; t += kSmThreads) {
-    s_keys[t] = 0ULL;
-    s_vals[t] = 0xFFFFFFFFu;
-  }
+  for (int64_t t = tid; t < g.tslots; t += kSmThreads) s_keys[t] = 0ULL;
   const int per = static_cast<int>((cnt + kSmThreads - 1) / kSmThreads);
   const int64_t j0 = static_cast<int64_t>(tid) * per;
   if (j0 < cnt) {
@@ -556,10 +552,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     const uint64_t seed = 0x243F6A8885A308D3ULL * static_cast<uint64_t>(2 * attempt + 1) + 0x13198A2E03707344ULL;
     // ---- P0: clear the table slice (retries); per-token elements; chunk-local inclusive scan ----
     if (attempt > 0)
-      for (int64_t t = tid; t < g.tslots; t += kSmThreads) {
-        s_keys[t] = 0ULL;
-        s_vals[t] = 0xFFFFFFFFu;
-      }
+      for (int64_t t = tid; t < g.tslots; t += kSmThreads) s_keys[t] = 0ULL;
     if (me == 0 && attempt > 0)
       for (int64_t q = tid; q < nseq; q += kSmThreads) s_lcp[q] = static_cast<int32_t>(s_cu[q + 1] - s_cu[q]);
     {
@@ -613,6 +606,15 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
       const uint64_t k = fmix64(h ^ seed);
       return k == 0 ? 1ULL : k;
     };
+    // A slot is one 64-bit word: the key's top 48 bits (nonzero) over the 16-bit index of
+    // the path's first token (cluster batches have <= 65536 tokens).  Claiming an empty
+    // slot is one CAS, a repeated key one 64-bit atomicMin (equal high bits: min index),
+    // and a lookup one load.  Two paths sharing 48 key bits share a slot; the inductive
+    // verification catches that like any other collision (retry with a new seed).
+    auto tag_of = [&](unsigned long long key) -> unsigned long long {
+      const unsigned long long k48 = key >> 16;
+      return k48 == 0 ? 1ULL : k48;
+    };
     const uint32_t tsl = static_cast<uint32_t>(g.tslots), tsz = static_cast<uint32_t>(g.tsize);
     auto home = [&](unsigned long long key) -> uint32_t { return static_cast<uint32_t>(__umul64hi(key, tsz)); };
 
@@ -633,13 +635,23 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
       }
       uint32_t t = 0xFFFFFFFFu;
       if (insert) {
-        const unsigned long long key = key_of(h);
+        const unsigned long long key = key_of(h), tag = tag_of(key);
+        const unsigned long long word = (tag << 16) | static_cast<unsigned long long>(i);
         t = home(key);
         while (true) {
           const uint32_t o = t / tsl, lt = t - o * tsl;
-          const unsigned long long prev = atomicCAS(cl.map_shared_rank(&s_keys[lt], o), 0ULL, key);
-          if (prev == 0ULL || prev == key) {
-            atomicMin(cl.map_shared_rank(&s_vals[lt], o), static_cast<uint32_t>(i));
+          unsigned long long* slot = cl.map_shared_rank(&s_keys[lt], o);
+          const unsigned long long prev = atomicCAS(slot, 0ULL, word);
+          if (prev == 0ULL) break;
+          if ((prev >> 16) == tag) {
+            // min index by CAS: a 64-bit atomicMin through the cluster-mapped pointer gave
+            // wrong minima here (tests/test_plan_gpu.py::test_multilevel_trie_vs_oracle)
+            unsigned long long cur = prev;
+            while (word < cur) {
+              const unsigned long long got = atomicCAS(slot, cur, word);
+              if (got == cur) break;
+              cur = got;
+            }
             break;
           }
           t = t + 1 == tsz ? 0 : t + 1;
@@ -651,9 +663,9 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     if (g.trace && tid == 0 && me < 16) g.trace[32 + me] = globaltimer_ns();  // this CTA's P2 end
     cl_sync();  // B3: table final
     mark(6);
-    auto vals_at = [&](uint32_t t) -> uint32_t {
+    auto slot_at = [&](uint32_t t) -> unsigned long long {
       const uint32_t o = t / tsl;
-      return *cl.map_shared_rank(&s_vals[t - o * tsl], o);
+      return *cl.map_shared_rank(&s_keys[t - o * tsl], o);
     };
 
     // ---- P3: representatives (table lookups), inductive verification, lcp ----
@@ -675,14 +687,16 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
         const uint64_t pst1 = P_at(st - 1);
         uint32_t t = s_slot[j];
         bool lost = false;
-        if (t == 0xFFFFFFFFu) {  // not inserted: find the key
-          const unsigned long long key = key_of(s_P[j] + s_carry[me] - pst1);
+        unsigned long long w;
+        if (t != 0xFFFFFFFFu) {
+          w = slot_at(t);
+        } else {  // not inserted: find the key
+          const unsigned long long key = key_of(s_P[j] + s_carry[me] - pst1), tag = tag_of(key);
           t = home(key);
           while (true) {
-            const uint32_t o = t / tsl;
-            const unsigned long long k = *cl.map_shared_rank(&s_keys[t - o * tsl], o);
-            if (k == key) break;
-            if (k == 0ULL) {  // cannot happen unless hashes collided: retry with a new seed
+            w = slot_at(t);
+            if ((w >> 16) == tag) break;
+            if (w == 0ULL) {  // cannot happen unless hashes collided: retry with a new seed
               lost = true;
               break;
             }
@@ -690,7 +704,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
           }
         }
         if (lost) fail = 1;
-        r = lost ? static_cast<uint32_t>(i) : vals_at(t);
+        r = lost ? static_cast<uint32_t>(i) : static_cast<uint32_t>(w & 0xFFFFu);
         sr = si;
         if (r == static_cast<uint32_t>(i)) {
           mine = static_cast<int32_t>(di);
@@ -797,7 +811,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
 // Shared-memory geometry of the cluster planner for (n, nseq) on `ctas` CTAs; false
 // when it does not fit (the cooperative grid kernel takes the batch).
 bool sm_geometry(int64_t n, int64_t nseq, int ctas, SmGeom* g) {
-  if (ctas < 1 || nseq + 1 > 8192) return false;
+  if (ctas < 1 || nseq + 1 > 8192 || n > 65536) return false;  // 16-bit token indices in the slots
   const int64_t chunk = (n + ctas - 1) / ctas;
   if (chunk > kSmChunkMax) return false;
   int64_t tslots = (2 * n + ctas - 1) / ctas;
@@ -815,7 +829,6 @@ bool sm_geometry(int64_t n, int64_t nseq, int ctas, SmGeom* g) {
   g->off_seg = take(4 * static_cast<size_t>(chunk));
   g->off_tok = take(4 * static_cast<size_t>(chunk));
   g->off_pos = take(4 * static_cast<size_t>(chunk));
-  g->off_vals = take(4 * static_cast<size_t>(tslots));
   g->off_lcp = take(4 * static_cast<size_t>(nseq > 0 ? nseq : 1));
   g->off_cuq = take(4 * static_cast<size_t>(nseq + 1));
   g->bytes = static_cast<uint32_t>(off);
