@@ -191,16 +191,18 @@ def build_plan_device(tok, pos, cu, *, allow_empty: bool = False, stream=None,
     # the one host wait (GIL released in the ctypes call): (N', status, attempts, max_q) are in `info`
     _native.check(lib.rdx_stream_synchronize(sh), "rdx_stream_synchronize")
     n_compact, status, attempts, max_q = (int(x) for x in iv)
-    cu_q, lcp = buf[o:o + b + 1], buf[o + b + 1:]
     if status == -1:
         raise NativeLibraryError("rdx_plan_build: the planner kernel did not report a status")
     raise_for_status(status, "rdx_plan_build")
+    # every view in one call (five separate slices cost ~13 us of host time at C2)
+    gather, _, scatter, _, cpos, _, cu_q, lcp = buf.split(
+        [n_compact, nn - n_compact, n, nn - n, n_compact, nn - n_compact, b + 1, nb])
     return DevicePlan(
-        gather=buf[:n_compact],
-        scatter=buf[nn:nn + n],
-        compact_positions=buf[2 * nn:2 * nn + n_compact],
+        gather=gather,
+        scatter=scatter,
+        compact_positions=cpos,
         cu_q=cu_q,
-        lcp=lcp[:b],
+        lcp=lcp if b else lcp[:0],
         n_original=n,
         n_compact=n_compact,
         attempts=attempts,
