@@ -318,6 +318,14 @@ int rdx_gemm_debug_colpart(int on);
  * %globaltimer of the last rdx_rmsnorm_rows_after launch (n_blocks <= 4096). */
 int rdx_norm_debug_times(unsigned long long* host, int n_blocks);
 
+/* Debug: warps per block (4 or 8, default 4) of later rdx_rmsnorm_rows_after
+ * launches without ready_ctr; 4-warp blocks fit beside a GEMM CTA. */
+int rdx_norm_debug_warps(int w);
+
+/* Debug: longest nanosleep (64..16384 ns, default 2048) of the rdx_rmsnorm_rows_after
+ * slab pollers, read by the kernel at run time. */
+int rdx_norm_debug_backoff(unsigned ns);
+
 /* Debug: pin the GEMM tile shape (cg = 1 or 2 CTAs, block_n = 128 or 256) for
  * later launches, or cg = 0 for the automatic choice (A/B experiments; the
  * RDX_GEMM_SHAPE="cg,bn" environment variable sets the same override). */

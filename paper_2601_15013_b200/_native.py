@@ -47,6 +47,8 @@ EXPORTS = (
     "rdx_gemm_debug_tail_split",
     "rdx_gemm_debug_colpart",
     "rdx_norm_debug_times",
+    "rdx_norm_debug_warps",
+    "rdx_norm_debug_backoff",
     "rdx_gemm_debug_stats",
     "rdx_gemm_debug_shape",
     "rdx_gemm_debug_group_m",
@@ -149,6 +151,8 @@ _SIGNATURES = {
     "rdx_gemm_debug_tail_split": (ctypes.c_int, [ctypes.c_int]),
     "rdx_gemm_debug_colpart": (ctypes.c_int, [ctypes.c_int]),
     "rdx_norm_debug_times": (ctypes.c_int, [_vp, ctypes.c_int]),
+    "rdx_norm_debug_warps": (ctypes.c_int, [ctypes.c_int]),
+    "rdx_norm_debug_backoff": (ctypes.c_int, [ctypes.c_uint]),
     "rdx_gemm_debug_pair": (ctypes.c_int, [ctypes.c_int]),
     "rdx_plan_debug_smem": (ctypes.c_int, [ctypes.c_int]),
     "rdx_attention_debug_bk64": (ctypes.c_int, [ctypes.c_int]),

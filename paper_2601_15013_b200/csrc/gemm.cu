@@ -124,8 +124,10 @@ struct Cfg {
   // RESID_NORM warps stage two fp32 boxes (h in/out) and two bf16 boxes (hb out)
   static constexpr int EPI_WARP_BYTES = EPI == RDX_EPI_RESID_NORM ? 2 * kEpiBoxBytes + 2 * 2048 : 2 * kEpiBoxBytes;
   static constexpr int EPI_BYTES = kEpiWarps * EPI_WARP_BYTES;
-  // q/k-norm weights (2 x 128 fp32); QKV adds the RoPE inverse frequencies (64 x (hi, lo) fp32)
-  static constexpr int AUX_BYTES = EPI == RDX_EPI_QKV ? 1536 : 1024;
+  // QKV only: q/k-norm weights (2 x 128 fp32) and the RoPE inverse frequencies (64 x (hi, lo)
+  // fp32).  Other epilogues keep none, which leaves an SM room for a small rmsnorm block
+  // beside the GEMM CTA (its 1 KB per-block reservation included).
+  static constexpr int AUX_BYTES = EPI == RDX_EPI_QKV ? 1536 : 0;
   static constexpr int BAR_BYTES = 512;
   static constexpr int BUDGET = 227 * 1024 - 1024 - BAR_BYTES - EPI_BYTES - AUX_BYTES;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);

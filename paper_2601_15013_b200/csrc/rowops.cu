@@ -268,6 +268,7 @@ rmsnorm_rows_pipe_kernel(const float* __restrict__ x, int64_t ld_x, const uint32
 #ifndef RDX_NORM_BACKOFF_MAX
 #define RDX_NORM_BACKOFF_MAX 2048  // ns: the slab poller's longest nanosleep
 #endif
+__device__ unsigned g_norm_backoff_max = RDX_NORM_BACKOFF_MAX;  // rdx_norm_debug_backoff
 
 // W warps per block, one row per warp per step.  ready_ctr != NULL (the chained mode):
 // after each step the block publishes its W finished rows on ready_ctr[slab] (release),
@@ -301,10 +302,11 @@ rmsnorm_rows_after_kernel(const float* __restrict__ x, int64_t ld_x, int64_t n_r
       const int64_t last = base + W - 1 < n_rows ? base + W - 1 : n_rows - 1;
       for (int64_t slab = base >> 5; slab <= (last >> 5); ++slab) {
         unsigned ns = 128;
+        const unsigned ns_max = g_norm_backoff_max;
         uint32_t spins = 0;
         while (ld_acquire_u32(done_ctr + slab) < target) {
           __nanosleep(ns);
-          ns = ns < RDX_NORM_BACKOFF_MAX ? 2 * ns : ns;
+          ns = ns < ns_max ? 2 * ns : ns;
           if (++spins > (1u << 22)) {  // ~8 s: the producing GEMM never completed this slab
             atomicCAS(&g_device_status, 0, static_cast<int>(RDX_ERR_DEVICE_TIMEOUT));  // reported by rdx_device_status
             break;
@@ -515,6 +517,12 @@ extern "C" int rdx_rmsnorm_rows(const float* x, int64_t ld_x, const uint32_t* ro
 
 namespace rdx {
 namespace {
+// Warps per block of the (non-chained) rmsnorm_rows_after grid (rdx_norm_debug_warps).  4:
+// a 128-thread block fits beside a GEMM CTA (registers; the non-QKV GEMMs leave the shared
+// memory for its reservation), so more of the grid is resident before the GEMM exits
+// (C2 +0.2-0.3 %, C3 +0.7 %, C4 +0.2 % over 8-warp blocks, scripts/ab_graph.py normw).
+int g_norm_warps = 4;
+
 template <int V, int W>
 cudaError_t launch_norm_after(cudaLaunchConfig_t& cfg, const float* x, int64_t ld_x, int64_t n_rows, const float* w,
                               float eps, __nv_bfloat16* o, int64_t ld_out, const uint32_t* done_ctr, uint32_t target,
@@ -543,8 +551,9 @@ extern "C" int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_ro
     return v && v[0] == '1' ? 1 : 0;
   }();
   const bool small = ready_ctr && chain_grid;
+  const bool w4 = !small && g_norm_warps == 4;
   cfg.gridDim = dim3(static_cast<unsigned>(small ? (n_rows < num_sms() ? n_rows : num_sms())
-                                                 : grid_for_rows(n_rows, 8)));
+                                                 : grid_for_rows(n_rows, w4 ? 4 : 8)));
   cfg.stream = as_stream(stream);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // always: it overlaps the GEMM's tail
@@ -557,7 +566,8 @@ extern "C" int rdx_rmsnorm_rows_after(const float* x, int64_t ld_x, int64_t n_ro
   cfg.numAttrs = 1;
   cudaError_t e;
 #define RDX_NA(V, WCH) (small ? launch_norm_after<V, WCH>(cfg, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target, ready_ctr) \
-                              : launch_norm_after<V, 8>(cfg, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target, ready_ctr))
+                              : w4 ? launch_norm_after<V, 4>(cfg, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target, ready_ctr) \
+                                   : launch_norm_after<V, 8>(cfg, x, ld_x, n_rows, w, eps, o, ld_out, done_ctr, target, ready_ctr))
   switch (d) {
     case 256: e = RDX_NA(2, 8); break;
     case 512: e = RDX_NA(4, 8); break;
@@ -621,6 +631,21 @@ extern "C" int rdx_rerank_scores(const float* logits, int64_t n_rows, int64_t ld
 }
 
 int rdx::take_device_status_rowops(int* out, cudaStream_t st) { return take_device_status(out, st); }
+
+// Debug: longest nanosleep (ns, 64..16384) of the rmsnorm_rows_after slab pollers; read by
+// the kernel at run time (graph replays included).
+extern "C" int rdx_norm_debug_backoff(unsigned ns) {
+  if (ns < 64 || ns > 16384) return RDX_ERR_INVALID_ARGUMENT;
+  RDX_CUDA_TRY(cudaMemcpyToSymbol(rdx::g_norm_backoff_max, &ns, sizeof(ns)));
+  return RDX_OK;
+}
+
+// Debug: warps per block of the plain rmsnorm_rows_after grid (4 or 8; read at launch).
+extern "C" int rdx_norm_debug_warps(int w) {
+  if (w != 4 && w != 8) return RDX_ERR_INVALID_ARGUMENT;
+  rdx::g_norm_warps = w;
+  return RDX_OK;
+}
 
 // Debug (-DRDX_NORM_STATS_BUILD): per-block [entry, exit] %globaltimer of the last
 // rdx_rmsnorm_rows_after launch, n_blocks <= 4096 entries.

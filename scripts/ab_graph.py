@@ -27,6 +27,12 @@ elif what == "pair":  # gate|up + down as one launch (rdx_gemm_pair) vs two laun
 elif what == "chain":  # model-level switch: norm -> next GEMM chained on ready counters
     def setter(on):
         os.environ["RDX_NORM_CHAIN"] = str(on)
+elif what == "normw":  # rmsnorm_rows_after blocks of 4 warps (fit beside a GEMM CTA) vs 8
+    def setter(on):
+        lib.rdx_norm_debug_warps(4 if on else 8)
+elif what == "backoff":  # norm slab-poller backoff cap B_ON vs B_OFF ns (device variable: set per replay)
+    def setter(on):
+        lib.rdx_norm_debug_backoff(int(os.environ.get("B_ON", "512") if on else os.environ.get("B_OFF", "2048")))
 elif what == "colpart":  # GEMM column partition of few-round launches
     setter = lib.rdx_gemm_debug_colpart
 else:
@@ -47,6 +53,8 @@ res = {1: [], 0: []}
 for it in range(int(os.environ.get("AB_ITERS", "20"))):
     for on in (1, 0):
         flush()
+        if what == "backoff":
+            setter(on)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         arms[on].score_device(db)

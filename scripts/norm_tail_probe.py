@@ -1,6 +1,6 @@
 """Where the exposed rmsnorm tail goes (stats build: RDX_LIB_VARIANT=nstats): the C2 o_proj GEMM
 with slab counters + rdx_rmsnorm_rows_after, %globaltimer landmarks of the GEMM and per-block
-entry/exit of the norm, relative to the GEMM's last CTA exit."""
+entry/exit of the norm, relative to the GEMM's last CTA exit.  NORM_W=4|8: warps per norm block."""
 import ctypes
 import os
 import sys
@@ -26,7 +26,9 @@ args = _native.GemmArgs()
 args.a, args.b, args.m, args.n, args.k = a.data_ptr(), w.data_ptr(), M, d, K
 args.lda, args.ldb, args.epi, args.out, args.ldo = K, K, _native.EPI_RESID_F32, h.data_ptr(), d
 args.done_ctr = ctr.data_ptr()
-nb = -(-M // 8)
+W = int(os.environ.get("NORM_W", "8"))  # warps per norm block (rdx_norm_debug_warps)
+_native.check(lib.rdx_norm_debug_warps(W), "warps")
+nb = min(-(-M // W), 4096)
 for it in range(4):
     ctr.zero_()
     torch.cuda.synchronize()
