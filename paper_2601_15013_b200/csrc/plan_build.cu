@@ -427,8 +427,15 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+// Phase barrier of the cluster planner; the one-CTA instance (batches <= 1024 tokens)
+// only needs its block barrier.
+template <bool kOne>
 __device__ __forceinline__ void cl_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if constexpr (kOne) {
+    __syncthreads();
+  } else {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
 }
 
 template <int NW>
@@ -458,6 +465,8 @@ __device__ uint64_t block_exclusive_scan_u64_w(uint64_t v, uint64_t* warp_tot, u
   return warp_prefix + x - v;
 }
 
+// kOne: the single-CTA instance, every access local (no DSMEM mapping, block barriers).
+template <bool kOne>
 __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs a, SmGeom g) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks());
@@ -531,7 +540,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     }
   }
   mark(1);
-  cl_sync();  // B1
+  cl_sync<kOne>();  // B1
   mark(2);
   {
     const uint32_t bits = s_flags[0];  // this CTA's own verdict on the whole cu
@@ -544,7 +553,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
         a.info[2] = 0;
         a.info[3] = 0;
       }
-      cl_sync();  // nobody leaves while another CTA may still read CTA 0's flag
+      cl_sync<kOne>();  // nobody leaves while another CTA may still use this one's shared memory
       return;
     }
   }
@@ -581,9 +590,9 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
       if (tid == 0) s_total = tot;
     }
     mark(3);
-    cl_sync();  // B2: chunk prefixes and totals visible, tables clear
+    cl_sync<kOne>();  // B2: chunk prefixes and totals visible, tables clear
     mark(4);
-    if (tid < C) s_carry[tid] = *cl.map_shared_rank(&s_total, tid);
+    if (tid < C) s_carry[tid] = kOne ? s_total : *cl.map_shared_rank(&s_total, tid);
     __syncthreads();
     if (tid == 0) {
       uint64_t acc = 0;
@@ -600,7 +609,8 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     auto P_at = [&](int64_t x) -> uint64_t {
       if (x < 0) return 0ULL;
       const uint32_t o = static_cast<uint32_t>(x) / static_cast<uint32_t>(chunk);
-      return *cl.map_shared_rank(&s_P[static_cast<uint32_t>(x) - o * static_cast<uint32_t>(chunk)], o) + s_carry[o];
+      const uint32_t lx = static_cast<uint32_t>(x) - o * static_cast<uint32_t>(chunk);
+      return (kOne ? s_P[lx] : *cl.map_shared_rank(&s_P[lx], o)) + s_carry[o];
     };
     auto key_of = [&](uint64_t h) -> unsigned long long {
       const uint64_t k = fmix64(h ^ seed);
@@ -640,7 +650,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
         t = home(key);
         while (true) {
           const uint32_t o = t / tsl, lt = t - o * tsl;
-          unsigned long long* slot = cl.map_shared_rank(&s_keys[lt], o);
+          unsigned long long* slot = kOne ? &s_keys[lt] : cl.map_shared_rank(&s_keys[lt], o);
           const unsigned long long prev = atomicCAS(slot, 0ULL, word);
           if (prev == 0ULL) break;
           if ((prev >> 16) == tag) {
@@ -661,11 +671,11 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     }
     mark(5);
     if (g.trace && tid == 0 && me < 16) g.trace[32 + me] = globaltimer_ns();  // this CTA's P2 end
-    cl_sync();  // B3: table final
+    cl_sync<kOne>();  // B3: table final
     mark(6);
     auto slot_at = [&](uint32_t t) -> unsigned long long {
       const uint32_t o = t / tsl;
-      return *cl.map_shared_rank(&s_keys[t - o * tsl], o);
+      return kOne ? s_keys[t] : *cl.map_shared_rank(&s_keys[t - o * tsl], o);
     };
 
     // ---- P3: representatives (table lookups), inductive verification, lcp ----
@@ -709,13 +719,22 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
         if (r == static_cast<uint32_t>(i)) {
           mine = static_cast<int32_t>(di);
         } else {
-          // the representative's sequence, token and position come from this CTA's copy of
-          // cu and from global memory (L1/L2): the representatives of a shared prefix all live
-          // in one CTA, whose shared memory would otherwise serve every such lookup (C2 18.3 ->
-          // 17.4 us, C3 36.0 -> 34.3 us per launch)
-          sr = find_seq(s_cu, nseq, r);
+          // a representative in another CTA: its sequence from this CTA's copy of cu, its
+          // token and position from global memory (L1/L2) -- the representatives of a shared
+          // prefix all live in one CTA, whose shared memory would otherwise serve every such
+          // lookup (C2 18.3 -> 17.4 us, C3 36.0 -> 34.3 us per launch)
+          uint32_t rtok, rpos;
+          if constexpr (kOne) {  // one CTA: plain shared-memory loads
+            sr = s_seg[r];
+            rtok = s_tok[r];
+            rpos = s_pos[r];
+          } else {
+            sr = find_seq(s_cu, nseq, r);
+            rtok = __ldg(a.tok + r);
+            rpos = __ldg(a.pos + r);
+          }
           const int64_t sst = s_cu[sr];
-          bool ok = (__ldg(a.tok + r) == s_tok[j]) && (__ldg(a.pos + r) == s_pos[j]) &&
+          bool ok = (rtok == s_tok[j]) && (rpos == s_pos[j]) &&
                     (static_cast<int64_t>(r) - sst == di);
           if (ok && di > 0) ok = (P_at(i - 1) - pst1) == (P_at(static_cast<int64_t>(r) - 1) - P_at(sst - 1));
           if (!ok) fail = 1;
@@ -728,12 +747,12 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
       const unsigned grp = __match_any_sync(0xffffffffu, si);
       const int32_t mn = __reduce_min_sync(grp, mine);
       if (live && mn != INT_MAX && (threadIdx.x & 31) == __ffs(grp) - 1)
-        atomicMin(cl.map_shared_rank(&s_lcp[si], 0), mn);
+        atomicMin(kOne ? &s_lcp[si] : cl.map_shared_rank(&s_lcp[si], 0), mn);
     }
     if (__syncthreads_or(fail) && tid == 0) atomicOr(cl.map_shared_rank(&s_flags[1 + attempt], 0), 1u);
     mark(7);
     if (g.trace && tid == 0 && me < 16) g.trace[48 + me] = globaltimer_ns();  // this CTA's P3 end
-    cl_sync();  // B4: verification and lcp final
+    cl_sync<kOne>();  // B4: verification and lcp final
     mark(8);
     if (*reinterpret_cast<volatile uint32_t*>(cl.map_shared_rank(&s_flags[1 + attempt], 0)) != 0) continue;
 
@@ -742,7 +761,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
       for (int64_t q = tid; q < nseq; q += kSmThreads) s_lcp[q] = *cl.map_shared_rank(&s_lcp[q], 0);
     __syncthreads();
     // done with every other CTA's shared memory: let them leave once P5 is done
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if constexpr (!kOne) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     {
       uint64_t carry = 0;
       uint32_t vmax = 0;  // longest compact suffix (info[3] = max_q)
@@ -795,7 +814,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
       }
     }
     mark(10);
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if constexpr (!kOne) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     mark(11);
     return;
   }
@@ -805,7 +824,7 @@ __global__ void __launch_bounds__(kSmThreads, 1) plan_build_smem_kernel(PlanArgs
     a.info[2] = kMaxAttempts;
     a.info[3] = 0;
   }
-  cl_sync();
+  cl_sync<kOne>();
 }
 
 // Shared-memory geometry of the cluster planner for (n, nseq) on `ctas` CTAs; false
@@ -843,9 +862,11 @@ int sm_cluster_max() {
   static int cached = -1;
   if (cached < 0) {
     cached = 0;
-    auto kern = plan_build_smem_kernel;
+    auto kern = plan_build_smem_kernel<false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmBudget)) !=
-        cudaSuccess) {
+            cudaSuccess ||
+        cudaFuncSetAttribute(plan_build_smem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmBudget)) != cudaSuccess) {
       cudaGetLastError();
       return cached;
     }
@@ -1015,7 +1036,8 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
       attr.val.clusterDim.z = 1;
       cfg.attrs = &attr;
       cfg.numAttrs = 1;
-      RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, plan_build_smem_kernel, a, g));
+      RDX_CUDA_TRY(cudaLaunchKernelEx(&cfg, ctas == 1 ? plan_build_smem_kernel<true> : plan_build_smem_kernel<false>,
+                                      a, g));
       return RDX_OK;
     }
   }
