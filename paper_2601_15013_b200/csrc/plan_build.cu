@@ -180,28 +180,35 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
   }
 
   // ---- validation of cu (device-side mirror of ragged.validate_batch) ----
-  // bit0 start!=0, bit1 decrease, bit2 empty, bit3 end!=n
-  if (gtid == 0) {
-    s.flags[kMaxAttempts] = 0;
+  // bit0 start!=0, bit1 decrease, bit2 empty, bit3 end!=n.  With cu staged in shared
+  // memory every block checks all of it itself (no grid barrier); otherwise the blocks
+  // split the check and meet at two grid barriers.  The attempt flags are cleared here
+  // and first set in P3, three grid barriers later.
+  const bool staged = nseq + 1 <= kSmemCu;
+  if (!staged && gtid == 0) s.flags[kMaxAttempts] = 0;
+  if (gtid == 0)
     for (int t = 0; t < kMaxAttempts; ++t) s.flags[t] = 0;
-  }
-  grid.sync();
+  if (!staged) grid.sync();
   {
+    __shared__ uint32_t s_bits;
+    if (threadIdx.x == 0) s_bits = 0;
+    __syncthreads();
     uint32_t bits = 0;
-    if (gtid == 0) {
+    if (staged ? threadIdx.x == 0 : gtid == 0) {
       if (cu[0] != 0) bits |= 1u;
       if (cu[nseq] != n) bits |= 8u;
     }
-    for (int64_t q = gtid; q < nseq; q += nthreads) {
+    const int64_t q0 = staged ? threadIdx.x : gtid, qs = staged ? static_cast<int64_t>(blockDim.x) : nthreads;
+    for (int64_t q = q0; q < nseq; q += qs) {
       const int64_t d = cu[q + 1] - cu[q];
       if (d < 0) bits |= 2u;
       if (d == 0 && !(a.flags & RDX_PLAN_ALLOW_EMPTY)) bits |= 4u;
     }
-    if (bits) atomicOr(&s.flags[kMaxAttempts], bits);
-  }
-  grid.sync();
-  {
-    const uint32_t bits = *((volatile uint32_t*)&s.flags[kMaxAttempts]);
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (bits && (threadIdx.x & 31) == 0) atomicOr(staged ? &s_bits : &s.flags[kMaxAttempts], bits);
+    if (staged) __syncthreads();
+    else grid.sync();
+    bits = staged ? s_bits : *((volatile uint32_t*)&s.flags[kMaxAttempts]);
     if (bits) {
       if (gtid == 0) {
         uint32_t st = (bits & 1u) ? RDX_ERR_BOUNDARY_MISMATCH
