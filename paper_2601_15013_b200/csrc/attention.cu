@@ -705,8 +705,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       auto issue_PV = [&](int h, int nkt_h, int j, uint32_t tile) {
         int& o_cnt = h ? o_cnt1 : o_cnt0;
         const int s_cnt = h ? s_cnt1 : s_cnt0;
-        RDX_TWAIT(&p_full[2 * h], (s_cnt - 1) & 1, st_p);  // P_h(j) published (S_h(j) was the last S of h)
-        if (lane == 0) RDX_EV(1, 2, h * 16 + j);  // MMA: P_h(j) seen
+        // P_h(j) is published in two halves (keys [0, BKT/2) on p_full[2h+1], the rest on
+        // p_full[2h]): the first half's MMAs run while the softmax exponentiates the second.
+        // Same K = 16 MMA sequence into O as one batch, so the same bits.
+        RDX_TWAIT(&p_full[2 * h + 1], (s_cnt - 1) & 1, st_p);
+        if (lane == 0) RDX_EV(1, 2, h * 16 + j);  // MMA: P_h(j) first half seen
         if (j == 0 && o_cnt > 0) RDX_TWAIT(&o_free[h], (o_cnt - 1) & 1, st_o);
         if (!a.use_tma) fence_proxy_async_smem();
         tc_fence_after();
@@ -715,8 +718,13 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         const uint64_t vd = sdesc(va, BKT * 128, 1024);
         const long long st_i0 = RDX_STATS_ON ? clock64() : 0;
 #pragma unroll
-        for (int kk = 0; kk < BKT / 16; ++kk)
+        for (int kk = 0; kk < BKT / 32; ++kk)
           umma_ts_elect(o, pa + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+        RDX_TWAIT(&p_full[2 * h], (s_cnt - 1) & 1, st_p);  // second half
+        tc_fence_after();
+#pragma unroll
+        for (int kk = BKT / 32; kk < BKT / 16; ++kk)
+          umma_ts_elect(o, pa + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, 1u);
         if (RDX_STATS_ON) st_iss += clock64() - st_i0;
         if (j == nkt_h - 1) {
           commit_elect(&o_full[h]);
@@ -1060,6 +1068,11 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 #pragma unroll
             for (int e = 0; e < 16; ++e) pw[e] = 0u;
             tmem_st16u(s_cur + c / 2, pw);
+            if (!DB && c == BKT / 2 - 32) {  // first half of P_h(j) complete (see below)
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(&p_full[2 * h + 1]);
+            }
             continue;
           }
 #pragma unroll
@@ -1079,6 +1092,12 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
             pw[e >> 1] = pack_bf16x2(p0, p1);
           }
           tmem_st16u(s_cur + c / 2, pw);  // P over the first BKT / 2 columns of S_h
+          if (!DB && c == BKT / 2 - 32) {
+            // first half of P_h(j) complete: its PV MMAs may start (p_full[2h+1])
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&p_full[2 * h + 1]);
+          }
         }
         {
           float s0, s1;
