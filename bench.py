@@ -191,6 +191,14 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return
+        # nvidia-smi needs ~0.1-0.3 s to print its first sample; a short timed region (C2: ~0.15 s)
+        # could end before that, so wait for the first (pre-region, discarded) sample
+        import select
+
+        ready, _, _ = select.select([self.proc.stdout], [], [], 5.0)
+        if ready:
+            self.proc.stdout.readline()
 
     def stop(self):
         if self.proc is None:
