@@ -85,6 +85,7 @@ struct Tile {
   static constexpr int SMEM = RING_OFF + kRing * kUnitWords * 4 + 2 * kRing * 8;
   static_assert(SMEM <= 232448, "shared memory budget");
   static constexpr uint32_t IDESC_S = umma_idesc_bf16(BQ, BKT);
+  static constexpr uint32_t IDESC_S_HALF = umma_idesc_bf16(BQ, BKT / 2);  // a short last key tile
   static constexpr uint32_t IDESC_PV = umma_idesc_bf16(BQ, HDP) | (1u << 16);  // B (V) MN-major
 };
 
@@ -678,7 +679,10 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
       int q_cnt0 = 0, q_cnt1 = 0;  // Q tiles consumed per h
       uint32_t gt = 0;             // global key-tile counter (K at seq 2gt, V at 2gt+1)
 
-      auto issue_S = [&](int h, int nkt_h, int j, uint32_t tile) {
+      // half: every row of the query tile sees fewer than BKT/2 keys of this tile (a short
+      // last tile): S with N = BKT/2 and only the first half of PV (the rest of P is zero).
+      // S columns the softmax never reads and PV terms that are all exactly zero: same O.
+      auto issue_S = [&](int h, int nkt_h, int j, uint32_t tile, bool half = false) {
         int& q_cnt = h ? q_cnt1 : q_cnt0;
         const int qb = q_cnt % NQB;
         if (j == 0) RDX_TWAIT(&q_full[h * NQB + qb], (q_cnt / NQB) & 1, st_q);
@@ -692,7 +696,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 #pragma unroll
         for (int kk = 0; kk < HDP / 16; ++kk)
           umma_ss_elect(sacc, qd + (((kk >> 2) * (BQ * 128) + (kk & 3) * 32) >> 4),
-                        kd + (((kk >> 2) * (BKT * 128) + (kk & 3) * 32) >> 4), T::IDESC_S, kk > 0 ? 1u : 0u);
+                        kd + (((kk >> 2) * (BKT * 128) + (kk & 3) * 32) >> 4), half ? T::IDESC_S_HALF : T::IDESC_S,
+                        kk > 0 ? 1u : 0u);
         commit_elect(&s_full[2 * h]);
         if (lane == 0) RDX_EV(1, 1, h * 16 + j);  // MMA: S_h(j) issued
         if (RDX_STATS_ON) st_iss += clock64() - st_i0;
@@ -702,7 +707,7 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           ++q_cnt;
         }
       };
-      auto issue_PV = [&](int h, int nkt_h, int j, uint32_t tile) {
+      auto issue_PV = [&](int h, int nkt_h, int j, uint32_t tile, bool half = false) {
         int& o_cnt = h ? o_cnt1 : o_cnt0;
         const int s_cnt = h ? s_cnt1 : s_cnt0;
         // P_h(j) is published in two halves (keys [0, BKT/2) on p_full[2h+1], the rest on
@@ -720,11 +725,13 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
 #pragma unroll
         for (int kk = 0; kk < BKT / 32; ++kk)
           umma_ts_elect(o, pa + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
-        RDX_TWAIT(&p_full[2 * h], (s_cnt - 1) & 1, st_p);  // second half
+        RDX_TWAIT(&p_full[2 * h], (s_cnt - 1) & 1, st_p);  // second half (waited even when unused: parity)
         tc_fence_after();
+        if (!half) {
 #pragma unroll
-        for (int kk = BKT / 32; kk < BKT / 16; ++kk)
-          umma_ts_elect(o, pa + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, 1u);
+          for (int kk = BKT / 32; kk < BKT / 16; ++kk)
+            umma_ts_elect(o, pa + kk * 8, vd + ((kk * 2048) >> 4), T::IDESC_PV, 1u);
+        }
         if (RDX_STATS_ON) st_iss += clock64() - st_i0;
         if (j == nkt_h - 1) {
           commit_elect(&o_full[h]);
@@ -855,39 +862,46 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
         }
       } else {
         Unit tmp, pre;
+        // keys visible to the last row of query tile h of a unit: tile j is short when
+        // khi - j * BKT <= BKT / 2 (only 128-key tiles; the 64-key ones never split)
+        auto khi = [&](const Unit& u, int h) { return u.lcp + min(u.qlen, (u.mb0 + h + 1) * a.qpt); };
+        auto short_tile = [&](int kh, int j) { return BKT == 128 && kh - j * BKT <= BKT / 2; };
         int kcur = 0;  // ring entry of the current unit
         int ucur = ring_unit(ring, 0, tmp, lane);
         int c0 = tmp.nkt0, c1 = tmp.nkt1, call = max(tmp.nkt0, tmp.nkt1);  // key tiles of the current unit
+        int ck0 = khi(tmp, 0), ck1 = khi(tmp, 1);
         int jcur = 0;
         int upre = a.n_units;  // the unit after the current one, fetched while S/softmax of this one run
         if (ucur < a.n_units) {
           wait_tile(2 * gt);
-          if (c0 > 0) issue_S(0, c0, 0, gt);
-          if (c1 > 0) issue_S(1, c1, 0, gt);
+          if (c0 > 0) issue_S(0, c0, 0, gt, short_tile(ck0, 0));
+          if (c1 > 0) issue_S(1, c1, 0, gt, short_tile(ck1, 0));
           commit_elect(&t_free[(2 * gt) % NSLOT]);  // both S of tile 0 issued: K slot free when done
           upre = ring_unit(ring, kcur + 1, pre, lane);
         }
         while (ucur < a.n_units) {
-          int unxt = ucur, jnxt = jcur + 1, n0 = c0, n1 = c1, nall = call;
+          int unxt = ucur, jnxt = jcur + 1, n0 = c0, n1 = c1, nall = call, nk0 = ck0, nk1 = ck1;
           if (jnxt >= call) {
             unxt = upre;
             jnxt = 0;
             n0 = pre.nkt0;
             n1 = pre.nkt1;
             nall = max(pre.nkt0, pre.nkt1);
+            nk0 = khi(pre, 0);
+            nk1 = khi(pre, 1);
           }
           const bool has_next = unxt < a.n_units;
           const uint32_t tnext = gt + 1;
           wait_tile(2 * gt + 1);  // V(cur)
-          if (jcur < c0) issue_PV(0, c0, jcur, gt);
+          if (jcur < c0) issue_PV(0, c0, jcur, gt, short_tile(ck0, jcur));
           if (has_next) {
             wait_tile(2 * tnext);  // K(next)
-            if (jnxt < n0) issue_S(0, n0, jnxt, tnext);
+            if (jnxt < n0) issue_S(0, n0, jnxt, tnext, short_tile(nk0, jnxt));
           }
-          if (jcur < c1) issue_PV(1, c1, jcur, gt);
+          if (jcur < c1) issue_PV(1, c1, jcur, gt, short_tile(ck1, jcur));
           commit_elect(&t_free[(2 * gt + 1) % NSLOT]);  // V(cur) consumed by both PV
           if (has_next) {
-            if (jnxt < n1) issue_S(1, n1, jnxt, tnext);
+            if (jnxt < n1) issue_S(1, n1, jnxt, tnext, short_tile(nk1, jnxt));
             commit_elect(&t_free[(2 * tnext) % NSLOT]);  // K(next) consumed by both S
           }
           const bool switched = unxt != ucur;
@@ -895,6 +909,8 @@ attention_kernel(const __grid_constant__ CUtensorMap map_kv, const __grid_consta
           jcur = jnxt;
           c0 = n0;
           c1 = n1;
+          ck0 = nk0;
+          ck1 = nk1;
           call = nall;
           ++gt;
           // new current unit: its S tiles are issued; the entry after it is already in the ring
