@@ -350,34 +350,46 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
     grid.sync();
     if (*((volatile uint32_t*)&s.flags[attempt]) != 0) continue;  // re-run with a new seed
 
-    // ---- P4: cu_q (block 0) ----
-    if (blockIdx.x == 0) {
+    // ---- P4: cu_q.  Few sequences (cu staged, <= 1024): every block scans them into its
+    // own shared copy (no grid barrier before P5); else block 0 alone, then a barrier ----
+    const bool local_cuq = staged && nseq <= 1024;
+    int32_t* s_cuq = reinterpret_cast<int32_t*>(s_cu + nseq + 1);  // staged layout only
+    if (local_cuq || blockIdx.x == 0) {
       uint64_t carry = 0;
       uint32_t vmax = 0;  // longest compact suffix (info[3] = max_q)
       for (int64_t base = 0; base < nseq; base += blockDim.x) {
         const int64_t q = base + threadIdx.x;
-        const uint64_t v = q < nseq ? static_cast<uint64_t>(cu[q + 1] - cu[q] - s.lcp[q]) : 0;
+        const int32_t lq = q < nseq ? s.lcp[q] : 0;
+        const uint64_t v = q < nseq ? static_cast<uint64_t>(cu[q + 1] - cu[q] - lq) : 0;
         vmax = max(vmax, static_cast<uint32_t>(v));
         uint64_t tile_total;
         const uint64_t ex = block_exclusive_scan_u64(v, warp_tot, tile_total);
         if (q < nseq) {
-          a.cu_q[q] = static_cast<int32_t>(carry + ex);
-          if (a.lcp_out) a.lcp_out[q] = s.lcp[q];
+          if (local_cuq) s_cuq[q] = static_cast<int32_t>(carry + ex);
+          if (blockIdx.x == 0) {
+            a.cu_q[q] = static_cast<int32_t>(carry + ex);
+            if (a.lcp_out) a.lcp_out[q] = lq;
+          }
         }
         carry += tile_total;
       }
-      vmax = __reduce_max_sync(0xffffffffu, vmax);
-      if ((threadIdx.x & 31) == 0) atomicMax(&s_vmax, vmax);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        a.cu_q[nseq] = static_cast<int32_t>(carry);
-        a.info[0] = static_cast<uint32_t>(carry);
-        a.info[1] = RDX_OK;
-        a.info[2] = static_cast<uint32_t>(attempt + 1);
-        a.info[3] = s_vmax;
+      if (local_cuq && threadIdx.x == 0) s_cuq[nseq] = static_cast<int32_t>(carry);
+      if (blockIdx.x != 0) {
+        __syncthreads();  // s_cuq complete
+      } else {
+        vmax = __reduce_max_sync(0xffffffffu, vmax);
+        if ((threadIdx.x & 31) == 0) atomicMax(&s_vmax, vmax);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          a.cu_q[nseq] = static_cast<int32_t>(carry);
+          a.info[0] = static_cast<uint32_t>(carry);
+          a.info[1] = RDX_OK;
+          a.info[2] = static_cast<uint32_t>(attempt + 1);
+          a.info[3] = s_vmax;
+        }
       }
     }
-    grid.sync();
+    if (!local_cuq) grid.sync();
 
     // ---- P5: emit ----
     for (int64_t i = gtid; i < n; i += nthreads) {
@@ -385,7 +397,7 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
       const uint32_t si = s.seg[i];
       const int64_t depth = i - cu[si];
       const uint32_t sr = (r == static_cast<uint32_t>(i)) ? si : s.seg[r];
-      const uint32_t cid = static_cast<uint32_t>(a.cu_q[sr] + depth - s.lcp[sr]);
+      const uint32_t cid = static_cast<uint32_t>((local_cuq ? s_cuq[sr] : a.cu_q[sr]) + depth - s.lcp[sr]);
       a.scatter[i] = cid;
       if (r == static_cast<uint32_t>(i)) {
         a.gather[cid] = static_cast<uint32_t>(i);
@@ -1022,7 +1034,9 @@ extern "C" int rdx_plan_build(const uint32_t* tok, const uint32_t* pos, const in
   if (want < 1) want = 1;
   const int grid = static_cast<int>(want < mg ? want : mg);
   void* params[] = {&a, &s};
-  const size_t dsmem = n_seqs + 1 <= kSmemCu ? static_cast<size_t>(8 * (n_seqs + 1)) : 0;
+  // staged cu (int64) + the per-block cu_q copy (int32) of the few-sequence P4 (<= 1024
+  // sequences: at most 32 KB either way, under the 48 KB default)
+  const size_t dsmem = n_seqs + 1 <= kSmemCu ? static_cast<size_t>((n_seqs <= 1024 ? 12 : 8) * (n_seqs + 1)) : 0;
   // up to 16 x 4096 tokens: the cluster-resident planner (everything in shared memory)
   if (sm_planner_enabled()) {
     const int cmax = sm_cluster_max();
