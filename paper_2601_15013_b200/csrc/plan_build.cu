@@ -421,9 +421,11 @@ plan_build_kernel(PlanArgs a, PlanScratch s) {
 // slice of the open-addressing table; the cross-token lookups (P at a sequence
 // start and at rep-1, the table itself) are distributed-shared-memory accesses
 // (~200 cycles) instead of L2 round trips (the representative's tok/pos are read
-// from global memory: a shared prefix's representatives all sit in one CTA), and the phases are separated by 4 hardware cluster barriers (the
-// cooperative grid version has 4-7 grid barriers and L2 traffic in every phase).
-// Same algorithm, same seeds, same outputs as plan_build_kernel.
+// from global memory: a shared prefix's representatives all sit in one CTA), and
+// the phases are separated by 4 hardware cluster barriers (the cooperative grid
+// version has 4-7 grid barriers and L2 traffic in every phase).  A hash slot is
+// one 64-bit word: 48-bit key tag over the 16-bit index of the path's first token.
+// Same algorithm and outputs as plan_build_kernel.
 constexpr int kSmThreads = 1024;
 constexpr int kSmWarps = kSmThreads / 32;
 constexpr int kSmPerThread = 4;                               // tokens per thread at most
